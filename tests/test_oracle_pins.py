@@ -1,0 +1,330 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix
+(not against itself).  CPU only.  See DESIGN.md §3 for the list and citations."""
+from fractions import Fraction
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import gamegen
+import oracle
+
+
+# ----------------------------------------------------------------- structure
+TABLE7 = {  # PAPER.md Table 7: nodes, terminals, infosets
+    "kuhn": (58, 30, 12),
+    "kuhn3": (617, 312, 48),
+    "leduc": (9457, 5520, 936),
+    "liars_dice": (294883, 147420, 24576),
+}
+
+
+@pytest.mark.parametrize("name", sorted(TABLE7))
+def test_table7_counts(name):
+    d = gamegen.by_name(name)
+    assert (d.num_nodes, d.num_terminals, d.num_infosets) == TABLE7[name]
+
+
+def test_goofspiel_and_synthetic_counts():
+    d = gamegen.goofspiel()
+    assert (d.num_nodes, d.num_terminals, d.num_infosets) == (55731, 14400, 9948)
+    c = gamegen.synthetic_counts(40)
+    assert (c["V"], c["T"], c["H"], c["Q"], c["D"]) == (965153641, 916896000, 1206440, 24128800, 11)
+    for n in (1, 2, 3):
+        d = gamegen.synthetic(n_types=n)
+        c = gamegen.synthetic_counts(n)
+        assert (d.num_nodes, d.num_terminals, d.num_infosets) == (c["V"], c["T"], c["H"])
+
+
+def _sparsities(d):
+    """PAPER.md Table 8 quantities from the game arrays."""
+    V = d.num_nodes
+    o = oracle.Oracle(d)
+    Q, H = o.Q, o.H
+    par = d.parent
+    player_children = int(np.sum((par >= 0) & (d.player[np.maximum(par, 0)] >= 1)))
+    depth = np.zeros(V, dtype=np.int64)
+    order = np.argsort(par)  # parents before children is not guaranteed: iterate
+    changed = True
+    while changed:
+        nd = np.where(par >= 0, depth[np.maximum(par, 0)] + 1, 0)
+        changed = not np.array_equal(nd, depth)
+        depth = nd
+    D = int(depth.max())
+    s_mqv = 1 - player_children / (Q * V)
+    s_mhq = 1 - Q / (H * Q)
+    s_g = 1 - (V - 1) / (V * V)
+    s_l = np.mean([1 - np.sum(depth == l) / (V * V) for l in range(1, D + 1)])
+    return [round(100 * x, 1) for x in (s_mqv, s_mhq, s_l, s_g)], D
+
+
+def test_table8_kuhn_sparsities():
+    sp, D = _sparsities(gamegen.kuhn(2))
+    assert D == 5
+    assert sp == [96.6, 91.7, 99.7, 98.3]
+
+
+def test_table8_kuhn3_sparsities():
+    sp, _ = _sparsities(gamegen.kuhn(3))
+    assert sp[0] == 99.0 and sp[1] == 97.9 and sp[3] == 99.8  # P:718 ("99.9+" for L)
+    assert sp[2] >= 99.9
+
+
+# ------------------------------------------------------- exact accumulation
+def test_slice_sum_order_free_and_accurate():
+    rng = np.random.default_rng(0)
+    for E in (1, 2, 3, 7):
+        x = rng.uniform(-1, 1, size=2000) * 2.0 ** (E - 1) * rng.choice([1, 1e-3, 1e-9, 1e-17], size=2000)
+        acc, dec = oracle.slice_sum(x, E)
+        for s in range(3):
+            acc2, dec2 = oracle.slice_sum(rng.permutation(x), E)
+            assert np.array_equal(acc, acc2) and dec == dec2
+        exact = sum(Fraction(float(v)) for v in x)
+        bound = len(x) * Fraction(2) ** (E - 121) + abs(exact) * Fraction(2) ** -51 + Fraction(2) ** (E - 200)
+        assert abs(Fraction(dec) - exact) <= bound
+        accn, decn = oracle.slice_sum(-x, E)
+        assert np.array_equal(accn, -acc) and decn == -dec
+
+
+def test_slice_sum_on_grid_values_exact():
+    x = np.array([0.5, 0.25, -0.125, 1.5, 3.0 * 2.0 ** -100])
+    acc, dec = oracle.slice_sum(x, 2)
+    assert dec == float(sum(Fraction(v) for v in x))
+
+
+# ------------------------------------------------------------ closed forms
+def _kuhn_equilibrium(d, alpha):
+    """Kuhn equilibrium family (alpha in [0, 1/3]); returns sigma in qbase order."""
+    keys = d.meta["infoset_keys"]
+    bet = {}
+    J, Qc, K = 0, 1, 2
+    bet[(1, (J, ()))] = alpha
+    bet[(1, (Qc, ()))] = 0.0
+    bet[(1, (K, ()))] = 3 * alpha
+    bet[(1, (J, (0, 1)))] = 0.0
+    bet[(1, (Qc, (0, 1)))] = alpha + 1.0 / 3.0
+    bet[(1, (K, (0, 1)))] = 1.0
+    bet[(2, (J, (0,)))] = 1.0 / 3.0
+    bet[(2, (J, (1,)))] = 0.0
+    bet[(2, (Qc, (0,)))] = 0.0
+    bet[(2, (Qc, (1,)))] = 1.0 / 3.0
+    bet[(2, (K, (0,)))] = 1.0
+    bet[(2, (K, (1,)))] = 1.0
+    s = np.zeros(2 * len(keys))
+    for h, k in enumerate(keys):
+        s[2 * h + 1] = bet[k]
+        s[2 * h] = 1.0 - bet[k]
+    return s
+
+
+@pytest.mark.parametrize("alpha", [0.0, 1.0 / 6.0, 1.0 / 3.0])
+def test_kuhn_equilibrium_value(alpha):
+    d = gamegen.kuhn(2)
+    o = oracle.Oracle(d)
+    s = _kuhn_equilibrium(d, alpha)
+    ev = o.expected_values(s)
+    assert abs(ev[0] + 1.0 / 18.0) <= 1e-15 and abs(ev[1] - 1.0 / 18.0) <= 1e-15
+    ex = o.exploitability(s)
+    assert abs(ex["nash_conv"]) <= 1e-15
+
+
+def test_kuhn_uniform_closed_forms():
+    o = oracle.Oracle(gamegen.kuhn(2))
+    assert np.allclose(o.expected_values("current"), [0.125, -0.125], rtol=0, atol=1e-15)
+    ex = o.exploitability("current")
+    assert abs(ex["br"][0] - 0.5) <= 1e-15 and abs(ex["br"][1] - 5.0 / 12.0) <= 1e-15
+    assert abs(ex["nash_conv"] - 11.0 / 12.0) <= 1e-15
+
+
+def test_chance_only_game_value_zero():
+    for P in (1, 2):
+        o = oracle.Oracle(gamegen.chance_pm1(P))
+        assert np.all(o.expected_values("current") == 0.0)
+
+
+def test_single_decision_regret_and_rm():
+    """payoffs (1, 0): r~ = (0.5, -0.5), sigma^(2) = (1, 0); sigma_bar(1) = sigma^(1)."""
+    o = oracle.Oracle(gamegen.single_decision()).run(1, 0)
+    st = o.state()
+    assert np.array_equal(st["regret"], [0.5, -0.5])
+    assert np.array_equal(st["sigma"], [1.0, 0.0])
+    assert np.array_equal(st["avg"], [0.5, 0.5])
+    o.run(1, 0)
+    assert np.array_equal(o.state()["sigma"], [1.0, 0.0])
+
+
+# ------------------------------------------------- brute force on tiny trees
+def _tree(d):
+    ch = [[] for _ in range(d.num_nodes)]
+    for v in np.argsort(d.action, kind="stable"):
+        p = d.parent[v]
+        if p >= 0:
+            ch[p].append(int(v))
+    for p in range(d.num_nodes):
+        ch[p].sort(key=lambda c: d.action[c])
+    root = int(np.nonzero(d.parent < 0)[0][0])
+    return ch, root
+
+
+def _pure_strategies(d, o, player):
+    hs = [h for h in range(o.H) if d.player[np.nonzero(d.infoset == h)[0][0]] == player]
+    n = [int(o.qbase[h + 1] - o.qbase[h]) for h in hs]
+    for choice in itertools.product(*[range(k) for k in n]):
+        yield hs, choice
+
+
+def test_best_response_equals_pure_strategy_enumeration():
+    """Brute-force BR (PAPER.md P:59 max over Sigma_j; pure strategies suffice)."""
+    d = gamegen.kuhn(2)
+    o = oracle.Oracle(d)
+    rng = np.random.default_rng(3)
+    profiles = [None]
+    for _ in range(4):
+        s = np.zeros(o.Q)
+        for h in range(o.H):
+            w = rng.uniform(0.05, 1, size=o.qbase[h + 1] - o.qbase[h])
+            s[o.qbase[h]:o.qbase[h + 1]] = w / w.sum()
+        profiles.append(s)
+    for prof in profiles:
+        base = o.current_strategy() if prof is None else prof
+        for pl in (1, 2):
+            best = -math.inf
+            for hs, choice in _pure_strategies(d, o, pl):
+                s = base.copy()
+                for h, a in zip(hs, choice):
+                    s[o.qbase[h]:o.qbase[h + 1]] = 0.0
+                    s[o.qbase[h] + a] = 1.0
+                best = max(best, o.expected_values(s)[pl - 1])
+            val, _ = o.best_response(pl, base)
+            assert abs(val - best) <= 1e-12
+            assert val >= o.expected_values(base)[pl - 1] - 1e-15
+
+
+def _eq7_bruteforce(d, o, sigma):
+    """r~(h,a) from the LITERAL Eq 6/7 with the override profile
+    sigma|h->a, pi_check by Eq 2 and pi_hat by Eq 4 -- plain Python."""
+    ch, root = _tree(d)
+    P = d.num_players
+    qb = o.qbase
+
+    def prob(v, a, prof):
+        pl = d.player[v]
+        c = ch[v][a]
+        return d.chance_prob[c] if pl == 0 else prof[qb[d.infoset[v]] + a]
+
+    def value(v, prof):
+        if d.player[v] < 0:
+            return d.utility[v].copy()
+        return sum(prob(v, a, prof) * value(c, prof) for a, c in enumerate(ch[v]))
+
+    pc = {}
+    ph = {}
+
+    def reach(v, rc, rh):
+        pc[v], ph[v] = rc, rh
+        if d.player[v] < 0:
+            return
+        pl = d.player[v]
+        for a, c in enumerate(ch[v]):
+            s = prob(v, a, sigma)
+            reach(c, [rc[j] * (s if pl != j + 1 else 1.0) for j in range(P)],
+                  [rh[j] * (s if pl == j + 1 else 1.0) for j in range(P)])
+
+    reach(root, [1.0] * P, [1.0] * P)
+    rt = np.zeros(o.Q)
+    pibar = np.zeros(o.H)
+    for h in range(o.H):
+        members = [int(v) for v in np.nonzero((d.infoset == h) & (d.player >= 1))[0]]
+        i = int(d.player[members[0]])
+        n = int(qb[h + 1] - qb[h])
+        pibar[h] = sum(ph[m][i - 1] for m in members)
+        base = sum(pc[m][i - 1] * value(m, sigma)[i - 1] for m in members)
+        for a in range(n):
+            over = sigma.copy()
+            over[qb[h]:qb[h + 1]] = 0.0
+            over[qb[h] + a] = 1.0
+            rt[qb[h] + a] = sum(pc[m][i - 1] * value(m, over)[i - 1] for m in members) - base
+    return rt, pibar
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 5, 8])
+def test_iteration_one_matches_literal_eq7_eq5_eq9(seed):
+    d = gamegen.random_game(seed, num_players=2 + seed % 2, max_nodes=300)
+    o = oracle.Oracle(d)
+    sigma1 = o.current_strategy()
+    rt, pibar = _eq7_bruteforce(d, o, sigma1)
+    o.run(1, 0)
+    st = o.state()
+    assert np.allclose(st["regret"], rt, rtol=0, atol=1e-13)
+    assert np.allclose(st["sden"], pibar, rtol=0, atol=1e-13)      # w_1 = 1: S_den = pi_bar
+    assert np.array_equal(st["avg"], sigma1)                       # sigma_bar(1) = sigma^(1)
+    # Eq 9 applied to the literal regrets
+    for h in range(o.H):
+        r = rt[o.qbase[h]:o.qbase[h + 1]]
+        pos = np.maximum(r, 0)
+        want = pos / pos.sum() if pos.sum() > 1e-12 else np.full(len(r), 1.0 / len(r))
+        assert np.allclose(st["sigma"][o.qbase[h]:o.qbase[h + 1]], want, atol=1e-9)
+
+
+def test_cfr_plus_linear_weights_and_rm_plus():
+    """Reading Q6: R <- max(R + r~, 0); S_num += t * pi_bar * sigma (w_t = t)."""
+    d = gamegen.random_game(4, max_nodes=300)
+    o = oracle.Oracle(d).run(1, 1)
+    st1 = o.state()
+    sig2 = st1["sigma"].copy()
+    rt2, pibar2 = _eq7_bruteforce(d, o, sig2)
+    o.run(1, 1)
+    st2 = o.state()
+    assert np.all(st2["regret"] >= 0)
+    assert np.allclose(st2["regret"], np.maximum(st1["regret"] + rt2, 0), atol=1e-12)
+    want_sden = st1["sden"] + 2 * pibar2
+    assert np.allclose(st2["sden"], want_sden, atol=1e-12)
+    h_of_q = np.repeat(np.arange(o.H), np.diff(o.qbase))
+    assert np.allclose(st2["snum"], st1["snum"] + 2 * pibar2[h_of_q] * sig2, atol=1e-12)
+
+
+# ------------------------------------------------------------- convergence
+def test_kuhn_1000_value_and_2eps_bound():
+    """BASELINE configs[0]: EV1 -> -1/18; |EV1 - v*| <= NashConv."""
+    o = oracle.Oracle(gamegen.kuhn(2)).run(1000, 0)
+    ev = o.expected_values()
+    nc = o.exploitability()["nash_conv"]
+    assert abs(ev[0] + 1.0 / 18.0) <= 1e-4
+    assert abs(ev[0] + 1.0 / 18.0) <= nc
+    assert ev[0] + ev[1] == 0.0
+
+
+@pytest.mark.parametrize("game,variant", [("kuhn", 0), ("kuhn", 1), ("kuhn3", 0)])
+def test_checkpoint_monotone_exploitability(game, variant):
+    """SPEC S:665 / PAPER Fig 3: NashConv of sigma_bar falls at checkpoints."""
+    o = oracle.Oracle(gamegen.by_name(game))
+    vals = []
+    done = 0
+    for T in (10, 100, 1000, 5000):
+        o.run(T - done, variant)
+        done = T
+        vals.append(o.exploitability()["nash_conv"])
+    assert all(b < a for a, b in zip(vals, vals[1:])), vals
+    assert vals[-1] < 1e-2
+
+
+def test_f32_vs_f64_kuhn():
+    a = oracle.Oracle(gamegen.kuhn(2), 64).run(1000, 0).average_strategy()
+    b = oracle.Oracle(gamegen.kuhn(2), 32).run(1000, 0).average_strategy()
+    assert np.max(np.abs(a - b)) <= 1e-3
+    assert not np.array_equal(a, b)
+
+
+def test_leduc_cfr_plus_value_bound():
+    """Leduc value ~ -0.0856 (literature, not in PAPER.md): |EV1 - v| <= NashConv."""
+    o = oracle.Oracle(gamegen.leduc()).run(500, 1)
+    ex = o.exploitability()
+    assert abs(ex["ev"][0] + 0.0856) <= ex["nash_conv"]
+    assert ex["nash_conv"] < 0.05
+
+
+def test_goofspiel_symmetric_value_bound():
+    o = oracle.Oracle(gamegen.goofspiel()).run(100, 1)
+    ex = o.exploitability()
+    assert abs(ex["ev"][0]) <= ex["nash_conv"]
