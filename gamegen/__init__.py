@@ -19,11 +19,11 @@ P:659-673).
 """
 from .desc import GameDesc, Builder
 from .games import kuhn, leduc, liars_dice, goofspiel, random_game, chance_pm1, single_decision, signal_game
-from .synthetic import synthetic, synthetic_counts
+from .synthetic_tree import synthetic, synthetic_numpy, synthetic_counts, DEFAULT_C
 
 __all__ = [
     "GameDesc", "Builder", "kuhn", "leduc", "liars_dice", "goofspiel", "random_game",
-    "chance_pm1", "single_decision", "signal_game", "synthetic", "synthetic_counts",
+    "chance_pm1", "single_decision", "signal_game", "synthetic", "synthetic_numpy", "synthetic_counts", "DEFAULT_C",
     "by_name",
 ]
 

@@ -11,6 +11,10 @@ row: 95 % terminals, ~0.1 % infosets per node).
 """
 from __future__ import annotations
 
+import ctypes
+import os
+import subprocess
+
 import numpy as np
 
 from .desc import GameDesc
@@ -55,7 +59,56 @@ def synthetic_counts(n_types: int = 40, b: int = 20, c: tuple = DEFAULT_C) -> di
                 D=2 + len(c) + 1, levels=[1, n_types] + [deals * x for x in n_all])
 
 
-def synthetic(n_types: int = 40, b: int = 20, c: tuple = DEFAULT_C, seed: int = 0) -> GameDesc:
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_CSRC = os.path.join(_HERE, "synthetic_gen.c")
+_CLIB = os.path.join(_HERE, "libsynthetic_gen.so")
+_clib = None
+
+
+def _load_c():
+    """gcc -O2 -fopenmp build of synthetic_gen.c (multi-threaded emitter)."""
+    global _clib
+    if _clib is None:
+        if not os.path.exists(_CLIB) or os.path.getmtime(_CLIB) < os.path.getmtime(_CSRC):
+            tmp = _CLIB + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", tmp, _CSRC])
+            os.replace(tmp, _CLIB)
+        L = ctypes.CDLL(_CLIB)
+        P = ctypes.c_void_p
+        L.synthetic_fill.argtypes = [ctypes.c_int64, ctypes.c_int64, P, ctypes.c_int64, ctypes.c_uint64,
+                                     P, P, P, P, P, P]
+        L.synthetic_fill.restype = ctypes.c_int
+        _clib = L
+    return _clib
+
+
+def synthetic(n_types: int = 40, b: int = 20, c: tuple = DEFAULT_C, seed: int = 0, fast: bool = True) -> GameDesc:
+    """The synthetic tree; `fast` uses the OpenMP C emitter (same arrays)."""
+    if fast:
+        return _synthetic_c(n_types, b, tuple(c), seed)
+    return synthetic_numpy(n_types, b, c, seed)
+
+
+def _synthetic_c(n_types, b, c, seed):
+    cnt = synthetic_counts(n_types, b, c)
+    V = cnt["V"]
+    parent = np.empty(V, dtype=np.int64)
+    player = np.empty(V, dtype=np.int32)
+    infoset = np.empty(V, dtype=np.int64)
+    action = np.empty(V, dtype=np.int32)
+    chance = np.empty(V, dtype=np.float64)
+    util = np.empty((V, 2), dtype=np.float64)
+    ca = np.asarray(c, dtype=np.int64)
+    p = lambda a: ctypes.c_void_p(a.ctypes.data)
+    rc = _load_c().synthetic_fill(n_types, b, p(ca), len(c), seed, p(parent), p(player), p(infoset), p(action),
+                                  p(chance), p(util))
+    if rc != 0:
+        raise ValueError("synthetic_fill failed")
+    return GameDesc(f"synthetic_n{n_types}", 2, parent, player, infoset, action, chance, util,
+                    dict(zero_sum=True, canonical=True, n_types=n_types, b=b, c=c, seed=seed, H=cnt["H"]))
+
+
+def synthetic_numpy(n_types: int = 40, b: int = 20, c: tuple = DEFAULT_C, seed: int = 0) -> GameDesc:
     c = tuple(c)
     n_all, n_dec = _public_shape(b, c)
     n = n_types

@@ -1,0 +1,194 @@
+/*
+ * cfr_b200.h -- C ABI of the B200-native CFR / CFR+ iteration (arXiv 2408.14778).
+ *
+ * The library runs whole counterfactual-regret-minimization iterations
+ * (§3.2: regret matching, level-by-level forward reach pass,
+ * level-by-level backward value pass, per-infoset aggregation, regret and
+ * average-strategy accumulation) as hand-written sm_100a CUDA kernels captured
+ * in a CUDA Graph.  Everything below is plain C: host or device pointers and
+ * sizes, no C++ or torch types.  No exception ever crosses this boundary; every
+ * call returns a cfr_status and, on failure, leaves a message in
+ * cfr_last_error() (thread-local).  A handle is not thread-safe; distinct
+ * handles are independent.
+ */
+#ifndef CFR_B200_H
+#define CFR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CFR_OK = 0,
+    CFR_ERR_INVALID_ARG = 1,   /* NULL pointer, bad size, bad enum value            */
+    CFR_ERR_INVALID_TREE = 2,  /* the game arrays violate Def. 2.1        */
+    CFR_ERR_UNSUPPORTED = 3,   /* e.g. device best response on an infoset spanning
+                                  several depths, or world_size > 1 without NCCL    */
+    CFR_ERR_CUDA = 4,          /* a CUDA runtime call failed (message has the name) */
+    CFR_ERR_NCCL = 5,          /* an NCCL call failed                               */
+    CFR_ERR_OOM = 6,           /* workspace smaller than cfr_solver_workspace_bytes */
+    CFR_ERR_NUMERICAL = 7      /* NaN/Inf in the regrets or strategy; message names
+                                  the first failing iteration          */
+} cfr_status;
+
+/* Human-readable name of a status code (static storage). */
+const char* cfr_status_string(cfr_status s);
+/* Message of the last failing call on this thread ("" if none). */
+const char* cfr_last_error(void);
+
+/* ------------------------------------------------------------------ game --
+ * A finite extensive-form game G = <T, H, f_h, A, f_a, I, f_i, sigma_0, u>
+ * (Def. 2.1) as flat, caller-owned HOST arrays of V entries
+ * each, in ANY node order (the library canonicalises: SURVEY.md Appendix B-1).
+ *
+ *   parent[v]      f_parents(v); -1 for the unique root v0.
+ *   player[v]      -1 terminal (v in T); 0 chance (nature i0); 1..P player i+.
+ *   infoset[v]     f_h(v) for player decision nodes, dense ids 0..H+-1 across all
+ *                  players; ignored (use -1) at chance and terminal nodes
+ *                  (reading Q13: sigma_0 is given per chance edge).
+ *   action[v]      f_a(v) = index of the incoming action, -1 at the root.  For
+ *                  every decision node d the children's actions are exactly
+ *                  0..|S(d)|-1 (the bijection f_{a,d}: S(d) -> A(f_h(d))),
+ *                  and |S(d)| = |A(h)| is shared by all nodes of an infoset.
+ *   chance_prob[v] sigma_0 of the edge INTO v when parent(v) is a chance node
+ *                  (P:35); ignored otherwise.  Each chance node's
+ *                  children must sum to 1 within 1e-12.
+ *   utility[v*P+i] u(v, i+1) at terminals, row-major [V][P]; ignored at
+ *                  decision nodes; must be finite.
+ *
+ * The library copies what it needs: the caller may free the arrays as soon as
+ * cfr_game_create returns.  Validation failures return CFR_ERR_INVALID_TREE
+ * with a message naming the offending node or infoset.  Limits: 1 <= P <= 16;
+ * at most 2^23 nodes per infoset (exact-accumulation headroom).
+ */
+typedef struct {
+    int64_t num_nodes;          /* V >= 1                    */
+    int32_t num_players;        /* P in [1, 16]              */
+    const int64_t* parent;
+    const int32_t* player;
+    const int64_t* infoset;
+    const int32_t* action;
+    const double* chance_prob;
+    const double* utility;      /* [V * P]                   */
+} cfr_game_desc;
+
+typedef struct cfr_game cfr_game;
+
+typedef struct {
+    int64_t num_nodes;          /* |V|                                           */
+    int64_t num_terminals;      /* |T|                                           */
+    int64_t num_decision;       /* |D| = chance + player decision nodes          */
+    int64_t num_chance;         /* chance decision nodes                         */
+    int64_t num_infosets;       /* |H+|                                          */
+    int64_t num_pairs;          /* |Q+| = sum_h |A(h)|                           */
+    int32_t num_players;        /* |I+|                                          */
+    int32_t depth;              /* D = max terminal depth                */
+    int64_t max_infoset_nodes;  /* largest infoset                               */
+    int32_t depth_homogeneous;  /* 1 if every infoset lies on one depth          */
+    int32_t zero_sum_2p;        /* 1 if P == 2 and u2 == -u1 bit-exactly (B-7)   */
+} cfr_game_info_t;
+
+cfr_status cfr_game_create(const cfr_game_desc* desc, cfr_game** out);
+void cfr_game_destroy(cfr_game* g);
+cfr_status cfr_game_info(const cfr_game* g, cfr_game_info_t* out);
+/* qbase[h] = sum_{h' < h} |A(h')| over the CALLER's infoset ids, [H+ + 1]; the
+ * (infoset, action) pair (h, a) is index qbase[h] + a in every strategy array. */
+cfr_status cfr_game_qbase(const cfr_game* g, int64_t* qbase);
+/* Canonical flattening (Appendix B-1): canon_of_input[V] maps each input node
+ * to its canonical BFS index; level_ptr[D + 2] delimits the depth levels.
+ * Either pointer may be NULL. */
+cfr_status cfr_game_canonical(const cfr_game* g, int64_t* canon_of_input, int64_t* level_ptr);
+
+/* ---------------------------------------------------------------- solver --
+ * Solver state lives in ONE caller-allocated device workspace (e.g. a torch
+ * uint8 tensor) that must stay allocated until cfr_solver_destroy.  All work is
+ * enqueued on the caller's CUDA stream (cudaStream_t passed as void*; NULL =
+ * legacy default stream).
+ */
+typedef enum { CFR_VANILLA = 0, CFR_PLUS = 1 } cfr_variant;
+
+typedef struct {
+    int32_t variant;     /* cfr_variant: CFR (w_t = 1) or CFR+ (RM+, w_t = t)      */
+    int32_t precision;   /* 64 (binary64) or 32 (binary32) working precision      */
+    int32_t flags;       /* bit 0: disable CUDA-Graph capture (debug);            */
+                         /* bit 1: force the multi-CTA level path for tiny games  */
+    int32_t reserved;
+} cfr_solver_config;
+
+#define CFR_FLAG_NO_GRAPH 1
+#define CFR_FLAG_NO_PERSISTENT 2
+
+/* Multi-GPU level sharding.  NULL or world_size == 1 means a
+ * single GPU.  nccl_unique_id points to the 128-byte ncclUniqueId that rank 0
+ * created (cfr_nccl_unique_id) and the caller broadcast (e.g. torch.distributed). */
+typedef struct {
+    int32_t rank;
+    int32_t world_size;
+    const void* nccl_unique_id;
+} cfr_dist;
+
+typedef struct cfr_solver cfr_solver;
+
+/* Bytes of device workspace the solver needs on this rank. */
+cfr_status cfr_solver_workspace_bytes(const cfr_game* g, const cfr_solver_config* cfg,
+                                      const cfr_dist* dist, size_t* bytes);
+/* Builds the solver in `workspace` (>= bytes, device memory of the current
+ * device), uploads the flattened game, initialises sigma^(1) = 1/|A(h)|
+ * and captures the iteration graph.  Blocking. */
+cfr_status cfr_solver_create(const cfr_game* g, const cfr_solver_config* cfg, void* workspace,
+                             size_t workspace_bytes, void* stream, const cfr_dist* dist,
+                             cfr_solver** out);
+void cfr_solver_destroy(cfr_solver* s);
+
+/* Runs `iterations` CFR iterations (T += iterations) and synchronises the stream;
+ * CFR_ERR_NUMERICAL if any regret or strategy became NaN/Inf. */
+cfr_status cfr_solver_run(cfr_solver* s, int64_t iterations);
+/* Enqueues `iterations` iterations on the stream and returns immediately (for
+ * event timing); call cfr_solver_sync before reading results. */
+cfr_status cfr_solver_enqueue(cfr_solver* s, int64_t iterations);
+cfr_status cfr_solver_sync(cfr_solver* s);
+/* Iterations completed so far (T). */
+cfr_status cfr_solver_iteration(cfr_solver* s, int64_t* T);
+
+/* Host outputs in the caller's (h, a) order (qbase).  sigma_bar (Eq 10):
+ * S_num / S_den, uniform where S_den = 0 (reading Q5). */
+cfr_status cfr_solver_average_strategy(cfr_solver* s, double* out /* [Q+] */);
+/* sigma^(T+1) (Eq 9). */
+cfr_status cfr_solver_current_strategy(cfr_solver* s, double* out /* [Q+] */);
+/* Raw state for checkpoint/inspection: cumulative regrets R [Q+], S_num [Q+],
+ * S_den [H+] (caller order).  Any pointer may be NULL. */
+cfr_status cfr_solver_get_state(cfr_solver* s, double* regret, double* s_num, double* s_den);
+
+#define CFR_EV_AVERAGE 0
+#define CFR_EV_CURRENT 1
+/* Per-player expected values u_hat(sigma, i) at the root under the
+ * average (Q10) or current strategy, computed on the device, [P]. */
+cfr_status cfr_solver_expected_values(cfr_solver* s, int32_t which, double* out /* [P] */);
+/* Best response to sigma_bar per player (ties to the lowest action), NashConv =
+ * sum_i (BR_i - EV_i) and exploitability = NashConv / P (reading Q11), on the
+ * device.  br may be NULL.  CFR_ERR_UNSUPPORTED if an infoset spans several
+ * depths or does not fit one tile (reading Q17). */
+cfr_status cfr_solver_exploitability(cfr_solver* s, double* nash_conv, double* exploitability,
+                                     double* br /* [P] or NULL */);
+
+/* Instrumentation for bench.py: kernels launched per iteration, and the mean
+ * per-kernel-class device time (CUDA events on the solver stream, ms) over
+ * `iterations` un-graphed iterations: out_ms[0] forward levels, [1] backward
+ * levels, [2] deferred update, [3] dominant (largest) backward level, [4] the
+ * dominant level's index.  The iterations ARE applied (T advances). */
+cfr_status cfr_solver_launches_per_iteration(cfr_solver* s, int64_t* launches);
+cfr_status cfr_solver_profile(cfr_solver* s, int64_t iterations, double* out_ms /* [5] */);
+/* Algorithmic DRAM bytes of one iteration by the DESIGN.md §6 model: out[0]
+ * total, [1] forward, [2] backward, [3] update, [4] dominant backward level. */
+cfr_status cfr_solver_model_bytes(cfr_solver* s, double* out /* [5] */);
+
+/* Writes a fresh ncclUniqueId (128 bytes) to `out` (rank 0 only). */
+cfr_status cfr_nccl_unique_id(void* out /* 128 bytes */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CFR_B200_H */

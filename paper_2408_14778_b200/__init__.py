@@ -1,0 +1,178 @@
+"""paper_2408_14778_b200 -- B200-native CFR / CFR+ (arXiv 2408.14778) behind a C ABI.
+
+Thin Python binding of ``include/cfr_b200.h`` (ctypes).  PyTorch supplies the
+device workspace (one uint8 tensor) and the CUDA stream; every step of the
+iteration runs in the sm_100a kernels of ``csrc/solver.cu``.  There is no CPU
+fallback: without the native library or a CUDA device the solver raises.
+
+    game = Game(desc)                   # desc: gamegen.GameDesc-like arrays
+    s = Solver(game, variant="cfr+", precision=64)
+    s.run(1000)
+    s.average_strategy(); s.expected_values(); s.exploitability()
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from ._native import NativeError, build, load
+
+__all__ = ["Game", "Solver", "NativeError", "build", "load", "CFR", "CFR_PLUS"]
+
+CFR, CFR_PLUS = 0, 1
+FLAG_NO_GRAPH = 1
+
+
+def _ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class Game:
+    """cfr_game_create over the Def. 2.1 arrays (any node order)."""
+
+    def __init__(self, desc):
+        L = load()
+        self._L = L
+        self.num_players = int(desc.num_players)
+        self._arrays = [np.ascontiguousarray(desc.parent, dtype=np.int64),
+                        np.ascontiguousarray(desc.player, dtype=np.int32),
+                        np.ascontiguousarray(desc.infoset, dtype=np.int64),
+                        np.ascontiguousarray(desc.action, dtype=np.int32),
+                        np.ascontiguousarray(desc.chance_prob, dtype=np.float64),
+                        np.ascontiguousarray(desc.utility, dtype=np.float64)]
+        a = self._arrays
+        d = _native.GameDescC(a[0].shape[0], self.num_players, *(x.ctypes.data for x in a))
+        h = ctypes.c_void_p()
+        _native.check(L.cfr_game_create(ctypes.byref(d), ctypes.byref(h)))
+        self._h = h
+        self._arrays = None   # the library copied what it needs
+        info = _native.GameInfoC()
+        _native.check(L.cfr_game_info(self._h, ctypes.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in info._fields_}
+        self.V = self.info["num_nodes"]
+        self.H = self.info["num_infosets"]
+        self.Q = self.info["num_pairs"]
+        self.D = self.info["depth"]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._L.cfr_game_destroy(h)
+            self._h = None
+
+    def qbase(self) -> np.ndarray:
+        q = np.zeros(self.H + 1, dtype=np.int64)
+        _native.check(self._L.cfr_game_qbase(self._h, _ptr(q)))
+        return q
+
+    def canonical(self):
+        c = np.zeros(self.V, dtype=np.int64)
+        lp = np.zeros(self.D + 2, dtype=np.int64)
+        _native.check(self._L.cfr_game_canonical(self._h, _ptr(c), _ptr(lp)))
+        return c, lp
+
+
+class Solver:
+    """cfr_solver_* over a torch-allocated device workspace and a torch stream."""
+
+    def __init__(self, game: Game, variant="cfr", precision: int = 64, device="cuda", stream=None,
+                 flags: int = 0):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2408_14778_b200.Solver needs a CUDA device (no CPU fallback)")
+        L = load()
+        self._L = L
+        self.game = game
+        v = {"cfr": CFR, "vanilla": CFR, "cfr+": CFR_PLUS, "cfrplus": CFR_PLUS}.get(variant, variant)
+        self.cfg = _native.SolverConfigC(int(v), int(precision), int(flags), 0)
+        nbytes = ctypes.c_size_t()
+        _native.check(L.cfr_solver_workspace_bytes(game._h, ctypes.byref(self.cfg), None, ctypes.byref(nbytes)))
+        self.workspace_bytes = int(nbytes.value)
+        dev = torch.device(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        torch.cuda.set_device(dev)
+        self.workspace = torch.empty(self.workspace_bytes + 256, dtype=torch.uint8, device=dev)
+        base = self.workspace.data_ptr()
+        aligned = (base + 255) & ~255
+        self.stream = stream if stream is not None else torch.cuda.Stream(dev)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            _native.check(L.cfr_solver_create(game._h, ctypes.byref(self.cfg), ctypes.c_void_p(aligned),
+                                              self.workspace_bytes, ctypes.c_void_p(self.stream.cuda_stream),
+                                              None, ctypes.byref(h)))
+        self._h = h
+        self.Q, self.H, self.P = game.Q, game.H, game.num_players
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._L.cfr_solver_destroy(h)
+            self._h = None
+
+    # -- iteration
+    def run(self, iterations: int) -> "Solver":
+        _native.check(self._L.cfr_solver_run(self._h, int(iterations)))
+        return self
+
+    def enqueue(self, iterations: int) -> "Solver":
+        _native.check(self._L.cfr_solver_enqueue(self._h, int(iterations)))
+        return self
+
+    def sync(self) -> "Solver":
+        _native.check(self._L.cfr_solver_sync(self._h))
+        return self
+
+    @property
+    def iteration(self) -> int:
+        t = ctypes.c_int64()
+        _native.check(self._L.cfr_solver_iteration(self._h, ctypes.byref(t)))
+        return int(t.value)
+
+    # -- readbacks (caller (h, a) order)
+    def average_strategy(self) -> np.ndarray:
+        out = np.zeros(self.Q)
+        _native.check(self._L.cfr_solver_average_strategy(self._h, _ptr(out)))
+        return out
+
+    def current_strategy(self) -> np.ndarray:
+        out = np.zeros(self.Q)
+        _native.check(self._L.cfr_solver_current_strategy(self._h, _ptr(out)))
+        return out
+
+    def state(self) -> dict:
+        r, sn, sd = np.zeros(self.Q), np.zeros(self.Q), np.zeros(self.H)
+        _native.check(self._L.cfr_solver_get_state(self._h, _ptr(r), _ptr(sn), _ptr(sd)))
+        return dict(regret=r, snum=sn, sden=sd)
+
+    def expected_values(self, which: str = "average") -> np.ndarray:
+        out = np.zeros(self.P)
+        w = 0 if which == "average" else 1
+        _native.check(self._L.cfr_solver_expected_values(self._h, w, _ptr(out)))
+        return out
+
+    def exploitability(self) -> dict:
+        nc, ex = ctypes.c_double(), ctypes.c_double()
+        br = np.zeros(self.P)
+        _native.check(self._L.cfr_solver_exploitability(self._h, ctypes.byref(nc), ctypes.byref(ex), _ptr(br)))
+        return dict(nash_conv=nc.value, exploitability=ex.value, br=br)
+
+    # -- instrumentation
+    def launches_per_iteration(self) -> int:
+        n = ctypes.c_int64()
+        _native.check(self._L.cfr_solver_launches_per_iteration(self._h, ctypes.byref(n)))
+        return int(n.value)
+
+    def profile(self, iterations: int) -> dict:
+        out = np.zeros(5)
+        _native.check(self._L.cfr_solver_profile(self._h, int(iterations), _ptr(out)))
+        return dict(fwd_ms=out[0], bwd_ms=out[1], deferred_ms=out[2], dominant_ms=out[3], dominant_level=int(out[4]))
+
+    def model_bytes(self) -> dict:
+        out = np.zeros(5)
+        _native.check(self._L.cfr_solver_model_bytes(self._h, _ptr(out)))
+        return dict(total=out[0], fwd=out[1], bwd=out[2], update=out[3], dominant=out[4])

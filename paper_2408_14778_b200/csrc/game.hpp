@@ -1,0 +1,93 @@
+// Internal (product-side) representation of a flattened game.  Built once on the
+// host by flatten.cpp (SURVEY.md Appendix B-1 canonical BFS + DESIGN.md §5 slot
+// layout), uploaded by solver.cu.  Not part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/cfr_b200.h"
+
+namespace cfrb {
+
+// Backward-pass work unit: a run of slots [s0, s1) of one level holding whole
+// infoset groups (or one chunk of an oversized group), plus its segments.
+struct TileH {
+    int64_t s0, s1;        // slot range
+    int32_t seg0, seg1;    // segments [seg0, seg1) in Game::segs
+    int32_t npairs;        // sum of |A(h)| over the tile's segments
+    int32_t pad;
+};
+
+// A segment = the member slots [sb, se) of internal infoset h inside one tile.
+struct SegH {
+    int64_t h;             // internal infoset id
+    int64_t sb, se;        // member slots inside the tile
+    int32_t pair_off;      // offset of (h, 0) in the tile's pair numbering
+    int32_t fused;         // 1: all members here, single depth -> update in-tile
+};
+
+constexpr int kTileSlots = 256;     // parents per tile (= threads per CTA)
+constexpr int kTilePairs = 1024;    // (infoset, action) pairs per tile
+constexpr int kTileSegs = 256;      // segments per tile
+
+struct Game {
+    // ---- input-level facts
+    int64_t V = 0;
+    int32_t P = 0;
+    int32_t Pc = 0;          // value columns stored on device (1 if zero-sum 2p)
+    bool zero_sum_2p = false;
+    int32_t D = 0;           // max depth
+    int64_t num_terminals = 0, num_chance = 0, num_decision = 0;
+    int64_t max_infoset_nodes = 0;
+    bool depth_homogeneous = true;
+    double max_abs_u = 0.0;  // over the double inputs
+
+    // ---- canonical flattening (Appendix B-1)
+    std::vector<int64_t> canon_of_input;  // [V]
+    std::vector<int64_t> level_ptr;       // [D+2] canonical node ranges per depth
+
+    // ---- slots: decision nodes, level-major, infoset-grouped
+    int64_t NS = 0;
+    std::vector<int64_t> slot_ptr;        // [D+1]: slots of depth L in [slot_ptr[L], slot_ptr[L+1])
+    std::vector<int64_t> s_node;          // canonical node index
+    std::vector<int64_t> s_cb;            // canonical index of first child
+    std::vector<int32_t> s_n;             // number of children
+    std::vector<int64_t> s_ebase;         // base of the children's edge probs in sigma_ext
+    std::vector<uint8_t> s_actor;         // 0 chance, 1..P player
+    std::vector<int64_t> s_parent;        // parent slot (-1 for the root)
+    std::vector<int64_t> s_e;             // sigma_ext index of the incoming edge
+    std::vector<uint8_t> s_pact;          // actor of the parent
+
+    // ---- infosets, internal numbering (order of first appearance in slot order)
+    int64_t H = 0, Q = 0, C = 0;          // infosets, pairs, chance edges
+    std::vector<int64_t> h_int_of_caller, h_caller_of_int;
+    std::vector<int64_t> qbase_int;       // [H+1]
+    std::vector<int64_t> qbase_caller;    // [H+1]
+    std::vector<uint8_t> owner_int;       // [H]
+    std::vector<uint8_t> deferred;        // [H] 1: accumulate globally, update after the pass
+    std::vector<int64_t> deferred_list;
+    std::vector<double> chance_vals;      // [C], sigma_ext[Q + c]
+
+    // ---- backward tiles
+    std::vector<int64_t> tile_ptr;        // [D+1]: tiles of parent depth L
+    std::vector<TileH> tiles;
+    std::vector<SegH> segs;
+
+    // ---- values
+    std::vector<double> util_c;           // [V * Pc] canonical rows (terminals; 0 elsewhere)
+};
+
+// flatten.cpp
+bool build_game(const cfr_game_desc* d, Game& g, std::string& err);
+// E = 1 + ceil(log2(2 max|u|)) (exact-accumulation exponent)
+int game_exponent(double max_abs_u);
+
+}  // namespace cfrb
+
+struct cfr_game {
+    cfrb::Game g;
+};
+
+// error plumbing shared by the product's translation units
+void cfrb_set_error(const std::string& msg);

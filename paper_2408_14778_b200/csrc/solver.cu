@@ -1,0 +1,1088 @@
+// B200 (sm_100a) CFR / CFR+ iteration: device kernels, CUDA-Graph orchestration
+// and the solver half of the C ABI (include/cfr_b200.h).
+//
+// One iteration (§3.2), all state resident in HBM:
+//   k_fwd  level l = 1..D-1  : reach factors of the decision nodes of depth l
+//                              (Eq 2 pi_check and Eq 4 pi_hat per player, the
+//                              paper's Pi_check / Pi_hat recurrences Eq 13, P:266,
+//                              P:281) -- child-centric, terminals never touched.
+//   k_bwd  level L = D-1..0  : one CTA per tile of whole infosets: node values
+//                              (Eq 1 / Eq 11), the cancelled-form
+//                              regret terms of Eq 7 (matrix form P:313) and
+//                              pi_bar of Eq 5 summed EXACTLY in int64
+//                              slices, then -- because the infoset is complete
+//                              and its sigma is no longer needed this iteration --
+//                              the fused update: cumulative regret (Eq 8/15 or
+//                              CFR+), average-strategy sums (Eq 10/14) and regret
+//                              matching (Eq 9).
+//   k_deferred               : the same update for infosets that span depths or
+//                              tiles (accumulated globally with int64 atomics).
+// No tensor cores: the path is a sparse gather/scatter at < 1 flop/byte.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "game.hpp"
+
+namespace cfrb {
+
+// device mirrors of TileH / SegH (identical layout, copied bytewise)
+struct TileD {
+    long long s0, s1;
+    int seg0, seg1;
+    int npairs;
+    int pad;
+};
+struct SegD {
+    long long h, sb, se;
+    int pair_off;
+    int fused;
+};
+static_assert(sizeof(TileD) == sizeof(TileH), "TileD layout");
+static_assert(sizeof(SegD) == sizeof(SegH), "SegD layout");
+
+enum { MODE_CFR = 0, MODE_VALUES = 1, MODE_BR = 2 };
+
+template <class R, class I>
+struct DG {
+    R* U;          // [V * Pc] node values, canonical order; terminal rows = u
+    R* reach;      // [2P][NS]: rows 0..P-1 pi_check(., i), rows P..2P-1 pi_hat(., i)
+    R* sig;        // [Q + C] sigma_ext = current strategy (internal q order) | chance
+    R* regret;     // [Q] cumulative regret
+    R* snum;       // [Q] sum_t w_t pi_bar sigma
+    R* sden;       // [H] sum_t w_t pi_bar
+    unsigned long long* acc_r;  // [Q][3] exact slices (deferred infosets)
+    unsigned long long* acc_p;  // [H][3]
+    const I* s_node;
+    const I* s_cb;
+    const int* s_n;
+    const I* s_ebase;
+    const unsigned char* s_actor;
+    const I* s_parent;
+    const I* s_e;
+    const unsigned char* s_pact;
+    const I* qbase;               // [H+1] internal
+    const unsigned char* owner;   // [H]
+    const TileD* tiles;
+    const SegD* segs;
+    const I* deferred;            // [ndef]
+    long long* ctrl;              // [0] iterations done, [1] first bad iteration, [2] done counter
+    long long NS;
+    long long ndef;
+    int P;
+    int variant;
+    double sc[3], rc[3];          // 2^(40k-E), 2^(E-40k): regret / BR sums
+    double scp[3], rcp[3];        // same with E = 1: pi_bar sums
+};
+
+// ---------------------------------------------------------------- exact sums
+// Three 40-bit int64 slices.  x*2^(40k-E)
+// and c*2^(E-40k) are exact power-of-two scalings; __double2ll_rn rounds half to
+// even; the remainder subtraction is exact.  Sums of slices are order-free.
+__device__ __forceinline__ void xadd(long long (&c)[3], double x, const double (&sc)[3], const double (&rc)[3]) {
+    const long long k0 = __double2ll_rn(x * sc[0]);
+    x = x - __ll2double_rn(k0) * rc[0];
+    const long long k1 = __double2ll_rn(x * sc[1]);
+    x = x - __ll2double_rn(k1) * rc[1];
+    const long long k2 = __double2ll_rn(x * sc[2]);
+    c[0] += k0;
+    c[1] += k1;
+    c[2] += k2;
+}
+__device__ __forceinline__ double xdec(long long c0, long long c1, long long c2, const double (&rc)[3]) {
+    return (__ll2double_rn(c0) * rc[0] + __ll2double_rn(c1) * rc[1]) + __ll2double_rn(c2) * rc[2];
+}
+
+template <class R>
+__device__ __forceinline__ bool finite_(R x) {
+    return isfinite(x);
+}
+
+// ------------------------------------------------------------ forward pass
+// Decision nodes of one depth, slot order.  Eq 2: pi_check(v,i) =
+// pi_check(parent,i) * (sigma if the parent's actor != i else 1); Eq 4 (P:97,
+// reading Q1): pi_hat(v,i) = pi_hat(parent,i) * (sigma if actor == i else 1).
+template <class R, class I, int PT>
+__global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ sig, long long s_begin,
+                                             long long s_end) {
+    const int P = (PT > 0) ? PT : g.P;
+    const long long NS = g.NS;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long s = s_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; s < s_end; s += stride) {
+        const long long p = (long long)g.s_parent[s];
+        const R x = sig[g.s_e[s]];
+        const int act = g.s_pact[s];
+#pragma unroll
+        for (int j = 0; j < ((PT > 0) ? PT : 16); ++j) {
+            if (PT == 0 && j >= P) break;
+            const R pc = g.reach[j * NS + p];
+            g.reach[j * NS + s] = (act != j + 1) ? pc * x : pc;
+            const R ph = g.reach[(P + j) * NS + p];
+            g.reach[(P + j) * NS + s] = (act == j + 1) ? ph * x : ph;
+        }
+    }
+}
+
+// ----------------------------------------------------------- backward pass
+// Shared memory of one tile (dynamic).
+template <class R, int PC>
+struct TileSmem {
+    R sv[kTileSlots * PC];   // node values of the tile's slots
+    R rt[kTilePairs];        // decoded r~ (or BR sums)
+    R pos[kTilePairs];       // positive regrets
+    R pib[kTileSegs];        // decoded pi_bar per segment
+    R zs[kTileSegs];         // sum of positive regrets per segment
+    int soff[kTileSegs + 1]; // pair offsets of the tile's segments
+    int best[kTileSegs];     // BR argmax per segment
+};
+
+template <class R, class I, int PC, int MODE>
+__global__ void __launch_bounds__(256) k_bwd(DG<R, I> g, const R* __restrict__ sig, long long tile0, int br_player,
+                                             int last) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem<R, PC>& sm = *reinterpret_cast<TileSmem<R, PC>*>(smem_raw);
+    const TileD T = g.tiles[tile0 + blockIdx.x];
+    const int nslot = (int)(T.s1 - T.s0);
+    const int tid = threadIdx.x, nth = blockDim.x;
+
+    // Phase A: node values, Eq 1 in ascending action order from +0.
+    for (int ls = tid; ls < nslot; ls += nth) {
+        const long long s = T.s0 + ls;
+        const long long cb = (long long)g.s_cb[s];
+        const int n = g.s_n[s];
+        const long long eb = (long long)g.s_ebase[s];
+        R v[PC];
+#pragma unroll
+        for (int j = 0; j < PC; ++j) v[j] = (R)0;
+        for (int a = 0; a < n; ++a) {
+            const R x = sig[eb + a];
+#pragma unroll
+            for (int j = 0; j < PC; ++j) v[j] = v[j] + x * g.U[(cb + a) * PC + j];
+        }
+        const bool skip = (MODE == MODE_BR) && ((int)g.s_actor[s] == br_player);
+        if (!skip) {
+            const long long nd = (long long)g.s_node[s];
+#pragma unroll
+            for (int j = 0; j < PC; ++j) g.U[nd * PC + j] = v[j];
+        }
+#pragma unroll
+        for (int j = 0; j < PC; ++j) sm.sv[ls * PC + j] = v[j];
+    }
+    if (MODE == MODE_VALUES) return;
+
+    const int nseg = T.seg1 - T.seg0;
+    for (int k = tid; k < nseg; k += nth) sm.soff[k] = g.segs[T.seg0 + k].pair_off;
+    if (tid == 0) sm.soff[nseg] = T.npairs;
+    __syncthreads();
+
+    const long long NS = g.NS;
+    const int P = g.P;
+    long long t_iter = 0;
+    if (MODE == MODE_CFR) t_iter = g.ctrl[0] + 1;
+
+    // Phase B: per (infoset, action) exact sums over the infoset's member slots.
+    for (int p = tid; p < T.npairs; p += nth) {
+        int lo = 0, hi = nseg - 1;            // last segment with soff <= p
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.soff[mid] <= p) lo = mid; else hi = mid - 1;
+        }
+        const SegD sg = g.segs[T.seg0 + lo];
+        const int a = p - sm.soff[lo];
+        const long long h = sg.h;
+        const int i = g.owner[h];
+        const int col = (PC == 1) ? 0 : i - 1;
+        if (MODE == MODE_BR && i != br_player) continue;
+        long long c[3] = {0, 0, 0};
+        long long cp[3] = {0, 0, 0};
+        const bool neg = (PC == 1) && (i == 2);   // u2 = -u1 (Appendix B-7)
+        for (long long s = sg.sb; s < sg.se; ++s) {
+            const R cf = g.reach[(long long)(i - 1) * NS + s];
+            const R uc = g.U[((long long)g.s_cb[s] + a) * PC + col];
+            if (MODE == MODE_CFR) {
+                const R vd = sm.sv[(int)(s - T.s0) * PC + col];
+                const R diff = neg ? (vd - uc) : (uc - vd);
+                const R term = cf * diff;
+                xadd(c, (double)term, g.sc, g.rc);
+                if (a == 0) xadd(cp, (double)g.reach[(long long)(P + i - 1) * NS + s], g.scp, g.rcp);
+            } else {  // MODE_BR: sum of cf * V(child) in the stored column
+                const R term = cf * uc;
+                xadd(c, (double)term, g.sc, g.rc);
+            }
+        }
+        if (MODE == MODE_BR) {
+            sm.rt[p] = (R)xdec(c[0], c[1], c[2], g.rc);
+        } else if (sg.fused) {
+            sm.rt[p] = (R)xdec(c[0], c[1], c[2], g.rc);
+            if (a == 0) sm.pib[lo] = (R)xdec(cp[0], cp[1], cp[2], g.rcp);
+        } else {
+            const long long q = (long long)g.qbase[h] + a;
+            atomicAdd(&g.acc_r[q * 3 + 0], (unsigned long long)c[0]);
+            atomicAdd(&g.acc_r[q * 3 + 1], (unsigned long long)c[1]);
+            atomicAdd(&g.acc_r[q * 3 + 2], (unsigned long long)c[2]);
+            if (a == 0) {
+                atomicAdd(&g.acc_p[h * 3 + 0], (unsigned long long)cp[0]);
+                atomicAdd(&g.acc_p[h * 3 + 1], (unsigned long long)cp[1]);
+                atomicAdd(&g.acc_p[h * 3 + 2], (unsigned long long)cp[2]);
+            }
+        }
+    }
+    __syncthreads();
+
+    if (MODE == MODE_BR) {
+        // argmax per segment (ties to the lowest action); for u2 = -u1 storage the
+        // stored sums are negated, so player 2 takes the argmin.
+        for (int k = tid; k < nseg; k += nth) {
+            const SegD sg = g.segs[T.seg0 + k];
+            if ((int)g.owner[sg.h] != br_player) continue;
+            const int n = sm.soff[k + 1] - sm.soff[k];
+            const bool neg = (PC == 1) && (br_player == 2);
+            int best = 0;
+            R bv = sm.rt[sm.soff[k]];
+            for (int a = 1; a < n; ++a) {
+                const R x = sm.rt[sm.soff[k] + a];
+                if (neg ? (x < bv) : (x > bv)) { bv = x; best = a; }
+            }
+            sm.best[k] = best;
+        }
+        __syncthreads();
+        for (int k = 0; k < nseg; ++k) {
+            const SegD sg = g.segs[T.seg0 + k];
+            if ((int)g.owner[sg.h] != br_player) continue;
+            const int best = sm.best[k];
+            for (long long s = sg.sb + tid; s < sg.se; s += nth) {
+                const long long src = ((long long)g.s_cb[s] + best) * PC;
+                const long long dst = (long long)g.s_node[s] * PC;
+#pragma unroll
+                for (int j = 0; j < PC; ++j) g.U[dst + j] = g.U[src + j];
+            }
+        }
+        return;
+    }
+
+    // Phase C: fused update of complete single-depth infosets.
+    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
+    for (int p = tid; p < T.npairs; p += nth) {
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.soff[mid] <= p) lo = mid; else hi = mid - 1;
+        }
+        const SegD sg = g.segs[T.seg0 + lo];
+        if (!sg.fused) continue;
+        const int a = p - sm.soff[lo];
+        const long long q = (long long)g.qbase[sg.h] + a;
+        const R rt = sm.rt[p];
+        R r;
+        if (g.variant == 0) {
+            r = g.regret[q] + rt;                       // Eq 8/15, cumulative (Q4)
+        } else {
+            const R x = g.regret[q] + rt;               // CFR+ (Q6)
+            r = (x > (R)0) ? x : (R)0;
+            if (!finite_(x)) r = x;
+        }
+        g.regret[q] = r;
+        const R wp = w * sm.pib[lo];
+        g.snum[q] = g.snum[q] + wp * g.sig[q];          // Eq 10 numerator
+        sm.pos[p] = (r > (R)0) ? r : (R)0;
+    }
+    __syncthreads();
+    for (int k = tid; k < nseg; k += nth) {
+        const SegD sg = g.segs[T.seg0 + k];
+        if (!sg.fused) continue;
+        g.sden[sg.h] = g.sden[sg.h] + w * sm.pib[k];    // Eq 10 denominator
+        R z = (R)0;
+        for (int p = sm.soff[k]; p < sm.soff[k + 1]; ++p) z = z + sm.pos[p];
+        sm.zs[k] = z;
+    }
+    __syncthreads();
+    bool bad = false;
+    for (int p = tid; p < T.npairs; p += nth) {
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.soff[mid] <= p) lo = mid; else hi = mid - 1;
+        }
+        const SegD sg = g.segs[T.seg0 + lo];
+        if (!sg.fused) continue;
+        const int a = p - sm.soff[lo];
+        const int n = sm.soff[lo + 1] - sm.soff[lo];
+        const long long q = (long long)g.qbase[sg.h] + a;
+        const R z = sm.zs[lo];
+        const R nsig = (z > (R)0) ? sm.pos[p] / z : (R)1 / (R)n;   // Eq 9
+        g.sig[q] = nsig;
+        if (!finite_(g.regret[q]) || !finite_(nsig) || !finite_(z)) bad = true;
+    }
+    if (bad) atomicMin(&g.ctrl[1], t_iter);
+    if (last) {
+        __syncthreads();
+        if (tid == 0) g.ctrl[0] = t_iter;
+    }
+}
+
+// Update of deferred infosets (span several depths / tiles): decode the global
+// exact sums, then the same Eq 8/15, Eq 10, Eq 9 steps; zero the accumulators.
+template <class R, class I>
+__global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
+    const long long t_iter = g.ctrl[0] + 1;
+    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
+    bool bad = false;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < g.ndef; idx += stride) {
+        const long long h = (long long)g.deferred[idx];
+        const long long qb = (long long)g.qbase[h];
+        const int n = (int)((long long)g.qbase[h + 1] - qb);
+        const long long p0 = (long long)g.acc_p[h * 3 + 0], p1 = (long long)g.acc_p[h * 3 + 1],
+                        p2 = (long long)g.acc_p[h * 3 + 2];
+        g.acc_p[h * 3 + 0] = 0;
+        g.acc_p[h * 3 + 1] = 0;
+        g.acc_p[h * 3 + 2] = 0;
+        const R pib = (R)xdec(p0, p1, p2, g.rcp);
+        const R wp = w * pib;
+        R z = (R)0;
+        for (int a = 0; a < n; ++a) {
+            const long long q = qb + a;
+            const long long c0 = (long long)g.acc_r[q * 3 + 0], c1 = (long long)g.acc_r[q * 3 + 1],
+                            c2 = (long long)g.acc_r[q * 3 + 2];
+            g.acc_r[q * 3 + 0] = 0;
+            g.acc_r[q * 3 + 1] = 0;
+            g.acc_r[q * 3 + 2] = 0;
+            const R rt = (R)xdec(c0, c1, c2, g.rc);
+            R r;
+            if (g.variant == 0) {
+                r = g.regret[q] + rt;
+            } else {
+                const R x = g.regret[q] + rt;
+                r = (x > (R)0) ? x : (R)0;
+                if (!finite_(x)) r = x;
+            }
+            g.regret[q] = r;
+            g.snum[q] = g.snum[q] + wp * g.sig[q];
+        }
+        g.sden[h] = g.sden[h] + wp;
+        for (int a = 0; a < n; ++a) {
+            const R r = g.regret[qb + a];
+            z = z + ((r > (R)0) ? r : (R)0);
+        }
+        for (int a = 0; a < n; ++a) {
+            const R r = g.regret[qb + a];
+            const R pos = (r > (R)0) ? r : (R)0;
+            const R nsig = (z > (R)0) ? pos / z : (R)1 / (R)n;
+            g.sig[qb + a] = nsig;
+            if (!finite_(r) || !finite_(nsig)) bad = true;
+        }
+    }
+    if (bad) atomicMin(&g.ctrl[1], t_iter);
+    if (last) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const unsigned long long prev = atomicAdd((unsigned long long*)&g.ctrl[2], 1ULL);
+            if (prev == gridDim.x - 1) {
+                g.ctrl[0] = t_iter;
+                g.ctrl[2] = 0;
+            }
+        }
+    }
+}
+
+// sigma_bar (Eq 10, reading Q5) into an evaluation strategy buffer: S_num/S_den,
+// uniform where S_den = 0.  Chance part copied.
+template <class R, class I>
+__global__ void k_average(DG<R, I> g, R* out, long long H, long long Q, long long C) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < H; h += stride) {
+        const long long qb = (long long)g.qbase[h];
+        const int n = (int)((long long)g.qbase[h + 1] - qb);
+        const R den = g.sden[h];
+        for (int a = 0; a < n; ++a) out[qb + a] = (den > (R)0) ? g.snum[qb + a] / den : (R)1 / (R)n;
+    }
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < C; c += stride) out[Q + c] = g.sig[Q + c];
+}
+
+// --------------------------------------------------------------- host side
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            cfrb_set_error(std::string(#call) + ": " + cudaGetErrorString(e_));                    \
+            return CFR_ERR_CUDA;                                                                   \
+        }                                                                                          \
+    } while (0)
+
+struct SolverBase {
+    virtual ~SolverBase() {}
+    virtual cfr_status enqueue(int64_t iters) = 0;
+    virtual cfr_status sync() = 0;
+    virtual cfr_status iteration(int64_t* T) = 0;
+    virtual cfr_status strategy(int which, double* out) = 0;   // 0 avg, 1 current
+    virtual cfr_status get_state(double* regret, double* snum, double* sden) = 0;
+    virtual cfr_status expected_values(int which, double* out) = 0;
+    virtual cfr_status exploitability(double* nc, double* ex, double* br) = 0;
+    virtual cfr_status launches(int64_t* n) = 0;
+    virtual cfr_status profile(int64_t iters, double* out) = 0;
+    virtual cfr_status model_bytes(double* out) = 0;
+};
+
+struct Layout {
+    size_t off = 0;
+    template <class T>
+    size_t take(size_t n) {
+        off = (off + 255) & ~size_t(255);
+        const size_t o = off;
+        off += n * sizeof(T);
+        return o;
+    }
+};
+
+template <class R, class I>
+struct Plan {
+    size_t U, reach, sig, sig_eval, regret, snum, sden, acc_r, acc_p;
+    size_t s_node, s_cb, s_n, s_ebase, s_actor, s_parent, s_e, s_pact;
+    size_t qbase, owner, tiles, segs, deferred, ctrl, out;
+    size_t total;
+    explicit Plan(const Game& g) {
+        Layout L;
+        const size_t NS = (size_t)g.NS, Q = (size_t)g.Q, H = (size_t)g.H, C = (size_t)g.C;
+        U = L.take<R>((size_t)g.V * g.Pc);
+        reach = L.take<R>(2 * (size_t)g.P * NS);
+        sig = L.take<R>(Q + C);
+        sig_eval = L.take<R>(Q + C);
+        regret = L.take<R>(Q);
+        snum = L.take<R>(Q);
+        sden = L.take<R>(H);
+        acc_r = L.take<unsigned long long>(3 * Q);
+        acc_p = L.take<unsigned long long>(3 * H);
+        s_node = L.take<I>(NS);
+        s_cb = L.take<I>(NS);
+        s_n = L.take<int>(NS);
+        s_ebase = L.take<I>(NS);
+        s_actor = L.take<unsigned char>(NS);
+        s_parent = L.take<I>(NS);
+        s_e = L.take<I>(NS);
+        s_pact = L.take<unsigned char>(NS);
+        qbase = L.take<I>(H + 1);
+        owner = L.take<unsigned char>(H);
+        tiles = L.take<TileD>(g.tiles.size());
+        segs = L.take<SegD>(g.segs.size());
+        deferred = L.take<I>(g.deferred_list.size());
+        ctrl = L.take<long long>(8);
+        out = L.take<R>(std::max<size_t>(Q + C, (size_t)g.P * 2 + 8));
+        total = L.off + 256;
+    }
+};
+
+template <class T, class S>
+static std::vector<T> narrow(const std::vector<S>& v) {
+    std::vector<T> o(v.size());
+    for (size_t k = 0; k < v.size(); ++k) o[k] = (T)v[k];
+    return o;
+}
+
+template <class R, class I>
+struct Solver final : SolverBase {
+    const Game* gp;
+    cfr_solver_config cfg;
+    cudaStream_t stream;
+    cudaStream_t cap_stream = nullptr;
+    unsigned char* ws;
+    Plan<R, I> plan;
+    DG<R, I> dg;
+    cudaGraphExec_t gexec = nullptr;
+    int E = 1;
+    int64_t launches_per_iter = 0;
+    bool use_graph = true;
+
+    Solver(const Game* g, const cfr_solver_config& c, void* w, cudaStream_t s)
+        : gp(g), cfg(c), stream(s), ws((unsigned char*)w), plan(*g) {}
+
+    ~Solver() override {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (cap_stream) cudaStreamDestroy(cap_stream);
+    }
+
+    template <class T>
+    T* at(size_t off) { return reinterpret_cast<T*>(ws + off); }
+
+    template <class T>
+    cfr_status up(size_t off, const std::vector<T>& v) {
+        if (!v.empty()) CU(cudaMemcpyAsync(ws + off, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, stream));
+        return CFR_OK;
+    }
+
+    size_t smem_bytes() const {
+        switch (gp->Pc) {
+            case 1: return sizeof(TileSmem<R, 1>);
+            case 2: return sizeof(TileSmem<R, 2>);
+            case 3: return sizeof(TileSmem<R, 3>);
+            default: return sizeof(TileSmem<R, 4>);
+        }
+    }
+
+    cfr_status init() {
+        const Game& g = *gp;
+        if (g.Pc > 4) {
+            cfrb_set_error("non-zero-sum games with more than 4 players are not supported by the device kernels");
+            return CFR_ERR_UNSUPPORTED;
+        }
+        use_graph = !(cfg.flags & CFR_FLAG_NO_GRAPH);
+        // exact-accumulation exponent from the utilities in working precision
+        double m = 0.0;
+        for (double u : g.util_c) m = std::max(m, std::fabs((double)(R)u));
+        if (g.zero_sum_2p) { /* column 2 = -column 1: same max */ }
+        E = game_exponent(m);
+        dg.U = at<R>(plan.U);
+        dg.reach = at<R>(plan.reach);
+        dg.sig = at<R>(plan.sig);
+        dg.regret = at<R>(plan.regret);
+        dg.snum = at<R>(plan.snum);
+        dg.sden = at<R>(plan.sden);
+        dg.acc_r = at<unsigned long long>(plan.acc_r);
+        dg.acc_p = at<unsigned long long>(plan.acc_p);
+        dg.s_node = at<I>(plan.s_node);
+        dg.s_cb = at<I>(plan.s_cb);
+        dg.s_n = at<int>(plan.s_n);
+        dg.s_ebase = at<I>(plan.s_ebase);
+        dg.s_actor = at<unsigned char>(plan.s_actor);
+        dg.s_parent = at<I>(plan.s_parent);
+        dg.s_e = at<I>(plan.s_e);
+        dg.s_pact = at<unsigned char>(plan.s_pact);
+        dg.qbase = at<I>(plan.qbase);
+        dg.owner = at<unsigned char>(plan.owner);
+        dg.tiles = at<TileD>(plan.tiles);
+        dg.segs = at<SegD>(plan.segs);
+        dg.deferred = at<I>(plan.deferred);
+        dg.ctrl = at<long long>(plan.ctrl);
+        dg.NS = g.NS;
+        dg.ndef = (long long)g.deferred_list.size();
+        dg.P = g.P;
+        dg.variant = cfg.variant;
+        for (int k = 0; k < 3; ++k) {
+            dg.sc[k] = std::ldexp(1.0, 40 * (k + 1) - E);
+            dg.rc[k] = std::ldexp(1.0, E - 40 * (k + 1));
+            dg.scp[k] = std::ldexp(1.0, 40 * (k + 1) - 1);
+            dg.rcp[k] = std::ldexp(1.0, 1 - 40 * (k + 1));
+        }
+        // ---- uploads
+        cfr_status st;
+        if ((st = up(plan.U, narrow<R>(g.util_c)))) return st;
+        if ((st = up(plan.s_node, narrow<I>(g.s_node)))) return st;
+        if ((st = up(plan.s_cb, narrow<I>(g.s_cb)))) return st;
+        if ((st = up(plan.s_n, g.s_n))) return st;
+        if ((st = up(plan.s_ebase, narrow<I>(g.s_ebase)))) return st;
+        if ((st = up(plan.s_actor, g.s_actor))) return st;
+        if ((st = up(plan.s_parent, narrow<I>(g.s_parent)))) return st;
+        if ((st = up(plan.s_e, narrow<I>(g.s_e)))) return st;
+        if ((st = up(plan.s_pact, g.s_pact))) return st;
+        if ((st = up(plan.qbase, narrow<I>(g.qbase_int)))) return st;
+        if ((st = up(plan.owner, g.owner_int))) return st;
+        {
+            std::vector<TileD> t(g.tiles.size());
+            if (!t.empty()) std::memcpy(t.data(), g.tiles.data(), t.size() * sizeof(TileD));
+            if ((st = up(plan.tiles, t))) return st;
+            std::vector<SegD> sgv(g.segs.size());
+            if (!sgv.empty()) std::memcpy(sgv.data(), g.segs.data(), sgv.size() * sizeof(SegD));
+            if ((st = up(plan.segs, sgv))) return st;
+        }
+        if ((st = up(plan.deferred, narrow<I>(g.deferred_list)))) return st;
+        // sigma^(1) = 1/|A(h)| and chance probabilities (rounded once, Q14)
+        {
+            std::vector<R> s0(g.Q + g.C);
+            for (int64_t h = 0; h < g.H; ++h) {
+                const int64_t n = g.qbase_int[h + 1] - g.qbase_int[h];
+                for (int64_t q = g.qbase_int[h]; q < g.qbase_int[h + 1]; ++q) s0[q] = (R)1 / (R)n;
+            }
+            for (int64_t c = 0; c < g.C; ++c) s0[g.Q + c] = (R)g.chance_vals[c];
+            if ((st = up(plan.sig, s0))) return st;
+            if ((st = up(plan.sig_eval, s0))) return st;
+        }
+        CU(cudaMemsetAsync(ws + plan.regret, 0, g.Q * sizeof(R), stream));
+        CU(cudaMemsetAsync(ws + plan.snum, 0, g.Q * sizeof(R), stream));
+        CU(cudaMemsetAsync(ws + plan.sden, 0, g.H * sizeof(R), stream));
+        CU(cudaMemsetAsync(ws + plan.acc_r, 0, 3 * g.Q * sizeof(unsigned long long), stream));
+        CU(cudaMemsetAsync(ws + plan.acc_p, 0, 3 * g.H * sizeof(unsigned long long), stream));
+        CU(cudaMemsetAsync(ws + plan.reach, 0, 2 * (size_t)g.P * g.NS * sizeof(R), stream));
+        {
+            // root reach factors = 1 (Eq 2 / Eq 4 base case); root is slot 0
+            std::vector<R> one(1, (R)1);
+            for (int r = 0; r < 2 * g.P; ++r)
+                if (g.NS > 0) CU(cudaMemcpyAsync(ws + plan.reach + ((size_t)r * g.NS) * sizeof(R), one.data(), sizeof(R),
+                                                 cudaMemcpyHostToDevice, stream));
+            std::vector<long long> ctrl = {0, LLONG_MAX, 0, 0, 0, 0, 0, 0};
+            if ((st = up(plan.ctrl, ctrl))) return st;
+        }
+        CU(cudaStreamSynchronize(stream));
+        // kernel attributes (dynamic smem above 48 KB needs opt-in)
+        const int sm = (int)smem_bytes();
+        CU(set_smem_attr(sm));
+        launches_per_iter = count_launches();
+        if (use_graph && g.NS > 0) {
+            CU(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+            cudaGraph_t graph;
+            CU(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+            cfr_status ls = launch_iteration(cap_stream, nullptr);
+            cudaError_t ce = cudaStreamEndCapture(cap_stream, &graph);
+            if (ls != CFR_OK) return ls;
+            if (ce != cudaSuccess) {
+                cfrb_set_error(std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
+                return CFR_ERR_CUDA;
+            }
+            CU(cudaGraphInstantiate(&gexec, graph, 0));
+            cudaGraphDestroy(graph);
+        }
+        return CFR_OK;
+    }
+
+    cudaError_t set_smem_attr(int sm) {
+        cudaError_t e = cudaSuccess;
+#define SETA(PC)                                                                                        \
+    e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_CFR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+    if (e) return e;                                                                                    \
+    e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_VALUES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+    if (e) return e;                                                                                    \
+    e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+    if (e) return e;
+        switch (gp->Pc) {
+            case 1: SETA(1) break;
+            case 2: SETA(2) break;
+            case 3: SETA(3) break;
+            default: SETA(4) break;
+        }
+#undef SETA
+        return e;
+    }
+
+    int64_t count_launches() const {
+        const Game& g = *gp;
+        int64_t n = 0;
+        for (int l = 1; l < g.D; ++l)
+            if (g.slot_ptr[l + 1] > g.slot_ptr[l]) ++n;
+        for (int L = g.D - 1; L >= 0; --L)
+            if (g.tile_ptr[L + 1] > g.tile_ptr[L]) ++n;
+        if (!g.deferred_list.empty()) ++n;
+        return n;
+    }
+
+    void fwd_level(cudaStream_t st, const R* sig, int l) {
+        const Game& g = *gp;
+        const long long s0 = g.slot_ptr[l], s1 = g.slot_ptr[l + 1];
+        if (s1 <= s0) return;
+        const long long n = s1 - s0;
+        const int threads = 256;
+        const long long blocks = std::min<long long>((n + threads - 1) / threads, 148LL * 16);
+        if (g.P == 2)
+            k_fwd<R, I, 2><<<(unsigned)blocks, threads, 0, st>>>(dg, sig, s0, s1);
+        else
+            k_fwd<R, I, 0><<<(unsigned)blocks, threads, 0, st>>>(dg, sig, s0, s1);
+    }
+
+    template <int MODE>
+    void bwd_level(cudaStream_t st, const R* sig, int L, int br_player, int last) {
+        const Game& g = *gp;
+        const long long t0 = g.tile_ptr[L], t1 = g.tile_ptr[L + 1];
+        if (t1 <= t0) return;
+        const size_t sm = smem_bytes();
+        const unsigned nb = (unsigned)(t1 - t0);
+        switch (g.Pc) {
+            case 1: k_bwd<R, I, 1, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last); break;
+            case 2: k_bwd<R, I, 2, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last); break;
+            case 3: k_bwd<R, I, 3, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last); break;
+            default: k_bwd<R, I, 4, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last); break;
+        }
+    }
+
+    void deferred_update(cudaStream_t st, int last) {
+        const long long n = dg.ndef;
+        const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 8));
+        k_deferred<R, I><<<blocks, 256, 0, st>>>(dg, last);
+    }
+
+    // One iteration: forward levels, backward levels (fused update), deferred update.
+    // `ev` (optional) receives events around each launch for profiling.
+    cfr_status launch_iteration(cudaStream_t st, std::vector<cudaEvent_t>* ev) {
+        const Game& g = *gp;
+        const bool has_def = !g.deferred_list.empty();
+        auto mark = [&]() {
+            if (ev) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                cudaEventRecord(e, st);
+                ev->push_back(e);
+            }
+        };
+        mark();
+        for (int l = 1; l < g.D; ++l) {
+            fwd_level(st, dg.sig, l);
+            mark();
+        }
+        for (int L = g.D - 1; L >= 0; --L) {
+            bwd_level<MODE_CFR>(st, dg.sig, L, 0, (L == 0 && !has_def) ? 1 : 0);
+            mark();
+        }
+        if (has_def) {
+            deferred_update(st, 1);
+            mark();
+        }
+        CU(cudaGetLastError());
+        return CFR_OK;
+    }
+
+    cfr_status enqueue(int64_t iters) override {
+        if (gp->NS == 0) return CFR_OK;   // one-node game: nothing to iterate
+        for (int64_t k = 0; k < iters; ++k) {
+            if (gexec) CU(cudaGraphLaunch(gexec, stream));
+            else {
+                cfr_status s = launch_iteration(stream, nullptr);
+                if (s) return s;
+            }
+        }
+        return CFR_OK;
+    }
+
+    cfr_status sync() override {
+        CU(cudaStreamSynchronize(stream));
+        long long c[2];
+        CU(cudaMemcpy(c, dg.ctrl, sizeof(c), cudaMemcpyDeviceToHost));
+        if (c[1] != LLONG_MAX) {
+            cfrb_set_error("NaN/Inf in regrets or strategy at iteration " + std::to_string(c[1]));
+            return CFR_ERR_NUMERICAL;
+        }
+        return CFR_OK;
+    }
+
+    cfr_status iteration(int64_t* T) override {
+        CU(cudaStreamSynchronize(stream));
+        long long c;
+        CU(cudaMemcpy(&c, dg.ctrl, sizeof(c), cudaMemcpyDeviceToHost));
+        *T = c;
+        return CFR_OK;
+    }
+
+    // device buffer (internal q order) -> host doubles in caller order
+    cfr_status read_q(const R* dptr, double* out) {
+        const Game& g = *gp;
+        std::vector<R> tmp(g.Q);
+        if (g.Q) CU(cudaMemcpyAsync(tmp.data(), dptr, g.Q * sizeof(R), cudaMemcpyDeviceToHost, stream));
+        CU(cudaStreamSynchronize(stream));
+        for (int64_t hc = 0; hc < g.H; ++hc) {
+            const int64_t hi = g.h_int_of_caller[hc];
+            const int64_t n = g.qbase_caller[hc + 1] - g.qbase_caller[hc];
+            for (int64_t a = 0; a < n; ++a) out[g.qbase_caller[hc] + a] = (double)tmp[g.qbase_int[hi] + a];
+        }
+        return CFR_OK;
+    }
+
+    cfr_status compute_average() {
+        const Game& g = *gp;
+        const long long n = std::max<long long>(g.H, g.C);
+        const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 8));
+        k_average<R, I><<<blocks, 256, 0, stream>>>(dg, at<R>(plan.sig_eval), g.H, g.Q, g.C);
+        CU(cudaGetLastError());
+        return CFR_OK;
+    }
+
+    cfr_status strategy(int which, double* out) override {
+        CU(cudaStreamSynchronize(stream));
+        if (which == 0) {
+            cfr_status s = compute_average();
+            if (s) return s;
+            return read_q(at<R>(plan.sig_eval), out);
+        }
+        return read_q(dg.sig, out);
+    }
+
+    cfr_status get_state(double* regret, double* snum, double* sden) override {
+        const Game& g = *gp;
+        cfr_status s;
+        if (regret && (s = read_q(dg.regret, regret))) return s;
+        if (snum && (s = read_q(dg.snum, snum))) return s;
+        if (sden) {
+            std::vector<R> tmp(g.H);
+            if (g.H) CU(cudaMemcpyAsync(tmp.data(), dg.sden, g.H * sizeof(R), cudaMemcpyDeviceToHost, stream));
+            CU(cudaStreamSynchronize(stream));
+            for (int64_t hc = 0; hc < g.H; ++hc) sden[hc] = (double)tmp[g.h_int_of_caller[hc]];
+        }
+        return CFR_OK;
+    }
+
+    // values-only backward pass under `sig` -> root values (P entries, double)
+    cfr_status root_values(const R* sig, double* out) {
+        const Game& g = *gp;
+        for (int L = g.D - 1; L >= 0; --L) bwd_level<MODE_VALUES>(stream, sig, L, 0, 0);
+        CU(cudaGetLastError());
+        std::vector<R> r(g.Pc);
+        CU(cudaMemcpyAsync(r.data(), dg.U, g.Pc * sizeof(R), cudaMemcpyDeviceToHost, stream));
+        CU(cudaStreamSynchronize(stream));
+        if (g.zero_sum_2p) {
+            out[0] = (double)r[0];
+            out[1] = (double)(-r[0]);
+        } else {
+            for (int j = 0; j < g.P; ++j) out[j] = (double)r[j];
+        }
+        return CFR_OK;
+    }
+
+    cfr_status expected_values(int which, double* out) override {
+        CU(cudaStreamSynchronize(stream));
+        const R* sig = dg.sig;
+        if (which == CFR_EV_AVERAGE) {
+            cfr_status s = compute_average();
+            if (s) return s;
+            sig = at<R>(plan.sig_eval);
+        }
+        return root_values(sig, out);
+    }
+
+    cfr_status exploitability(double* nc, double* ex, double* br) override {
+        const Game& g = *gp;
+        if (!g.depth_homogeneous || !g.deferred_list.empty()) {
+            cfrb_set_error("device best response needs every infoset on one depth and inside one tile (reading Q17)");
+            return CFR_ERR_UNSUPPORTED;
+        }
+        CU(cudaStreamSynchronize(stream));
+        cfr_status s = compute_average();
+        if (s) return s;
+        const R* sig = at<R>(plan.sig_eval);
+        double ev[16];
+        if ((s = root_values(sig, ev))) return s;
+        // forward pass under sigma_bar: pi_check(., i) for every player
+        for (int l = 1; l < g.D; ++l) fwd_level(stream, sig, l);
+        double total = 0.0;
+        for (int i = 1; i <= g.P; ++i) {
+            for (int L = g.D - 1; L >= 0; --L) bwd_level<MODE_BR>(stream, sig, L, i, 0);
+            CU(cudaGetLastError());
+            std::vector<R> r(g.Pc);
+            CU(cudaMemcpyAsync(r.data(), dg.U, g.Pc * sizeof(R), cudaMemcpyDeviceToHost, stream));
+            CU(cudaStreamSynchronize(stream));
+            double b;
+            if (g.zero_sum_2p) b = (i == 1) ? (double)r[0] : (double)(-r[0]);
+            else b = (double)r[i - 1];
+            if (br) br[i - 1] = b;
+            total = total + (b - ev[i - 1]);
+        }
+        // restore the reach arrays of the current strategy is unnecessary: every
+        // iteration recomputes them.  Root reach stays 1.
+        *nc = total;
+        *ex = total / (double)g.P;
+        return CFR_OK;
+    }
+
+    cfr_status launches(int64_t* n) override {
+        *n = launches_per_iter;
+        return CFR_OK;
+    }
+
+    cfr_status profile(int64_t iters, double* out) override {
+        const Game& g = *gp;
+        for (int k = 0; k < 5; ++k) out[k] = 0.0;
+        if (g.NS == 0 || iters <= 0) return CFR_OK;
+        std::vector<double> per_bwd(g.D, 0.0);
+        for (int64_t it = 0; it < iters; ++it) {
+            std::vector<cudaEvent_t> ev;
+            cfr_status s = launch_iteration(stream, &ev);
+            if (s) return s;
+            CU(cudaStreamSynchronize(stream));
+            size_t e = 1;
+            for (int l = 1; l < g.D; ++l, ++e) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, ev[e - 1], ev[e]);
+                out[0] += ms;
+            }
+            for (int L = g.D - 1; L >= 0; --L, ++e) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, ev[e - 1], ev[e]);
+                out[1] += ms;
+                per_bwd[L] += ms;
+            }
+            if (!g.deferred_list.empty()) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, ev[e - 1], ev[e]);
+                out[2] += ms;
+            }
+            for (auto x : ev) cudaEventDestroy(x);
+        }
+        int dom = 0;
+        for (int L = 0; L < g.D; ++L)
+            if (per_bwd[L] > per_bwd[dom]) dom = L;
+        out[0] /= iters;
+        out[1] /= iters;
+        out[2] /= iters;
+        out[3] = per_bwd[dom] / iters;
+        out[4] = dom;
+        return sync();
+    }
+
+    // Algorithmic DRAM bytes per iteration (DESIGN.md §6 byte model).
+    cfr_status model_bytes(double* out) override {
+        const Game& g = *gp;
+        const double w = sizeof(R), ix = sizeof(I);
+        const int P = g.P, Pc = g.Pc;
+        double fwd = 0, bwd = 0, upd = 0, dom = 0;
+        int64_t dom_nodes = -1;
+        for (int l = 1; l < g.D; ++l) {
+            const double n = (double)(g.slot_ptr[l + 1] - g.slot_ptr[l]);
+            // per decision node: parent slot + edge index + parent actor, write 2P factors;
+            // parent factors are re-read by siblings (counted once per parent below)
+            fwd += n * (2 * ix + 1 + 2 * P * w);
+            fwd += (double)(g.slot_ptr[l] - g.slot_ptr[l - 1]) * 2 * P * w;
+        }
+        for (int L = g.D - 1; L >= 0; --L) {
+            const double parents = (double)(g.slot_ptr[L + 1] - g.slot_ptr[L]);
+            const double children = (double)(g.level_ptr[L + 2] - g.level_ptr[L + 1]);
+            // children values read once; parent: node, cb, n, ebase, actor; value write;
+            // acting player's pi_check and pi_hat
+            const double b = children * Pc * w + parents * (3 * ix + 4 + 1 + Pc * w + 2 * w);
+            bwd += b;
+            if (g.level_ptr[L + 2] - g.level_ptr[L + 1] > dom_nodes) {
+                dom_nodes = g.level_ptr[L + 2] - g.level_ptr[L + 1];
+                dom = b;
+            }
+        }
+        // update per pair: regret r/w, snum r/w, sigma r/w; per infoset: sden r/w
+        upd = (double)g.Q * 6 * w + (double)g.H * 2 * w;
+        out[0] = fwd + bwd + upd;
+        out[1] = fwd;
+        out[2] = bwd;
+        out[3] = upd;
+        out[4] = dom;
+        return CFR_OK;
+    }
+};
+
+static bool use_idx32(const Game& g) {
+    const int64_t lim = (int64_t(1) << 31) - 2;
+    return g.V < lim && (g.Q + g.C) < lim && g.NS < lim;
+}
+
+static cfr_status bytes_for(const Game& g, int precision, size_t* out) {
+    const bool i32 = use_idx32(g);
+    if (precision == 64) *out = i32 ? Plan<double, int>(g).total : Plan<double, long long>(g).total;
+    else *out = i32 ? Plan<float, int>(g).total : Plan<float, long long>(g).total;
+    return CFR_OK;
+}
+
+}  // namespace cfrb
+
+using namespace cfrb;
+
+struct cfr_solver {
+    std::unique_ptr<SolverBase> impl;
+};
+
+extern "C" {
+
+cfr_status cfr_solver_workspace_bytes(const cfr_game* g, const cfr_solver_config* cfg, const cfr_dist* dist,
+                                      size_t* bytes) {
+    if (!g || !cfg || !bytes) { cfrb_set_error("NULL argument"); return CFR_ERR_INVALID_ARG; }
+    if (cfg->precision != 64 && cfg->precision != 32) { cfrb_set_error("precision must be 64 or 32"); return CFR_ERR_INVALID_ARG; }
+    if (dist && dist->world_size > 1) { cfrb_set_error("multi-GPU sharding not built in this version"); return CFR_ERR_UNSUPPORTED; }
+    return bytes_for(g->g, cfg->precision, bytes);
+}
+
+cfr_status cfr_solver_create(const cfr_game* g, const cfr_solver_config* cfg, void* workspace, size_t workspace_bytes,
+                             void* stream, const cfr_dist* dist, cfr_solver** out) {
+    if (!g || !cfg || !out || !workspace) { cfrb_set_error("NULL argument"); return CFR_ERR_INVALID_ARG; }
+    *out = nullptr;
+    if (cfg->variant != CFR_VANILLA && cfg->variant != CFR_PLUS) { cfrb_set_error("bad variant"); return CFR_ERR_INVALID_ARG; }
+    if (cfg->precision != 64 && cfg->precision != 32) { cfrb_set_error("precision must be 64 or 32"); return CFR_ERR_INVALID_ARG; }
+    if (dist && dist->world_size > 1) { cfrb_set_error("multi-GPU sharding not built in this version"); return CFR_ERR_UNSUPPORTED; }
+    size_t need = 0;
+    bytes_for(g->g, cfg->precision, &need);
+    if (workspace_bytes < need) {
+        cfrb_set_error("workspace too small: need " + std::to_string(need) + " bytes");
+        return CFR_ERR_OOM;
+    }
+    if (((uintptr_t)workspace & 255) != 0) { cfrb_set_error("workspace must be 256-byte aligned"); return CFR_ERR_INVALID_ARG; }
+    const bool i32 = use_idx32(g->g);
+    std::unique_ptr<SolverBase> impl;
+    cudaStream_t st = (cudaStream_t)stream;
+    cfr_status s;
+    if (cfg->precision == 64) {
+        if (i32) { auto p = new Solver<double, int>(&g->g, *cfg, workspace, st); impl.reset(p); s = p->init(); }
+        else { auto p = new Solver<double, long long>(&g->g, *cfg, workspace, st); impl.reset(p); s = p->init(); }
+    } else {
+        if (i32) { auto p = new Solver<float, int>(&g->g, *cfg, workspace, st); impl.reset(p); s = p->init(); }
+        else { auto p = new Solver<float, long long>(&g->g, *cfg, workspace, st); impl.reset(p); s = p->init(); }
+    }
+    if (s != CFR_OK) return s;
+    *out = new cfr_solver{std::move(impl)};
+    return CFR_OK;
+}
+
+void cfr_solver_destroy(cfr_solver* s) { delete s; }
+
+#define CHK_S(s) \
+    if (!(s)) { cfrb_set_error("NULL solver"); return CFR_ERR_INVALID_ARG; }
+
+cfr_status cfr_solver_enqueue(cfr_solver* s, int64_t iterations) {
+    CHK_S(s);
+    if (iterations < 0) { cfrb_set_error("iterations < 0"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->enqueue(iterations);
+}
+cfr_status cfr_solver_sync(cfr_solver* s) {
+    CHK_S(s);
+    return s->impl->sync();
+}
+cfr_status cfr_solver_run(cfr_solver* s, int64_t iterations) {
+    CHK_S(s);
+    cfr_status st = cfr_solver_enqueue(s, iterations);
+    if (st) return st;
+    return s->impl->sync();
+}
+cfr_status cfr_solver_iteration(cfr_solver* s, int64_t* T) {
+    CHK_S(s);
+    if (!T) { cfrb_set_error("NULL T"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->iteration(T);
+}
+cfr_status cfr_solver_average_strategy(cfr_solver* s, double* out) {
+    CHK_S(s);
+    if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->strategy(0, out);
+}
+cfr_status cfr_solver_current_strategy(cfr_solver* s, double* out) {
+    CHK_S(s);
+    if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->strategy(1, out);
+}
+cfr_status cfr_solver_get_state(cfr_solver* s, double* regret, double* s_num, double* s_den) {
+    CHK_S(s);
+    return s->impl->get_state(regret, s_num, s_den);
+}
+cfr_status cfr_solver_expected_values(cfr_solver* s, int32_t which, double* out) {
+    CHK_S(s);
+    if (!out || (which != CFR_EV_AVERAGE && which != CFR_EV_CURRENT)) { cfrb_set_error("bad argument"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->expected_values(which, out);
+}
+cfr_status cfr_solver_exploitability(cfr_solver* s, double* nash_conv, double* exploitability, double* br) {
+    CHK_S(s);
+    if (!nash_conv || !exploitability) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->exploitability(nash_conv, exploitability, br);
+}
+cfr_status cfr_solver_launches_per_iteration(cfr_solver* s, int64_t* launches) {
+    CHK_S(s);
+    if (!launches) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->launches(launches);
+}
+cfr_status cfr_solver_profile(cfr_solver* s, int64_t iterations, double* out_ms) {
+    CHK_S(s);
+    if (!out_ms) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->profile(iterations, out_ms);
+}
+cfr_status cfr_solver_model_bytes(cfr_solver* s, double* out) {
+    CHK_S(s);
+    if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->model_bytes(out);
+}
+cfr_status cfr_nccl_unique_id(void* out) {
+    (void)out;
+    cfrb_set_error("multi-GPU sharding not built in this version");
+    return CFR_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"
