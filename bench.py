@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of one CFR+ iteration on the B200 -- bench contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A "step" is one full CFR iteration (all §8(a) rows: forward reach pass, backward
+value pass, exact per-infoset aggregation, fused regret / average-strategy update
+and regret matching) over the workload, default = BASELINE.json configs[4]: the
+synthetic battleship-shaped tree (965,153,641 nodes, 1,206,440 infosets), f64,
+CFR+.  Inputs are resident in HBM; the working set (~13 GB per iteration) is far
+larger than the 126 MB L2, so no flush is needed between iterations.
+
+Rank 0 prints ONE JSON line.  `value` = iterations/s (whole job), `ms_per_step`
+from CUDA events on the solver's stream, max over ranks.  The `reference` arm
+times the CPU oracle (test infrastructure) on a bounded sample of the same
+workload and reports the same metric extrapolated by node count (the oracle's
+cost is linear in V).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import gamegen  # noqa: E402
+
+METRIC = "CFR iterations/sec (node-updates/sec = V x it/s; achieved HBM GB/s vs peak)"
+UNIT = "it/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n-types", type=int, default=40, help="synthetic size (40 = configs[4], ~1e9 nodes)")
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
+    ap.add_argument("--variant", default="cfr+", choices=["cfr", "cfr+"])
+    ap.add_argument("--no-games", action="store_true", help="skip the per-game (Kuhn/Leduc/...) lines")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--cpu-sample-types", type=int, default=4)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def ncu_traffic(n_types: int, precision: int):
+    """dram__bytes_read+write per launch of the dominant kernel, from the committed
+    ncu --set full summary (profiles/ncu_dominant.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_dominant.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        key = f"n{n_types}_f{precision}"
+        return d.get(key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(n_types: int, variant: int, precision: int, seconds: float, V_full: int):
+    """The oracle (as it stands) on a bounded sample of the workload, 1 core."""
+    import oracle
+
+    d = gamegen.synthetic(n_types=n_types)
+    o = oracle.Oracle(d, precision=precision)
+    del d
+    t0 = time.perf_counter()
+    it = 0
+    while True:
+        o.run(1, variant)
+        it += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    node_s = o.V * it / dt
+    return {
+        "value": node_s / V_full,
+        "unit": UNIT,
+        "cores": 1,
+        "kind": "oracle",
+        "node_updates_per_s": node_s,
+        "sample": (f"synthetic n_types={n_types} ({o.V:,} nodes = {100.0 * o.V / V_full:.2f}% of the "
+                   f"workload), {it} oracle iteration(s) in {dt:.1f} s; value = node-updates/s / V_workload"),
+    }
+
+
+def per_game(pb, torch, variant: str, precision: int):
+    """Secondary lines of the metric: it/s and node-updates/s per small game."""
+    out = {}
+    for name, iters in (("kuhn", 2000), ("leduc", 1000), ("goofspiel", 500), ("liars_dice", 500)):
+        d = gamegen.by_name(name)
+        g = pb.Game(d)
+        s = pb.Solver(g, variant=variant, precision=precision)
+        s.run(5)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s.stream)
+        s.enqueue(iters)
+        e1.record(s.stream)
+        s.sync()
+        ms = e0.elapsed_time(e1) / iters
+        out[name] = {"it_per_s": round(1e3 / ms, 1), "node_updates_per_s": float(f"{g.V * 1e3 / ms:.4g}"),
+                     "V": g.V, "launches_per_iter": s.launches_per_iteration()}
+        del s, g
+    return out
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    variant = 1 if args.variant == "cfr+" else 0
+    V_full = gamegen.synthetic_counts(args.n_types)["V"]
+    import oracle
+
+    d = gamegen.synthetic(n_types=args.cpu_sample_types)
+    o = oracle.Oracle(d, precision=args.precision)
+    del d
+    for _ in range(args.warmup):
+        o.run(1, variant)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.run(1, variant)
+    dt = time.perf_counter() - t0
+    node_s = o.V * args.steps / dt
+    value = node_s / V_full
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": f"f{args.precision}", "data": "synthetic",
+        "config": {"workload": f"synthetic_n{args.n_types}", "variant": args.variant,
+                   "sample": f"synthetic n_types={args.cpu_sample_types} ({o.V:,} nodes)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"synthetic n_types={args.cpu_sample_types} ({o.V:,} nodes), "
+                                   f"{args.steps} oracle iterations; value = node-updates/s / V_workload"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "node_updates_per_s": node_s,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_14778_b200 as pb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    variant = 1 if args.variant == "cfr+" else 0
+
+    # ---- setup (not timed): generate, flatten, upload
+    t0 = time.time()
+    desc = gamegen.synthetic(n_types=args.n_types, seed=0)
+    t_gen = time.time() - t0
+    t0 = time.time()
+    game = pb.Game(desc)
+    t_flat = time.time() - t0
+    del desc
+    t0 = time.time()
+    solver = pb.Solver(game, variant=args.variant, precision=args.precision, device=dev)
+    t_up = time.time() - t0
+    st = solver.stream
+
+    # ---- warm-up, then the timed region (CUDA events on the solver stream)
+    solver.run(args.warmup)
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    solver.enqueue(args.steps)
+    e1.record(st)
+    solver.sync()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    launches = solver.launches_per_iteration()
+
+    # ---- roofline of the dominant kernel (live CUDA events, un-graphed launches)
+    prof = solver.profile(5)
+    mb = solver.model_bytes()
+    peak, peak_src = peaks()
+    dom_ms = prof["dominant_ms"]
+    achieved = mb["dominant"] / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else None
+    roofline = {
+        "bound": "hbm", "kernel": f"k_bwd (parent level {prof['dominant_level']})",
+        "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
+        "frac": round(achieved / peak, 4) if achieved else None,
+        "traffic": ncu_traffic(args.n_types, args.precision),
+        "algorithmic_bytes_per_launch": mb["dominant"], "launch_ms": dom_ms, "peak_source": peak_src,
+        "step_share": round(dom_ms / (prof["fwd_ms"] + prof["bwd_ms"] + prof["deferred_ms"]), 4),
+        "whole_step_model_GBps": round(mb["total"] / (ms * 1e-3) / 1e9, 1),
+    }
+
+    # ---- end to end through the public API with host buffers
+    Q = solver.Q
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        solver.run(1)                       # enqueue + sync + 16-byte status D2H
+    avg = solver.average_strategy()         # sigma_bar D2H into a host buffer
+    e2e_dt = time.perf_counter() - t0
+    w = args.precision // 8
+    e2e = {"value": args.e2e_steps / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+           "d2h_bytes_per_step": int(16 + Q * w / args.e2e_steps),
+           "note": "per step: cfr_solver_run(1) (status read back); sigma_bar read back once per window"}
+    assert np.isfinite(avg).all()
+
+    games = None
+    if rank == 0 and not args.no_games:
+        games = per_game(pb, torch, args.variant, args.precision)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.cpu_sample_types, variant, args.precision, args.cpu_seconds, game.V)
+
+    if rank == 0:
+        value = world * 1e3 / ms   # replicas: every rank completed `steps` iterations
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": f"f{args.precision}", "data": "synthetic",
+            "config": {"workload": f"synthetic_n{args.n_types}: {game.V:,} nodes, D={game.D}, {game.H:,} infosets, "
+                                   f"{game.Q:,} (h,a) pairs (BASELINE.json configs[4], single GPU)",
+                       "variant": args.variant, "precision": f"f{args.precision}",
+                       "parallelism": "single GPU" if world == 1 else f"replicas x{world}",
+                       "l2": "no flush: per-iteration working set ~13 GB >> 126 MB L2",
+                       "setup_s": {"generate": round(t_gen, 1), "flatten": round(t_flat, 1),
+                                   "upload": round(t_up, 1)}},
+            "node_updates_per_s": float(f"{game.V * value:.4g}"),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches * args.steps),
+            "launches_per_step": launches,
+            "clocks": clk,
+            "per_game": games,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
