@@ -23,8 +23,8 @@ NVCC_FLAGS = [
     # IEEE arithmetic contract (reading Q9): no FMA contraction,
     # correctly rounded division/sqrt, no flush-to-zero, never --use_fast_math.
     "--fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
-    "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
-    "-shared",
+    "-Xcompiler", "-fPIC,-O2,-ffp-contract=off,-fopenmp",
+    "-shared", "-lgomp",
 ]
 
 _lock = threading.Lock()

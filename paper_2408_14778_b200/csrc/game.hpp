@@ -16,8 +16,12 @@ struct TileH {
     int64_t s0, s1;        // slot range
     int32_t seg0, seg1;    // segments [seg0, seg1) in Game::segs
     int32_t npairs;        // sum of |A(h)| over the tile's segments
+    int32_t nch;           // staged child elements (padded rows), <= kTileChildren if staged
+    int32_t run0, run1;    // (unused, 0)
+    int32_t staged;        // 1: children staged in shared memory
     int32_t pad;
 };
+
 
 // A segment = the member slots [sb, se) of internal infoset h inside one tile.
 struct SegH {
@@ -27,9 +31,10 @@ struct SegH {
     int32_t fused;         // 1: all members here, single depth -> update in-tile
 };
 
-constexpr int kTileSlots = 256;     // parents per tile (= threads per CTA)
-constexpr int kTilePairs = 1024;    // (infoset, action) pairs per tile
-constexpr int kTileSegs = 256;      // segments per tile
+constexpr int kTileSlots = 128;     // parents per tile (= threads per CTA)
+constexpr int kTilePairs = 512;     // (infoset, action) pairs per tile
+constexpr int kTileSegs = 64;       // segments (infosets) per tile
+constexpr int kTileChildren = 2560; // staged child values (R elements, padded rows)
 
 struct Game {
     // ---- input-level facts
@@ -47,6 +52,13 @@ struct Game {
     std::vector<int64_t> canon_of_input;  // [V]
     std::vector<int64_t> level_ptr;       // [D+2] canonical node ranges per depth
 
+    // ---- decision nodes in canonical order ("dec" index): forward pass + reach
+    int64_t ND = 0;
+    std::vector<int64_t> dec_ptr;         // [D+1]: decision nodes of depth l in [dec_ptr[l], dec_ptr[l+1])
+    std::vector<int64_t> f_parent;        // [ND] dec index of the parent (-1 root)
+    std::vector<int64_t> f_e;             // [ND] sigma_ext index of the incoming edge
+    std::vector<uint8_t> f_pact;          // [ND] actor of the parent
+
     // ---- slots: decision nodes, level-major, infoset-grouped
     int64_t NS = 0;
     std::vector<int64_t> slot_ptr;        // [D+1]: slots of depth L in [slot_ptr[L], slot_ptr[L+1])
@@ -55,9 +67,8 @@ struct Game {
     std::vector<int32_t> s_n;             // number of children
     std::vector<int64_t> s_ebase;         // base of the children's edge probs in sigma_ext
     std::vector<uint8_t> s_actor;         // 0 chance, 1..P player
-    std::vector<int64_t> s_parent;        // parent slot (-1 for the root)
-    std::vector<int64_t> s_e;             // sigma_ext index of the incoming edge
-    std::vector<uint8_t> s_pact;          // actor of the parent
+    std::vector<int64_t> s_dec;           // dec index (reach row)
+    std::vector<int32_t> s_coff;          // tile-local offset of the staged child row
 
     // ---- infosets, internal numbering (order of first appearance in slot order)
     int64_t H = 0, Q = 0, C = 0;          // infosets, pairs, chance edges

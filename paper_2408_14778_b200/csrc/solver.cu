@@ -32,72 +32,96 @@
 
 namespace cfrb {
 
-// device mirrors of TileH / SegH (identical layout, copied bytewise)
+// Device tile / segment records (built by the solver from the game's TileH /
+// SegH plus the precision-dependent staging layout).
 struct TileD {
-    long long s0, s1;
-    int seg0, seg1;
-    int npairs;
-    int pad;
+    long long s0, s1;    // slot range
+    int seg0, seg1;      // segments
+    int npairs;          // (h, a) pairs of the tile's segments
+    int staged;          // 0: children read from global; 1: uniform rows, chunked; 2: generic rows
+    int rowlen;          // elements per row (mode 1)
+    int cpr;             // chunks per row (mode 1)
+    int stride;          // row stride in elements (mode 1)
+    float inv_cpr;       // 1 / cpr
 };
 struct SegD {
-    long long h, sb, se;
-    int pair_off;
-    int fused;
+    long long h, qb;     // internal infoset, qbase[h]
+    long long sb, se;    // member slots
+    int pair_off, n, owner, fused;
 };
-static_assert(sizeof(TileD) == sizeof(TileH), "TileD layout");
-static_assert(sizeof(SegD) == sizeof(SegH), "SegD layout");
 
 enum { MODE_CFR = 0, MODE_VALUES = 1, MODE_BR = 2 };
 
 template <class R, class I>
 struct DG {
     R* U;          // [V * Pc] node values, canonical order; terminal rows = u
-    R* reach;      // [2P][NS]: rows 0..P-1 pi_check(., i), rows P..2P-1 pi_hat(., i)
+    R* reach;      // [ND][2P] AoS, canonical decision order: pi_check(., 1..P), pi_hat(., 1..P)
     R* sig;        // [Q + C] sigma_ext = current strategy (internal q order) | chance
     R* regret;     // [Q] cumulative regret
     R* snum;       // [Q] sum_t w_t pi_bar sigma
     R* sden;       // [H] sum_t w_t pi_bar
     unsigned long long* acc_r;  // [Q][3] exact slices (deferred infosets)
     unsigned long long* acc_p;  // [H][3]
-    const I* s_node;
+    const I* f_parent;            // [ND] forward pass (canonical decision order)
+    const I* f_e;
+    const unsigned char* f_pact;
+    const I* s_node;              // [NS] backward pass (slot order)
     const I* s_cb;
     const int* s_n;
     const I* s_ebase;
     const unsigned char* s_actor;
-    const I* s_parent;
-    const I* s_e;
-    const unsigned char* s_pact;
+    const I* s_dec;
+    const int* s_coff;
     const I* qbase;               // [H+1] internal
     const unsigned char* owner;   // [H]
     const TileD* tiles;
     const SegD* segs;
     const I* deferred;            // [ndef]
     long long* ctrl;              // [0] iterations done, [1] first bad iteration, [2] done counter
-    long long NS;
     long long ndef;
     int P;
     int variant;
-    double sc[3], rc[3];          // 2^(40k-E), 2^(E-40k): regret / BR sums
-    double scp[3], rcp[3];        // same with E = 1: pi_bar sums
+    double sc0, rc[3];            // 2^(40-E), 2^(E-40k): regret / BR sums
+    double scp0, rcp[3];          // same with E = 1: pi_bar sums
 };
 
 // ---------------------------------------------------------------- exact sums
-// Three 40-bit int64 slices.  x*2^(40k-E)
-// and c*2^(E-40k) are exact power-of-two scalings; __double2ll_rn rounds half to
-// even; the remainder subtraction is exact.  Sums of slices are order-free.
-__device__ __forceinline__ void xadd(long long (&c)[3], double x, const double (&sc)[3], const double (&rc)[3]) {
-    const long long k0 = __double2ll_rn(x * sc[0]);
-    x = x - __ll2double_rn(k0) * rc[0];
-    const long long k1 = __double2ll_rn(x * sc[1]);
-    x = x - __ll2double_rn(k1) * rc[1];
-    const long long k2 = __double2ll_rn(x * sc[2]);
-    c[0] += k0;
-    c[1] += k1;
-    c[2] += k2;
+// Three 40-bit slices per term:
+// c_k = rint(x * 2^(40k-E)), x <- x - c_k 2^(E-40k).  Implemented with FP64 adds
+// only: y = x*2^(40-E) is exact; rint(y) = (y + 1.5*2^52) - 1.5*2^52 (round half
+// to even, |y| < 2^51); y - c is exact and y' = (y - c) * 2^40 is the next slice's
+// input, identical to x_k * 2^(40(k+1)-E).  The slices are integers, so partial
+// sums of <= 2^13 of them are exact in binary64; they are converted to int64 only
+// for global accumulation.  decode = ((C1 2^(E-40) + C2 2^(E-80)) + C3 2^(E-120)).
+__device__ __forceinline__ double rint_magic(double y) {
+    const double M = 6755399441055744.0;  // 1.5 * 2^52
+    return (y + M) - M;
 }
-__device__ __forceinline__ double xdec(long long c0, long long c1, long long c2, const double (&rc)[3]) {
+__device__ __forceinline__ void xadd(double& a0, double& a1, double& a2, double x, double sc0) {
+    double y = x * sc0;
+    const double c0 = rint_magic(y);
+    y = (y - c0) * 1099511627776.0;   // 2^40
+    const double c1 = rint_magic(y);
+    y = (y - c1) * 1099511627776.0;
+    const double c2 = rint_magic(y);
+    a0 += c0;
+    a1 += c1;
+    a2 += c2;
+}
+__device__ __forceinline__ double xdec(double c0, double c1, double c2, const double (&rc)[3]) {
+    return (c0 * rc[0] + c1 * rc[1]) + c2 * rc[2];
+}
+__device__ __forceinline__ double xdec_ll(long long c0, long long c1, long long c2, const double (&rc)[3]) {
     return (__ll2double_rn(c0) * rc[0] + __ll2double_rn(c1) * rc[1]) + __ll2double_rn(c2) * rc[2];
 }
+
+// cp.async (LDGSTS): global -> shared without register staging, many in flight.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 template <class R>
 __device__ __forceinline__ bool finite_(R x) {
@@ -105,131 +129,293 @@ __device__ __forceinline__ bool finite_(R x) {
 }
 
 // ------------------------------------------------------------ forward pass
-// Decision nodes of one depth, slot order.  Eq 2: pi_check(v,i) =
+// Decision nodes of one depth in canonical order (streaming reads of the
+// parents' rows, streaming writes).  Eq 2: pi_check(v,i) =
 // pi_check(parent,i) * (sigma if the parent's actor != i else 1); Eq 4 (P:97,
 // reading Q1): pi_hat(v,i) = pi_hat(parent,i) * (sigma if actor == i else 1).
 template <class R, class I, int PT>
-__global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ sig, long long s_begin,
-                                             long long s_end) {
+__global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ sig, long long d_begin,
+                                             long long d_end) {
     const int P = (PT > 0) ? PT : g.P;
-    const long long NS = g.NS;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long s = s_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; s < s_end; s += stride) {
-        const long long p = (long long)g.s_parent[s];
-        const R x = sig[g.s_e[s]];
-        const int act = g.s_pact[s];
+    for (long long d = d_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; d < d_end; d += stride) {
+        const long long p = (long long)g.f_parent[d];
+        const R x = sig[g.f_e[d]];
+        const int act = g.f_pact[d];
+        const R* __restrict__ src = g.reach + p * 2 * P;
+        R* __restrict__ dst = g.reach + d * 2 * P;
 #pragma unroll
         for (int j = 0; j < ((PT > 0) ? PT : 16); ++j) {
             if (PT == 0 && j >= P) break;
-            const R pc = g.reach[j * NS + p];
-            g.reach[j * NS + s] = (act != j + 1) ? pc * x : pc;
-            const R ph = g.reach[(P + j) * NS + p];
-            g.reach[(P + j) * NS + s] = (act == j + 1) ? ph * x : ph;
+            const R pc = src[j];
+            const R ph = src[P + j];
+            dst[j] = (act != j + 1) ? pc * x : pc;
+            dst[P + j] = (act == j + 1) ? ph * x : ph;
         }
     }
 }
 
 // ----------------------------------------------------------- backward pass
-// Shared memory of one tile (dynamic).
-template <class R, int PC>
-struct TileSmem {
-    R sv[kTileSlots * PC];   // node values of the tile's slots
-    R rt[kTilePairs];        // decoded r~ (or BR sums)
-    R pos[kTilePairs];       // positive regrets
-    R pib[kTileSegs];        // decoded pi_bar per segment
-    R zs[kTileSegs];         // sum of positive regrets per segment
-    int soff[kTileSegs + 1]; // pair offsets of the tile's segments
-    int best[kTileSegs];     // BR argmax per segment
+// One CTA (kTileSlots threads) per tile of whole infosets.  Global memory is
+// touched in three dependency steps only (metadata; reach + sigma + children +
+// update state; writes), everything else runs out of shared memory.
+struct SegS {
+    long long h;     // internal infoset
+    long long qb;    // qbase[h]
+    int sb, se;      // tile-local member slots
+    int pair_off;    // first pair of the segment in the tile
+    int n;           // |A(h)|
+    int owner;       // acting player
+    int fused;
 };
 
+template <class R, int PC>
+struct TileSmem {
+    R ch[kTileChildren];         // staged child rows (odd strides, conflict-free row reads)
+    R sv[kTileSlots * PC];       // node values of the tile's slots
+    R spc[kTileSlots];           // owner's pi_check per slot
+    R sph[kTileSlots];           // owner's pi_hat per slot
+    R ssig[kTilePairs];          // sigma of the tile's (h, a) pairs
+    R sreg[kTilePairs];          // regret of the tile's pairs (prefetched for the update)
+    R ssn[kTilePairs];           // S_num of the tile's pairs (prefetched)
+    R pib[kTileSegs];            // decoded pi_bar per segment
+    R zs[kTileSegs];             // sum of positive regrets per segment
+    R sden[kTileSegs];           // S_den per segment (prefetched)
+    SegS seg[kTileSegs];
+    int soff[kTileSegs + 1];     // pair offsets of the segments
+    int best[kTileSegs];         // BR argmax per segment
+    int scoff[kTileSlots];       // staged row offset per slot
+    int spoff[kTileSlots];       // pair offset of the slot's segment (-1 chance)
+    long long scb[kTileSlots];   // first child per slot
+    int sn[kTileSlots];          // children per slot
+    unsigned char pseg[kTilePairs];  // segment of each pair
+};
+// rt / pos alias ch after phase B
+static_assert(kTileChildren >= 2 * kTilePairs, "alias");
+
+__device__ __forceinline__ int seg_of_pair(const int* soff, int nseg, int p) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (soff[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
 template <class R, class I, int PC, int MODE>
-__global__ void __launch_bounds__(256) k_bwd(DG<R, I> g, const R* __restrict__ sig, long long tile0, int br_player,
-                                             int last) {
+__global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restrict__ sig, long long tile0,
+                                                    int br_player, int last) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem<R, PC>& sm = *reinterpret_cast<TileSmem<R, PC>*>(smem_raw);
     const TileD T = g.tiles[tile0 + blockIdx.x];
     const int nslot = (int)(T.s1 - T.s0);
-    const int tid = threadIdx.x, nth = blockDim.x;
-
-    // Phase A: node values, Eq 1 in ascending action order from +0.
-    for (int ls = tid; ls < nslot; ls += nth) {
-        const long long s = T.s0 + ls;
-        const long long cb = (long long)g.s_cb[s];
-        const int n = g.s_n[s];
-        const long long eb = (long long)g.s_ebase[s];
-        R v[PC];
-#pragma unroll
-        for (int j = 0; j < PC; ++j) v[j] = (R)0;
-        for (int a = 0; a < n; ++a) {
-            const R x = sig[eb + a];
-#pragma unroll
-            for (int j = 0; j < PC; ++j) v[j] = v[j] + x * g.U[(cb + a) * PC + j];
-        }
-        const bool skip = (MODE == MODE_BR) && ((int)g.s_actor[s] == br_player);
-        if (!skip) {
-            const long long nd = (long long)g.s_node[s];
-#pragma unroll
-            for (int j = 0; j < PC; ++j) g.U[nd * PC + j] = v[j];
-        }
-#pragma unroll
-        for (int j = 0; j < PC; ++j) sm.sv[ls * PC + j] = v[j];
-    }
-    if (MODE == MODE_VALUES) return;
-
     const int nseg = T.seg1 - T.seg0;
-    for (int k = tid; k < nseg; k += nth) sm.soff[k] = g.segs[T.seg0 + k].pair_off;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+    const int P = g.P;
+    R* const rt = sm.ch;                  // valid after phase B
+    R* const pos = sm.ch + kTilePairs;
+    const bool sig_staged = T.npairs <= kTilePairs;
+    const bool staged = T.staged != 0;
+    constexpr int CH = (sizeof(R) == 8) ? 16 : 8;     // cp.async chunk (bytes) of uniform tiles
+    constexpr int CE = CH / (int)sizeof(R);            // elements per chunk
+    const long long t_iter = (MODE == MODE_CFR) ? g.ctrl[0] + 1 : 0;
+
+    // ---- step 1: per-slot metadata (thread = slot), owner reach, segment + run tables
+    long long my_node = 0, my_cb = 0, my_eb = 0;
+    int my_n = 0, my_actor = 0;
+    if (tid < nslot) {
+        const long long s = T.s0 + tid;
+        my_node = (long long)g.s_node[s];
+        my_cb = (long long)g.s_cb[s];
+        my_n = g.s_n[s];
+        my_eb = (long long)g.s_ebase[s];
+        my_actor = g.s_actor[s];
+        sm.scoff[tid] = g.s_coff[s];
+        sm.scb[tid] = my_cb;
+        sm.sn[tid] = my_n;
+        sm.spoff[tid] = -1;
+        if (MODE != MODE_VALUES && my_actor >= 1) {
+            const long long dd = (long long)g.s_dec[s];
+            sm.spc[tid] = g.reach[dd * 2 * P + (my_actor - 1)];
+            sm.sph[tid] = g.reach[dd * 2 * P + P + (my_actor - 1)];
+        }
+    }
+    if (tid < nseg) {
+        const SegD sg = g.segs[T.seg0 + tid];
+        SegS ss;
+        ss.h = sg.h;
+        ss.qb = sg.qb;
+        ss.n = sg.n;
+        ss.owner = sg.owner;
+        ss.sb = (int)(sg.sb - T.s0);
+        ss.se = (int)(sg.se - T.s0);
+        ss.pair_off = sg.pair_off;
+        ss.fused = sg.fused;
+        sm.seg[tid] = ss;
+        sm.soff[tid] = sg.pair_off;
+        if (MODE == MODE_CFR && sg.fused) sm.sden[tid] = g.sden[sg.h];
+    }
     if (tid == 0) sm.soff[nseg] = T.npairs;
     __syncthreads();
 
-    const long long NS = g.NS;
-    const int P = g.P;
-    long long t_iter = 0;
-    if (MODE == MODE_CFR) t_iter = g.ctrl[0] + 1;
-
-    // Phase B: per (infoset, action) exact sums over the infoset's member slots.
-    for (int p = tid; p < T.npairs; p += nth) {
-        int lo = 0, hi = nseg - 1;            // last segment with soff <= p
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (sm.soff[mid] <= p) lo = mid; else hi = mid - 1;
+    // ---- step 2: children (cp.async, every lane keeps issuing; nothing waits
+    // until cp.async.wait_all), sigma and update state of the tile's pairs
+    if (T.staged == 1) {
+        // uniform rows: flat loop over 16-B (f64) / 8-B (f32) chunks, all lanes busy
+        const int total = nslot * T.cpr;
+        for (int c = tid; c < total; c += nth) {
+            const int row = __float2int_rd(((float)c + 0.5f) * T.inv_cpr);
+            const int k = c - row * T.cpr;
+            cp_async<CH>(sm.ch + row * T.stride + k * CE, g.U + sm.scb[row] * PC + k * CE);
         }
-        const SegD sg = g.segs[T.seg0 + lo];
-        const int a = p - sm.soff[lo];
-        const long long h = sg.h;
-        const int i = g.owner[h];
-        const int col = (PC == 1) ? 0 : i - 1;
-        if (MODE == MODE_BR && i != br_player) continue;
-        long long c[3] = {0, 0, 0};
-        long long cp[3] = {0, 0, 0};
-        const bool neg = (PC == 1) && (i == 2);   // u2 = -u1 (Appendix B-7)
-        for (long long s = sg.sb; s < sg.se; ++s) {
-            const R cf = g.reach[(long long)(i - 1) * NS + s];
-            const R uc = g.U[((long long)g.s_cb[s] + a) * PC + col];
-            if (MODE == MODE_CFR) {
-                const R vd = sm.sv[(int)(s - T.s0) * PC + col];
-                const R diff = neg ? (vd - uc) : (uc - vd);
-                const R term = cf * diff;
-                xadd(c, (double)term, g.sc, g.rc);
-                if (a == 0) xadd(cp, (double)g.reach[(long long)(P + i - 1) * NS + s], g.scp, g.rcp);
-            } else {  // MODE_BR: sum of cf * V(child) in the stored column
-                const R term = cf * uc;
-                xadd(c, (double)term, g.sc, g.rc);
+    } else if (T.staged == 2) {
+        // generic rows: a warp per row, lanes over the row's elements
+        for (int ls = warp; ls < nslot; ls += nwarps) {
+            const R* __restrict__ src = g.U + sm.scb[ls] * PC;
+            R* dst = sm.ch + sm.scoff[ls];
+            const int cnt = sm.sn[ls] * PC;
+            for (int e = lane; e < cnt; e += 32) cp_async<(int)sizeof(R)>(dst + e, src + e);
+        }
+    }
+    if (sig_staged) {
+        for (int p = tid; p < T.npairs; p += nth) {
+            const int k = seg_of_pair(sm.soff, nseg, p);
+            sm.pseg[p] = (unsigned char)k;
+            const long long q = sm.seg[k].qb + (p - sm.soff[k]);
+            sm.ssig[p] = sig[q];
+            if (MODE == MODE_CFR && sm.seg[k].fused) {
+                sm.sreg[p] = g.regret[q];
+                sm.ssn[p] = g.snum[q];
             }
         }
-        if (MODE == MODE_BR) {
-            sm.rt[p] = (R)xdec(c[0], c[1], c[2], g.rc);
-        } else if (sg.fused) {
-            sm.rt[p] = (R)xdec(c[0], c[1], c[2], g.rc);
-            if (a == 0) sm.pib[lo] = (R)xdec(cp[0], cp[1], cp[2], g.rcp);
+    }
+    for (int k = warp; k < nseg; k += nwarps)
+        for (int s = sm.seg[k].sb + lane; s < sm.seg[k].se; s += 32) sm.spoff[s] = sm.soff[k];
+    cp_async_wait_all();
+    __syncthreads();
+
+    // ---- phase A: node values, Eq 1 in ascending action order from +0
+    if (tid < nslot) {
+        R v[PC];
+#pragma unroll
+        for (int j = 0; j < PC; ++j) v[j] = (R)0;
+        const int po = sig_staged ? sm.spoff[tid] : -1;
+        if (staged && po >= 0) {
+            const R* row = sm.ch + sm.scoff[tid];
+            const R* sg = sm.ssig + po;
+            for (int a = 0; a < my_n; ++a) {
+                const R x = sg[a];
+#pragma unroll
+                for (int j = 0; j < PC; ++j) v[j] = v[j] + x * row[a * PC + j];
+            }
         } else {
-            const long long q = (long long)g.qbase[h] + a;
-            atomicAdd(&g.acc_r[q * 3 + 0], (unsigned long long)c[0]);
-            atomicAdd(&g.acc_r[q * 3 + 1], (unsigned long long)c[1]);
-            atomicAdd(&g.acc_r[q * 3 + 2], (unsigned long long)c[2]);
-            if (a == 0) {
-                atomicAdd(&g.acc_p[h * 3 + 0], (unsigned long long)cp[0]);
-                atomicAdd(&g.acc_p[h * 3 + 1], (unsigned long long)cp[1]);
-                atomicAdd(&g.acc_p[h * 3 + 2], (unsigned long long)cp[2]);
+            for (int a = 0; a < my_n; ++a) {
+                const R x = (po >= 0) ? sm.ssig[po + a] : sig[my_eb + a];
+#pragma unroll
+                for (int j = 0; j < PC; ++j) {
+                    const R u = staged ? sm.ch[sm.scoff[tid] + a * PC + j] : g.U[(my_cb + a) * PC + j];
+                    v[j] = v[j] + x * u;
+                }
+            }
+        }
+        const bool skip = (MODE == MODE_BR) && (my_actor == br_player);
+        if (!skip) {
+#pragma unroll
+            for (int j = 0; j < PC; ++j) g.U[my_node * PC + j] = v[j];
+        }
+#pragma unroll
+        for (int j = 0; j < PC; ++j) sm.sv[tid * PC + j] = v[j];
+    }
+    if (MODE == MODE_VALUES) return;
+    __syncthreads();
+
+    // ---- phase B: exact sums.  Work items: every (infoset, action) pair (r~ or BR
+    // sums) plus one pi_bar item per segment (CFR mode).  Each item is split over
+    // `ns` adjacent lanes (members strided); partial slice sums are exact
+    // integer-valued doubles combined with shuffles.  The player-2 sign of the
+    // zero-sum storage (u2 = -u1) is applied to the sums: slices of -t are -slices of t.
+    const int nitems = T.npairs + ((MODE == MODE_CFR) ? nseg : 0);
+    int ns = 1;
+    while (ns < 8 && nitems * ns * 2 <= nth) ns <<= 1;
+    const int rounds = (nitems * ns + nth - 1) / nth;
+    double kr0 = 0, kr1 = 0, kr2 = 0, kr3 = 0, kr4 = 0;
+    for (int rd = 0; rd < rounds; ++rd) {
+        const int wi = rd * nth + tid;
+        const int it = wi / ns, part = wi - it * ns;
+        double c0 = 0, c1 = 0, c2 = 0;
+        int k = 0, a = 0;
+        bool is_pair = false, neg = false, active = false;
+        if (it < T.npairs) {
+            k = sig_staged ? (int)sm.pseg[it] : seg_of_pair(sm.soff, nseg, it);
+            a = it - sm.soff[k];
+            is_pair = true;
+            const int i = sm.seg[k].owner;
+            active = !(MODE == MODE_BR && i != br_player);
+            neg = (PC == 1) && (i == 2) && (MODE == MODE_CFR);
+        } else if (it < nitems) {
+            k = it - T.npairs;
+            active = true;
+        }
+        if (active) {
+            const SegS& sg = sm.seg[k];
+            const int col = (PC == 1) ? 0 : sg.owner - 1;
+            if (!is_pair) {
+                for (int ls = sg.sb + part; ls < sg.se; ls += ns) xadd(c0, c1, c2, (double)sm.sph[ls], g.scp0);
+            } else if (staged) {
+                for (int ls = sg.sb + part; ls < sg.se; ls += ns) {
+                    const R uc = sm.ch[sm.scoff[ls] + a * PC + col];
+                    const R t = (MODE == MODE_CFR) ? sm.spc[ls] * (uc - sm.sv[ls * PC + col]) : sm.spc[ls] * uc;
+                    xadd(c0, c1, c2, (double)t, g.sc0);
+                }
+            } else {
+                for (int ls = sg.sb + part; ls < sg.se; ls += ns) {
+                    const R uc = g.U[(sm.scb[ls] + a) * PC + col];
+                    const R t = (MODE == MODE_CFR) ? sm.spc[ls] * (uc - sm.sv[ls * PC + col]) : sm.spc[ls] * uc;
+                    xadd(c0, c1, c2, (double)t, g.sc0);
+                }
+            }
+            if (neg) { c0 = -c0; c1 = -c1; c2 = -c2; }
+        }
+        // combine the ns partial sums (exact: integer-valued doubles < 2^53)
+        for (int o = 1; o < ns; o <<= 1) {
+            c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+            c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+            c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+        }
+        if (active && part == 0) {
+            const bool keep = (MODE == MODE_BR) || sm.seg[k].fused;
+            if (keep) {
+                const double x = is_pair ? xdec(c0, c1, c2, g.rc) : xdec(c0, c1, c2, g.rcp);
+                if (rd == 0) kr0 = x;
+                else if (rd == 1) kr1 = x;
+                else if (rd == 2) kr2 = x;
+                else if (rd == 3) kr3 = x;
+                else kr4 = x;
+            } else if (MODE == MODE_CFR) {
+                if (is_pair) {
+                    const long long q = sm.seg[k].qb + a;
+                    atomicAdd(&g.acc_r[q * 3 + 0], (unsigned long long)(long long)c0);
+                    atomicAdd(&g.acc_r[q * 3 + 1], (unsigned long long)(long long)c1);
+                    atomicAdd(&g.acc_r[q * 3 + 2], (unsigned long long)(long long)c2);
+                } else {
+                    const long long h = sm.seg[k].h;
+                    atomicAdd(&g.acc_p[h * 3 + 0], (unsigned long long)(long long)c0);
+                    atomicAdd(&g.acc_p[h * 3 + 1], (unsigned long long)(long long)c1);
+                    atomicAdd(&g.acc_p[h * 3 + 2], (unsigned long long)(long long)c2);
+                }
+            }
+        }
+    }
+    __syncthreads();   // all reads of sm.ch done: rt / pos alias it from here on
+    if (sig_staged) {
+        for (int rd = 0; rd < rounds && rd < 5; ++rd) {
+            const int wi = rd * nth + tid;
+            const int it = wi / ns, part = wi - it * ns;
+            if (it < nitems && part == 0) {
+                const double x = rd == 0 ? kr0 : rd == 1 ? kr1 : rd == 2 ? kr2 : rd == 3 ? kr3 : kr4;
+                if (it < T.npairs) rt[it] = (R)x;
+                else sm.pib[it - T.npairs] = (R)x;
             }
         }
     }
@@ -239,24 +425,23 @@ __global__ void __launch_bounds__(256) k_bwd(DG<R, I> g, const R* __restrict__ s
         // argmax per segment (ties to the lowest action); for u2 = -u1 storage the
         // stored sums are negated, so player 2 takes the argmin.
         for (int k = tid; k < nseg; k += nth) {
-            const SegD sg = g.segs[T.seg0 + k];
-            if ((int)g.owner[sg.h] != br_player) continue;
-            const int n = sm.soff[k + 1] - sm.soff[k];
+            if (sm.seg[k].owner != br_player) continue;
+            const int n = sm.seg[k].n;
             const bool neg = (PC == 1) && (br_player == 2);
             int best = 0;
-            R bv = sm.rt[sm.soff[k]];
+            R bv = rt[sm.soff[k]];
             for (int a = 1; a < n; ++a) {
-                const R x = sm.rt[sm.soff[k] + a];
+                const R x = rt[sm.soff[k] + a];
                 if (neg ? (x < bv) : (x > bv)) { bv = x; best = a; }
             }
             sm.best[k] = best;
         }
         __syncthreads();
         for (int k = 0; k < nseg; ++k) {
-            const SegD sg = g.segs[T.seg0 + k];
-            if ((int)g.owner[sg.h] != br_player) continue;
+            if (sm.seg[k].owner != br_player) continue;
             const int best = sm.best[k];
-            for (long long s = sg.sb + tid; s < sg.se; s += nth) {
+            for (int ls = sm.seg[k].sb + tid; ls < sm.seg[k].se; ls += nth) {
+                const long long s = T.s0 + ls;
                 const long long src = ((long long)g.s_cb[s] + best) * PC;
                 const long long dst = (long long)g.s_node[s] * PC;
 #pragma unroll
@@ -266,58 +451,51 @@ __global__ void __launch_bounds__(256) k_bwd(DG<R, I> g, const R* __restrict__ s
         return;
     }
 
-    // Phase C: fused update of complete single-depth infosets.
+    // ---- phase C: fused update of complete single-depth infosets
     const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
-    for (int p = tid; p < T.npairs; p += nth) {
-        int lo = 0, hi = nseg - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (sm.soff[mid] <= p) lo = mid; else hi = mid - 1;
+    if (!sig_staged) {   // split tile: every segment is deferred
+        if (last) {
+            __syncthreads();
+            if (tid == 0) g.ctrl[0] = t_iter;
         }
-        const SegD sg = g.segs[T.seg0 + lo];
-        if (!sg.fused) continue;
-        const int a = p - sm.soff[lo];
-        const long long q = (long long)g.qbase[sg.h] + a;
-        const R rt = sm.rt[p];
+        return;
+    }
+    for (int p = tid; p < T.npairs; p += nth) {
+        const int k = sm.pseg[p];
+        if (!sm.seg[k].fused) continue;
+        const long long q = sm.seg[k].qb + (p - sm.soff[k]);
+        const R r_t = rt[p];
         R r;
         if (g.variant == 0) {
-            r = g.regret[q] + rt;                       // Eq 8/15, cumulative (Q4)
+            r = sm.sreg[p] + r_t;                       // Eq 8/15, cumulative (Q4)
         } else {
-            const R x = g.regret[q] + rt;               // CFR+ (Q6)
+            const R x = sm.sreg[p] + r_t;               // CFR+ (Q6)
             r = (x > (R)0) ? x : (R)0;
             if (!finite_(x)) r = x;
         }
         g.regret[q] = r;
-        const R wp = w * sm.pib[lo];
-        g.snum[q] = g.snum[q] + wp * g.sig[q];          // Eq 10 numerator
-        sm.pos[p] = (r > (R)0) ? r : (R)0;
+        const R wp = w * sm.pib[k];
+        g.snum[q] = sm.ssn[p] + wp * sm.ssig[p];        // Eq 10 numerator
+        pos[p] = (r > (R)0) ? r : (R)0;
     }
     __syncthreads();
     for (int k = tid; k < nseg; k += nth) {
-        const SegD sg = g.segs[T.seg0 + k];
-        if (!sg.fused) continue;
-        g.sden[sg.h] = g.sden[sg.h] + w * sm.pib[k];    // Eq 10 denominator
+        if (!sm.seg[k].fused) continue;
+        g.sden[sm.seg[k].h] = sm.sden[k] + w * sm.pib[k];   // Eq 10 denominator
         R z = (R)0;
-        for (int p = sm.soff[k]; p < sm.soff[k + 1]; ++p) z = z + sm.pos[p];
+        for (int p = sm.soff[k]; p < sm.soff[k + 1]; ++p) z = z + pos[p];
         sm.zs[k] = z;
     }
     __syncthreads();
     bool bad = false;
     for (int p = tid; p < T.npairs; p += nth) {
-        int lo = 0, hi = nseg - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (sm.soff[mid] <= p) lo = mid; else hi = mid - 1;
-        }
-        const SegD sg = g.segs[T.seg0 + lo];
-        if (!sg.fused) continue;
-        const int a = p - sm.soff[lo];
-        const int n = sm.soff[lo + 1] - sm.soff[lo];
-        const long long q = (long long)g.qbase[sg.h] + a;
-        const R z = sm.zs[lo];
-        const R nsig = (z > (R)0) ? sm.pos[p] / z : (R)1 / (R)n;   // Eq 9
-        g.sig[q] = nsig;
-        if (!finite_(g.regret[q]) || !finite_(nsig) || !finite_(z)) bad = true;
+        const int k = sm.pseg[p];
+        if (!sm.seg[k].fused) continue;
+        const int a = p - sm.soff[k];
+        const R z = sm.zs[k];
+        const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)sm.seg[k].n;   // Eq 9
+        g.sig[sm.seg[k].qb + a] = nsig;
+        if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
     }
     if (bad) atomicMin(&g.ctrl[1], t_iter);
     if (last) {
@@ -343,7 +521,7 @@ __global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
         g.acc_p[h * 3 + 0] = 0;
         g.acc_p[h * 3 + 1] = 0;
         g.acc_p[h * 3 + 2] = 0;
-        const R pib = (R)xdec(p0, p1, p2, g.rcp);
+        const R pib = (R)xdec_ll(p0, p1, p2, g.rcp);
         const R wp = w * pib;
         R z = (R)0;
         for (int a = 0; a < n; ++a) {
@@ -353,7 +531,7 @@ __global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
             g.acc_r[q * 3 + 0] = 0;
             g.acc_r[q * 3 + 1] = 0;
             g.acc_r[q * 3 + 2] = 0;
-            const R rt = (R)xdec(c0, c1, c2, g.rc);
+            const R rt = (R)xdec_ll(c0, c1, c2, g.rc);
             R r;
             if (g.variant == 0) {
                 r = g.regret[q] + rt;
@@ -441,17 +619,33 @@ struct Layout {
     }
 };
 
+// U rows of depth l start at u_off[l] (rows), each level aligned to 32 bytes so
+// that uniform child rows can be staged with 16-byte cp.async chunks.
+static std::vector<int64_t> u_layout(const Game& g, size_t elem) {
+    const int64_t rowbytes = (int64_t)g.Pc * (int64_t)elem;
+    int64_t a = 32, b = rowbytes;
+    while (b) { const int64_t t = a % b; a = b; b = t; }
+    const int64_t m = 32 / a;   // rows per alignment unit
+    std::vector<int64_t> off(g.D + 2, 0);
+    for (int l = 0; l <= g.D; ++l) {
+        const int64_t n = g.level_ptr[l + 1] - g.level_ptr[l];
+        off[l + 1] = ((off[l] + n + m - 1) / m) * m;
+    }
+    return off;
+}
+
 template <class R, class I>
 struct Plan {
     size_t U, reach, sig, sig_eval, regret, snum, sden, acc_r, acc_p;
-    size_t s_node, s_cb, s_n, s_ebase, s_actor, s_parent, s_e, s_pact;
+    size_t f_parent, f_e, f_pact;
+    size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, ctrl, out;
     size_t total;
     explicit Plan(const Game& g) {
         Layout L;
-        const size_t NS = (size_t)g.NS, Q = (size_t)g.Q, H = (size_t)g.H, C = (size_t)g.C;
-        U = L.take<R>((size_t)g.V * g.Pc);
-        reach = L.take<R>(2 * (size_t)g.P * NS);
+        const size_t NS = (size_t)g.NS, ND = (size_t)g.ND, Q = (size_t)g.Q, H = (size_t)g.H, C = (size_t)g.C;
+        U = L.take<R>((size_t)u_layout(g, sizeof(R)).back() * g.Pc + 8);
+        reach = L.take<R>(2 * (size_t)g.P * ND);
         sig = L.take<R>(Q + C);
         sig_eval = L.take<R>(Q + C);
         regret = L.take<R>(Q);
@@ -459,14 +653,16 @@ struct Plan {
         sden = L.take<R>(H);
         acc_r = L.take<unsigned long long>(3 * Q);
         acc_p = L.take<unsigned long long>(3 * H);
+        f_parent = L.take<I>(ND);
+        f_e = L.take<I>(ND);
+        f_pact = L.take<unsigned char>(ND);
         s_node = L.take<I>(NS);
         s_cb = L.take<I>(NS);
         s_n = L.take<int>(NS);
         s_ebase = L.take<I>(NS);
         s_actor = L.take<unsigned char>(NS);
-        s_parent = L.take<I>(NS);
-        s_e = L.take<I>(NS);
-        s_pact = L.take<unsigned char>(NS);
+        s_dec = L.take<I>(NS);
+        s_coff = L.take<int>(NS);
         qbase = L.take<I>(H + 1);
         owner = L.take<unsigned char>(H);
         tiles = L.take<TileD>(g.tiles.size());
@@ -545,51 +741,116 @@ struct Solver final : SolverBase {
         dg.sden = at<R>(plan.sden);
         dg.acc_r = at<unsigned long long>(plan.acc_r);
         dg.acc_p = at<unsigned long long>(plan.acc_p);
+        dg.f_parent = at<I>(plan.f_parent);
+        dg.f_e = at<I>(plan.f_e);
+        dg.f_pact = at<unsigned char>(plan.f_pact);
         dg.s_node = at<I>(plan.s_node);
         dg.s_cb = at<I>(plan.s_cb);
         dg.s_n = at<int>(plan.s_n);
         dg.s_ebase = at<I>(plan.s_ebase);
         dg.s_actor = at<unsigned char>(plan.s_actor);
-        dg.s_parent = at<I>(plan.s_parent);
-        dg.s_e = at<I>(plan.s_e);
-        dg.s_pact = at<unsigned char>(plan.s_pact);
+        dg.s_dec = at<I>(plan.s_dec);
+        dg.s_coff = at<int>(plan.s_coff);
         dg.qbase = at<I>(plan.qbase);
         dg.owner = at<unsigned char>(plan.owner);
         dg.tiles = at<TileD>(plan.tiles);
         dg.segs = at<SegD>(plan.segs);
         dg.deferred = at<I>(plan.deferred);
         dg.ctrl = at<long long>(plan.ctrl);
-        dg.NS = g.NS;
         dg.ndef = (long long)g.deferred_list.size();
         dg.P = g.P;
         dg.variant = cfg.variant;
+        dg.sc0 = std::ldexp(1.0, 40 - E);
+        dg.scp0 = std::ldexp(1.0, 40 - 1);
         for (int k = 0; k < 3; ++k) {
-            dg.sc[k] = std::ldexp(1.0, 40 * (k + 1) - E);
             dg.rc[k] = std::ldexp(1.0, E - 40 * (k + 1));
-            dg.scp[k] = std::ldexp(1.0, 40 * (k + 1) - 1);
             dg.rcp[k] = std::ldexp(1.0, 1 - 40 * (k + 1));
         }
         // ---- uploads
         cfr_status st;
-        if ((st = up(plan.U, narrow<R>(g.util_c)))) return st;
-        if ((st = up(plan.s_node, narrow<I>(g.s_node)))) return st;
-        if ((st = up(plan.s_cb, narrow<I>(g.s_cb)))) return st;
+        // ---- U rows with per-level 32-byte alignment (u_layout)
+        const std::vector<int64_t> uoff = u_layout(g, sizeof(R));
+        {
+            std::vector<R> u((size_t)uoff.back() * g.Pc + 8, (R)0);
+            for (int l = 0; l <= g.D; ++l)
+                for (int64_t k = g.level_ptr[l]; k < g.level_ptr[l + 1]; ++k)
+                    for (int j = 0; j < g.Pc; ++j)
+                        u[(size_t)(uoff[l] + k - g.level_ptr[l]) * g.Pc + j] = (R)g.util_c[(size_t)k * g.Pc + j];
+            if ((st = up(plan.U, u))) return st;
+        }
+        std::vector<int64_t> s_node_u(g.NS), s_cb_u(g.NS);
+        for (int L = 0; L < g.D; ++L)
+            for (int64_t s = g.slot_ptr[L]; s < g.slot_ptr[L + 1]; ++s) {
+                s_node_u[s] = uoff[L] + (g.s_node[s] - g.level_ptr[L]);
+                s_cb_u[s] = uoff[L + 1] + (g.s_cb[s] - g.level_ptr[L + 1]);
+            }
+        // ---- staging layout per tile (precision dependent): uniform rows whose
+        // starts and lengths are multiples of the cp.async chunk use chunked copies
+        // with an odd number of chunks per row stride (<= 2-way bank conflicts)
+        std::vector<int32_t> s_coff = g.s_coff;
+        std::vector<TileD> tiles(g.tiles.size());
+        {
+            const int CH = (sizeof(R) == 8) ? 16 : 8;
+            const int CE = CH / (int)sizeof(R);
+            for (size_t t = 0; t < g.tiles.size(); ++t) {
+                const TileH& th = g.tiles[t];
+                TileD td{};
+                td.s0 = th.s0;
+                td.s1 = th.s1;
+                td.seg0 = th.seg0;
+                td.seg1 = th.seg1;
+                td.npairs = th.npairs;
+                td.staged = th.staged ? 2 : 0;
+                if (th.staged) {
+                    const int rowlen = g.s_n[th.s0] * g.Pc;
+                    bool uni = (rowlen % CE) == 0;
+                    for (int64_t s = th.s0; s < th.s1 && uni; ++s)
+                        uni = (g.s_n[s] * g.Pc == rowlen) && ((s_cb_u[s] * g.Pc) % CE == 0);
+                    if (uni) {
+                        const int cpr = rowlen / CE;
+                        const int cstride = (cpr % 2 == 0) ? cpr + 1 : cpr;
+                        const int64_t need = (int64_t)(th.s1 - th.s0) * cstride * CE;
+                        if (need <= kTileChildren) {
+                            td.staged = 1;
+                            td.rowlen = rowlen;
+                            td.cpr = cpr;
+                            td.stride = cstride * CE;
+                            td.inv_cpr = 1.0f / (float)cpr;
+                            for (int64_t s = th.s0; s < th.s1; ++s) s_coff[s] = (int32_t)((s - th.s0) * td.stride);
+                        }
+                    }
+                }
+                tiles[t] = td;
+            }
+        }
+        std::vector<SegD> segs(g.segs.size());
+        for (size_t k = 0; k < g.segs.size(); ++k) {
+            const SegH& sh = g.segs[k];
+            SegD sd{};
+            sd.h = sh.h;
+            sd.qb = g.qbase_int[sh.h];
+            sd.n = (int)(g.qbase_int[sh.h + 1] - g.qbase_int[sh.h]);
+            sd.owner = g.owner_int[sh.h];
+            sd.sb = sh.sb;
+            sd.se = sh.se;
+            sd.pair_off = sh.pair_off;
+            sd.fused = sh.fused;
+            segs[k] = sd;
+        }
+        if ((st = up(plan.f_parent, narrow<I>(g.f_parent)))) return st;
+        if ((st = up(plan.f_e, narrow<I>(g.f_e)))) return st;
+        if ((st = up(plan.f_pact, g.f_pact))) return st;
+        if ((st = up(plan.s_node, narrow<I>(s_node_u)))) return st;
+        if ((st = up(plan.s_cb, narrow<I>(s_cb_u)))) return st;
         if ((st = up(plan.s_n, g.s_n))) return st;
         if ((st = up(plan.s_ebase, narrow<I>(g.s_ebase)))) return st;
         if ((st = up(plan.s_actor, g.s_actor))) return st;
-        if ((st = up(plan.s_parent, narrow<I>(g.s_parent)))) return st;
-        if ((st = up(plan.s_e, narrow<I>(g.s_e)))) return st;
-        if ((st = up(plan.s_pact, g.s_pact))) return st;
+        if ((st = up(plan.s_dec, narrow<I>(g.s_dec)))) return st;
+        if ((st = up(plan.s_coff, s_coff))) return st;
         if ((st = up(plan.qbase, narrow<I>(g.qbase_int)))) return st;
         if ((st = up(plan.owner, g.owner_int))) return st;
-        {
-            std::vector<TileD> t(g.tiles.size());
-            if (!t.empty()) std::memcpy(t.data(), g.tiles.data(), t.size() * sizeof(TileD));
-            if ((st = up(plan.tiles, t))) return st;
-            std::vector<SegD> sgv(g.segs.size());
-            if (!sgv.empty()) std::memcpy(sgv.data(), g.segs.data(), sgv.size() * sizeof(SegD));
-            if ((st = up(plan.segs, sgv))) return st;
-        }
+        if ((st = up(plan.tiles, tiles))) return st;
+        if ((st = up(plan.segs, segs))) return st;
         if ((st = up(plan.deferred, narrow<I>(g.deferred_list)))) return st;
         // sigma^(1) = 1/|A(h)| and chance probabilities (rounded once, Q14)
         {
@@ -607,13 +868,12 @@ struct Solver final : SolverBase {
         CU(cudaMemsetAsync(ws + plan.sden, 0, g.H * sizeof(R), stream));
         CU(cudaMemsetAsync(ws + plan.acc_r, 0, 3 * g.Q * sizeof(unsigned long long), stream));
         CU(cudaMemsetAsync(ws + plan.acc_p, 0, 3 * g.H * sizeof(unsigned long long), stream));
-        CU(cudaMemsetAsync(ws + plan.reach, 0, 2 * (size_t)g.P * g.NS * sizeof(R), stream));
+        CU(cudaMemsetAsync(ws + plan.reach, 0, 2 * (size_t)g.P * g.ND * sizeof(R), stream));
         {
-            // root reach factors = 1 (Eq 2 / Eq 4 base case); root is slot 0
-            std::vector<R> one(1, (R)1);
-            for (int r = 0; r < 2 * g.P; ++r)
-                if (g.NS > 0) CU(cudaMemcpyAsync(ws + plan.reach + ((size_t)r * g.NS) * sizeof(R), one.data(), sizeof(R),
-                                                 cudaMemcpyHostToDevice, stream));
+            // root reach factors = 1 (Eq 2 / Eq 4 base case); the root is decision 0
+            std::vector<R> one(2 * g.P, (R)1);
+            if (g.ND > 0) CU(cudaMemcpyAsync(ws + plan.reach, one.data(), one.size() * sizeof(R), cudaMemcpyHostToDevice,
+                                             stream));
             std::vector<long long> ctrl = {0, LLONG_MAX, 0, 0, 0, 0, 0, 0};
             if ((st = up(plan.ctrl, ctrl))) return st;
         }
@@ -662,7 +922,7 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         int64_t n = 0;
         for (int l = 1; l < g.D; ++l)
-            if (g.slot_ptr[l + 1] > g.slot_ptr[l]) ++n;
+            if (g.dec_ptr[l + 1] > g.dec_ptr[l]) ++n;
         for (int L = g.D - 1; L >= 0; --L)
             if (g.tile_ptr[L + 1] > g.tile_ptr[L]) ++n;
         if (!g.deferred_list.empty()) ++n;
@@ -671,7 +931,7 @@ struct Solver final : SolverBase {
 
     void fwd_level(cudaStream_t st, const R* sig, int l) {
         const Game& g = *gp;
-        const long long s0 = g.slot_ptr[l], s1 = g.slot_ptr[l + 1];
+        const long long s0 = g.dec_ptr[l], s1 = g.dec_ptr[l + 1];
         if (s1 <= s0) return;
         const long long n = s1 - s0;
         const int threads = 256;
@@ -915,42 +1175,61 @@ struct Solver final : SolverBase {
         out[2] /= iters;
         out[3] = per_bwd[dom] / iters;
         out[4] = dom;
+        dom_level = dom;
         return sync();
     }
 
     // Algorithmic DRAM bytes per iteration (DESIGN.md §6 byte model).
+    int dom_level = -1;   // set by profile(): the backward level with the largest time
+    double level_bwd_bytes(int L) const {
+        const Game& g = *gp;
+        const double w = sizeof(R), ix = sizeof(I);
+        const int Pc = g.Pc;
+        const double parents = (double)(g.slot_ptr[L + 1] - g.slot_ptr[L]);
+        const double children = (double)(g.level_ptr[L + 2] - g.level_ptr[L + 1]);
+        // children values read once; parent: node, cb, ebase, dec (ix each), n, coff
+        // (4 each), actor (1); value write; the owner's pi_check and pi_hat
+        double b = children * Pc * w + parents * (4 * ix + 8 + 1 + Pc * w + 2 * w);
+        // fused update of the level's infosets: R, S_num, sigma read + written per
+        // pair; S_den read + written per infoset
+        double pairs = 0, infosets = 0;
+        for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1]; ++t)
+            for (int k = g.tiles[t].seg0; k < g.tiles[t].seg1; ++k)
+                if (g.segs[k].fused) {
+                    pairs += (double)(g.qbase_int[g.segs[k].h + 1] - g.qbase_int[g.segs[k].h]);
+                    infosets += 1;
+                }
+        b += pairs * 6 * w + infosets * 2 * w;
+        return b;
+    }
     cfr_status model_bytes(double* out) override {
         const Game& g = *gp;
         const double w = sizeof(R), ix = sizeof(I);
-        const int P = g.P, Pc = g.Pc;
-        double fwd = 0, bwd = 0, upd = 0, dom = 0;
-        int64_t dom_nodes = -1;
+        const int P = g.P;
+        double fwd = 0, bwd = 0, upd = 0;
         for (int l = 1; l < g.D; ++l) {
-            const double n = (double)(g.slot_ptr[l + 1] - g.slot_ptr[l]);
-            // per decision node: parent slot + edge index + parent actor, write 2P factors;
-            // parent factors are re-read by siblings (counted once per parent below)
+            const double n = (double)(g.dec_ptr[l + 1] - g.dec_ptr[l]);
+            // per decision node: parent dec + edge index + parent actor, its 2P factors
+            // written; every parent's 2P factors read once (streaming, canonical order)
             fwd += n * (2 * ix + 1 + 2 * P * w);
-            fwd += (double)(g.slot_ptr[l] - g.slot_ptr[l - 1]) * 2 * P * w;
+            fwd += (double)(g.dec_ptr[l] - g.dec_ptr[l - 1]) * 2 * P * w;
         }
+        int big = 0;
         for (int L = g.D - 1; L >= 0; --L) {
-            const double parents = (double)(g.slot_ptr[L + 1] - g.slot_ptr[L]);
-            const double children = (double)(g.level_ptr[L + 2] - g.level_ptr[L + 1]);
-            // children values read once; parent: node, cb, n, ebase, actor; value write;
-            // acting player's pi_check and pi_hat
-            const double b = children * Pc * w + parents * (3 * ix + 4 + 1 + Pc * w + 2 * w);
-            bwd += b;
-            if (g.level_ptr[L + 2] - g.level_ptr[L + 1] > dom_nodes) {
-                dom_nodes = g.level_ptr[L + 2] - g.level_ptr[L + 1];
-                dom = b;
-            }
+            bwd += level_bwd_bytes(L);
+            if (g.level_ptr[L + 2] - g.level_ptr[L + 1] > g.level_ptr[big + 2] - g.level_ptr[big + 1]) big = L;
         }
-        // update per pair: regret r/w, snum r/w, sigma r/w; per infoset: sden r/w
-        upd = (double)g.Q * 6 * w + (double)g.H * 2 * w;
+        // deferred infosets: slices read + zeroed, R, S_num, sigma r/w per pair; S_den per infoset
+        for (int64_t h : g.deferred_list) {
+            const double n = (double)(g.qbase_int[h + 1] - g.qbase_int[h]);
+            upd += n * (6 * w + 48) + 2 * w + 48;
+        }
         out[0] = fwd + bwd + upd;
         out[1] = fwd;
         out[2] = bwd;
         out[3] = upd;
-        out[4] = dom;
+        out[4] = g.D > 0 ? level_bwd_bytes(dom_level >= 0 ? dom_level : big) : 0.0;
+        (void)ix;
         return CFR_OK;
     }
 };
