@@ -141,6 +141,7 @@ cfr_status cfr_solver_workspace_bytes(const cfr_game* g, const cfr_solver_config
 cfr_status cfr_solver_create(const cfr_game* g, const cfr_solver_config* cfg, void* workspace,
                              size_t workspace_bytes, void* stream, const cfr_dist* dist,
                              cfr_solver** out);
+/* (The game must outlive its solvers.) */
 void cfr_solver_destroy(cfr_solver* s);
 
 /* Runs `iterations` CFR iterations (T += iterations) and synchronises the stream;
@@ -187,6 +188,47 @@ cfr_status cfr_solver_model_bytes(cfr_solver* s, double* out /* [5] */);
 
 /* Writes a fresh ncclUniqueId (128 bytes) to `out` (rank 0 only). */
 cfr_status cfr_nccl_unique_id(void* out /* 128 bytes */);
+
+/* ------------------------------------------------------ multi-GPU sharding --
+ * With world_size > 1 the tree is level-sharded: depths 0..cut
+ * are replicated, the decision nodes of depth `cut` are split into world_size
+ * contiguous ranges balanced by subtree size, and each rank owns the descendants
+ * of its range.  One iteration has two exchanges, both sum-allreduces that are
+ * exact by construction:
+ *   CFR_XCHG_CUT  cut-level decision values (R = f64 or f32 elements; each value
+ *                 is nonzero on exactly one rank);
+ *   CFR_XCHG_ACC  int64 exact-slice partial sums of the deferred infosets.
+ * With an NCCL id both run inside the iteration's CUDA Graph.  Without one
+ * ("external" mode, used by the tests) the caller drives the phases and performs
+ * the two sums itself; readbacks then return this rank's part (zeros for the
+ * infosets another rank reports) and the caller sums them.
+ * cfr_solver_exploitability is single-GPU only (CFR_ERR_UNSUPPORTED otherwise). */
+#define CFR_PHASE_LOWER 0     /* forward pass + backward of the owned depths (+ cut pack) */
+#define CFR_PHASE_UPPER 1     /* cut unpack + trunk backward                              */
+#define CFR_PHASE_UPDATE 2    /* deferred-infoset update; ends the iteration (T += 1)     */
+#define CFR_PHASE_EV_LOWER 3  /* sigma_bar + values pass of the owned depths (+ cut pack) */
+#define CFR_PHASE_EV_UPPER 4  /* cut unpack + trunk values pass; out = root values [P]    */
+cfr_status cfr_solver_phase(cfr_solver* s, int32_t phase, double* out /* [P] or NULL */);
+#define CFR_XCHG_CUT 0
+#define CFR_XCHG_ACC 1
+cfr_status cfr_solver_exchange_size(cfr_solver* s, int32_t which, size_t* bytes);
+/* put = 0: device -> host copy of the exchange buffer; put = 1: host -> device. */
+cfr_status cfr_solver_exchange(cfr_solver* s, int32_t which, int32_t put, void* host, size_t bytes);
+/* out[8]: cut depth (-1 = unsharded), cut-level decision nodes, owned nodes below
+ * the cut, local nodes, local decision nodes, deferred infosets, deferred (h, a)
+ * pairs, world size. */
+cfr_status cfr_solver_shard_info(cfr_solver* s, int64_t* out);
+/* Host-only view of the same partition for (rank, world): out[10] = the eight
+ * fields above, cut-level decision nodes owned by `rank`, infosets `rank` reports
+ * in readbacks.  No GPU needed. */
+cfr_status cfr_game_shard_info(const cfr_game* g, int32_t rank, int32_t world, int64_t* out);
+/* Shard files, so that N ranks of one host do not each hold the whole tree:
+ * one process writes `<prefix>.r<rank>of<world>.cfrshard` for every rank; each
+ * rank then loads only its own view.  A loaded game serves cfr_game_info,
+ * cfr_game_qbase and solvers with exactly that (rank, world_size);
+ * cfr_game_canonical returns CFR_ERR_UNSUPPORTED for it. */
+cfr_status cfr_game_save_shards(const cfr_game* g, int32_t world, const char* prefix);
+cfr_status cfr_game_load_shard(const char* prefix, int32_t rank, int32_t world, cfr_game** out);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,15 @@ import numpy as np
 from . import _native
 from ._native import NativeError, build, load
 
-__all__ = ["Game", "Solver", "NativeError", "build", "load", "CFR", "CFR_PLUS"]
+__all__ = ["Game", "Solver", "NativeError", "build", "load", "CFR", "CFR_PLUS", "nccl_unique_id"]
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 creates it; broadcast it to the others)."""
+    L = load()
+    buf = ctypes.create_string_buffer(128)
+    _native.check(L.cfr_nccl_unique_id(buf))
+    return buf.raw
 
 CFR, CFR_PLUS = 0, 1
 FLAG_NO_GRAPH = 1
@@ -32,9 +40,13 @@ def _ptr(a: np.ndarray) -> ctypes.c_void_p:
 class Game:
     """cfr_game_create over the Def. 2.1 arrays (any node order)."""
 
-    def __init__(self, desc):
+    def __init__(self, desc=None, _handle=None):
         L = load()
         self._L = L
+        if _handle is not None:
+            self._h = _handle
+            self._info()
+            return
         self.num_players = int(desc.num_players)
         self._arrays = [np.ascontiguousarray(desc.parent, dtype=np.int64),
                         np.ascontiguousarray(desc.player, dtype=np.int32),
@@ -48,6 +60,10 @@ class Game:
         _native.check(L.cfr_game_create(ctypes.byref(d), ctypes.byref(h)))
         self._h = h
         self._arrays = None   # the library copied what it needs
+        self._info()
+
+    def _info(self):
+        L = self._L
         info = _native.GameInfoC()
         _native.check(L.cfr_game_info(self._h, ctypes.byref(info)))
         self.info = {f: getattr(info, f) for f, _ in info._fields_}
@@ -55,6 +71,18 @@ class Game:
         self.H = self.info["num_infosets"]
         self.Q = self.info["num_pairs"]
         self.D = self.info["depth"]
+        self.num_players = self.info["num_players"]
+
+    @classmethod
+    def load_shard(cls, prefix: str, rank: int, world: int) -> "Game":
+        """Load this rank's view written by save_shards (multi-GPU on one host)."""
+        L = load()
+        h = ctypes.c_void_p()
+        _native.check(L.cfr_game_load_shard(prefix.encode(), int(rank), int(world), ctypes.byref(h)))
+        return cls(_handle=h)
+
+    def save_shards(self, world: int, prefix: str):
+        _native.check(self._L.cfr_game_save_shards(self._h, int(world), prefix.encode()))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -67,6 +95,15 @@ class Game:
         _native.check(self._L.cfr_game_qbase(self._h, _ptr(q)))
         return q
 
+    SHARD_KEYS = ("cut", "n_cut", "owned_nodes", "local_nodes", "local_decision", "deferred", "deferred_pairs",
+                  "world", "owned_cut", "reported")
+
+    def shard_info(self, rank: int, world: int) -> dict:
+        """Host-side level-sharding plan for (rank, world)."""
+        out = np.zeros(10, dtype=np.int64)
+        _native.check(self._L.cfr_game_shard_info(self._h, int(rank), int(world), _ptr(out)))
+        return {k: int(v) for k, v in zip(self.SHARD_KEYS, out)}
+
     def canonical(self):
         c = np.zeros(self.V, dtype=np.int64)
         lp = np.zeros(self.D + 2, dtype=np.int64)
@@ -78,7 +115,11 @@ class Solver:
     """cfr_solver_* over a torch-allocated device workspace and a torch stream."""
 
     def __init__(self, game: Game, variant="cfr", precision: int = 64, device="cuda", stream=None,
-                 flags: int = 0):
+                 flags: int = 0, rank: int = 0, world_size: int = 1, nccl_id: bytes | None = None):
+        """world_size > 1: level-sharded solver for `rank`.  With
+        `nccl_id` (128 bytes from nccl_unique_id(), broadcast by the caller) the
+        exchanges run over NCCL inside the graph; without it the caller drives
+        phase() / exchange_get() / exchange_put() ("external" mode)."""
         import torch
 
         if not torch.cuda.is_available():
@@ -88,8 +129,19 @@ class Solver:
         self.game = game
         v = {"cfr": CFR, "vanilla": CFR, "cfr+": CFR_PLUS, "cfrplus": CFR_PLUS}.get(variant, variant)
         self.cfg = _native.SolverConfigC(int(v), int(precision), int(flags), 0)
+        self.precision = int(precision)
+        self.rank, self.world_size = int(rank), int(world_size)
+        self._nid = None
+        dist = None
+        if self.world_size > 1:
+            if nccl_id is not None:
+                self._nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            dist = _native.DistC(self.rank, self.world_size,
+                                 ctypes.cast(self._nid, ctypes.c_void_p) if self._nid is not None else None)
+        self._dist = dist
+        dptr = ctypes.byref(dist) if dist is not None else None
         nbytes = ctypes.c_size_t()
-        _native.check(L.cfr_solver_workspace_bytes(game._h, ctypes.byref(self.cfg), None, ctypes.byref(nbytes)))
+        _native.check(L.cfr_solver_workspace_bytes(game._h, ctypes.byref(self.cfg), dptr, ctypes.byref(nbytes)))
         self.workspace_bytes = int(nbytes.value)
         dev = torch.device(device)
         if dev.index is None:
@@ -104,7 +156,7 @@ class Solver:
         with torch.cuda.device(dev):
             _native.check(L.cfr_solver_create(game._h, ctypes.byref(self.cfg), ctypes.c_void_p(aligned),
                                               self.workspace_bytes, ctypes.c_void_p(self.stream.cuda_stream),
-                                              None, ctypes.byref(h)))
+                                              dptr, ctypes.byref(h)))
         self._h = h
         self.Q, self.H, self.P = game.Q, game.H, game.num_players
 
@@ -171,6 +223,33 @@ class Solver:
         out = np.zeros(5)
         _native.check(self._L.cfr_solver_profile(self._h, int(iterations), _ptr(out)))
         return dict(fwd_ms=out[0], bwd_ms=out[1], deferred_ms=out[2], dominant_ms=out[3], dominant_level=int(out[4]))
+
+    # -- multi-GPU (external mode drives the phases; see include/cfr_b200.h)
+    PHASE_LOWER, PHASE_UPPER, PHASE_UPDATE, PHASE_EV_LOWER, PHASE_EV_UPPER = 0, 1, 2, 3, 4
+    XCHG_CUT, XCHG_ACC = 0, 1
+
+    def phase(self, ph: int):
+        out = np.zeros(self.P)
+        _native.check(self._L.cfr_solver_phase(self._h, int(ph), _ptr(out)))
+        return out
+
+    def exchange_get(self, which: int) -> np.ndarray:
+        n = ctypes.c_size_t()
+        _native.check(self._L.cfr_solver_exchange_size(self._h, int(which), ctypes.byref(n)))
+        dt = np.int64 if which == self.XCHG_ACC else (np.float64 if self.precision == 64 else np.float32)
+        buf = np.zeros(n.value // np.dtype(dt).itemsize, dtype=dt)
+        _native.check(self._L.cfr_solver_exchange(self._h, int(which), 0, _ptr(buf), n.value))
+        return buf
+
+    def exchange_put(self, which: int, buf: np.ndarray):
+        buf = np.ascontiguousarray(buf)
+        _native.check(self._L.cfr_solver_exchange(self._h, int(which), 1, _ptr(buf), buf.nbytes))
+
+    def shard_info(self) -> dict:
+        out = np.zeros(8, dtype=np.int64)
+        _native.check(self._L.cfr_solver_shard_info(self._h, _ptr(out)))
+        keys = ("cut", "n_cut", "owned_nodes", "local_nodes", "local_decision", "deferred", "deferred_pairs", "world")
+        return {k: int(v) for k, v in zip(keys, out)}
 
     def model_bytes(self) -> dict:
         out = np.zeros(5)

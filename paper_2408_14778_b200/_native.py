@@ -14,8 +14,13 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _CSRC = os.path.join(_HERE, "csrc")
 LIB_PATH = os.path.join(_HERE, "libcfr_b200.so")
-SOURCES = [os.path.join(_CSRC, f) for f in ("solver.cu", "flatten.cpp", "cabi.cpp")]
+SOURCES = [os.path.join(_CSRC, f) for f in ("solver.cu", "flatten.cpp", "shard.cpp", "store.cpp", "cabi.cpp")]
 HEADERS = [os.path.join(_CSRC, "game.hpp"), os.path.join(os.path.dirname(_HERE), "include", "cfr_b200.h")]
+
+_NCCL = os.path.join(os.path.dirname(os.path.dirname(os.__file__)), "site-packages", "nvidia", "nccl")
+if not os.path.isdir(_NCCL):
+    import sysconfig
+    _NCCL = os.path.join(sysconfig.get_paths()["purelib"], "nvidia", "nccl")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -25,6 +30,9 @@ NVCC_FLAGS = [
     "--fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
     "-Xcompiler", "-fPIC,-O2,-ffp-contract=off,-fopenmp",
     "-shared", "-lgomp",
+    # NCCL (the torch-bundled 2.28 build) for the multi-GPU exchanges
+    "-I" + os.path.join(_NCCL, "include"), "-L" + os.path.join(_NCCL, "lib"), "-l:libnccl.so.2",
+    "-Xlinker", "-rpath=" + os.path.join(_NCCL, "lib"),
 ]
 
 _lock = threading.Lock()
@@ -117,6 +125,13 @@ SIGNATURES = {
     "cfr_solver_profile": (ctypes.c_int, [_P, _I64, _P]),
     "cfr_solver_model_bytes": (ctypes.c_int, [_P, _P]),
     "cfr_nccl_unique_id": (ctypes.c_int, [_P]),
+    "cfr_solver_phase": (ctypes.c_int, [_P, _I32, _P]),
+    "cfr_solver_exchange_size": (ctypes.c_int, [_P, _I32, _P]),
+    "cfr_solver_exchange": (ctypes.c_int, [_P, _I32, _I32, _P, ctypes.c_size_t]),
+    "cfr_solver_shard_info": (ctypes.c_int, [_P, _P]),
+    "cfr_game_shard_info": (ctypes.c_int, [_P, _I32, _I32, _P]),
+    "cfr_game_save_shards": (ctypes.c_int, [_P, _I32, ctypes.c_char_p]),
+    "cfr_game_load_shard": (ctypes.c_int, [ctypes.c_char_p, _I32, _I32, _P]),
 }
 
 

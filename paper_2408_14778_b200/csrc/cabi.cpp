@@ -92,6 +92,10 @@ cfr_status cfr_game_canonical(const cfr_game* gg, int64_t* canon_of_input, int64
         return CFR_ERR_INVALID_ARG;
     }
     const cfrb::Game& g = gg->g;
+    if (canon_of_input && gg->shard_only) {
+        cfrb_set_error("canonical order is not stored in a shard file");
+        return CFR_ERR_UNSUPPORTED;
+    }
     if (canon_of_input) std::memcpy(canon_of_input, g.canon_of_input.data(), g.V * sizeof(int64_t));
     if (level_ptr) std::memcpy(level_ptr, g.level_ptr.data(), g.level_ptr.size() * sizeof(int64_t));
     return CFR_OK;

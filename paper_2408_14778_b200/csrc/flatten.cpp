@@ -58,6 +58,98 @@ struct PhaseTimer {
 };
 }  // namespace
 
+// Tiles of each parent level: groups = maximal runs of equal infoset within the
+// level's slots; a tile packs whole groups under the slot / pair / segment /
+// staged-children limits; an oversized group is split (and its infoset deferred).
+void build_tiles(Game& g, const std::vector<int64_t>& slot_h) {
+    const int D = g.D;
+    const int Pc = g.Pc;
+    const int64_t H = g.H;
+    // Groups = maximal runs of equal infoset within a level's slots.  Tiles pack
+    // whole groups under the slot / pair / segment / staged-children limits.
+    g.tile_ptr.assign(D + 1, 0);
+    g.tiles.clear();
+    g.segs.clear();
+    // packing bound: >= the generic odd-stride row and the solver's chunked row
+    auto row_elems = [&](int64_t s) -> int64_t { return (int64_t)g.s_n[s] * Pc + 2; };
+    auto finish_tile = [&](TileH& t) {
+        // generic staged layout: one row per slot, odd strides (conflict-free
+        // per-thread row reads); the solver may re-lay uniform tiles in chunks
+        int64_t off = 0;
+        for (int64_t s = t.s0; s < t.s1; ++s) {
+            g.s_coff[s] = (int32_t)std::min<int64_t>(off, INT32_MAX);
+            off += ((int64_t)g.s_n[s] * Pc) | 1;
+        }
+        t.nch = (int32_t)std::min<int64_t>(off, INT32_MAX);
+        t.staged = off <= kTileChildren ? 1 : 0;
+        t.run0 = t.run1 = 0;
+        t.seg1 = (int32_t)g.segs.size();
+        g.tiles.push_back(t);
+    };
+    for (int L = 0; L < D; ++L) {
+        g.tile_ptr[L] = (int64_t)g.tiles.size();
+        const int64_t lo = g.slot_ptr[L], hi = g.slot_ptr[L + 1];
+        TileH cur{lo, lo, (int32_t)g.segs.size(), (int32_t)g.segs.size(), 0, 0, 0, 0, 0, 0};
+        int64_t cur_ch = 0;
+        auto close = [&]() {
+            if (cur.s1 > cur.s0) finish_tile(cur);
+            cur = TileH{cur.s1, cur.s1, (int32_t)g.segs.size(), (int32_t)g.segs.size(), 0, 0, 0, 0, 0, 0};
+            cur_ch = 0;
+        };
+        int64_t s = lo;
+        while (s < hi) {
+            int64_t e = s + 1;
+            const int64_t h = slot_h[s];
+            if (h >= 0)
+                while (e < hi && slot_h[e] == h) ++e;
+            const int64_t m = e - s;
+            const int32_t n = (h >= 0) ? (int32_t)(g.qbase_int[h + 1] - g.qbase_int[h]) : 0;
+            int64_t gch = 0;
+            for (int64_t x = s; x < e; ++x) gch += row_elems(x);
+            if (m > kTileSlots || n > kTilePairs) {
+                // split group: its own chunks, accumulated globally (deferred)
+                close();
+                g.deferred[h] = 1;
+                for (int64_t c0 = s; c0 < e; c0 += kTileSlots) {
+                    const int64_t c1 = std::min(e, c0 + kTileSlots);
+                    TileH t{c0, c1, (int32_t)g.segs.size(), 0, n, 0, 0, 0, 0, 0};
+                    g.segs.push_back(SegH{h, c0, c1, 0, 0});
+                    finish_tile(t);
+                }
+                cur = TileH{e, e, (int32_t)g.segs.size(), (int32_t)g.segs.size(), 0, 0, 0, 0, 0, 0};
+                cur_ch = 0;
+                s = e;
+                continue;
+            }
+            const int64_t segs_in = (int64_t)g.segs.size() - cur.seg0;
+            if ((cur.s1 - cur.s0) + m > kTileSlots || cur.npairs + n > kTilePairs ||
+                (h >= 0 && segs_in + 1 > kTileSegs) || (cur.s1 > cur.s0 && cur_ch + gch > kTileChildren))
+                close();
+            if (h >= 0) {
+                g.segs.push_back(SegH{h, s, e, cur.npairs, g.deferred[h] ? 0 : 1});
+                cur.npairs += n;
+            }
+            cur.s1 = e;
+            cur_ch += gch;
+            s = e;
+        }
+        close();
+    }
+    g.tile_ptr[D] = (int64_t)g.tiles.size();
+    for (auto& sg : g.segs)
+        if (g.deferred[sg.h]) sg.fused = 0;
+    g.deferred_list.clear();
+    g.dpos.assign(H, -1);
+    g.dqbase.assign(1, 0);
+    for (int64_t h = 0; h < H; ++h)
+        if (g.deferred[h]) {
+            g.dpos[h] = (int64_t)g.deferred_list.size();
+            g.deferred_list.push_back(h);
+            g.dqbase.push_back(g.dqbase.back() + (g.qbase_int[h + 1] - g.qbase_int[h]));
+        }
+
+}
+
 bool build_game(const cfr_game_desc* d, Game& g, std::string& err) {
     PhaseTimer tm;
     const int64_t V = d->num_nodes;
@@ -434,82 +526,7 @@ bool build_game(const cfr_game_desc* d, Game& g, std::string& err) {
 
     tm.mark("slots");
     // ------------------------------------------------------------------- tiles
-    // Groups = maximal runs of equal infoset within a level's slots.  Tiles pack
-    // whole groups under the slot / pair / segment / staged-children limits.
-    g.tile_ptr.assign(D + 1, 0);
-    g.tiles.clear();
-    g.segs.clear();
-    auto row_elems = [&](int64_t s) -> int64_t { return ((int64_t)g.s_n[s] * Pc) | 1; };
-    auto finish_tile = [&](TileH& t) {
-        // generic staged layout: one row per slot, odd strides (conflict-free
-        // per-thread row reads); the solver may re-lay uniform tiles in chunks
-        int64_t off = 0;
-        for (int64_t s = t.s0; s < t.s1; ++s) {
-            g.s_coff[s] = (int32_t)std::min<int64_t>(off, INT32_MAX);
-            off += row_elems(s);
-        }
-        t.nch = (int32_t)std::min<int64_t>(off, INT32_MAX);
-        t.staged = off <= kTileChildren ? 1 : 0;
-        t.run0 = t.run1 = 0;
-        t.seg1 = (int32_t)g.segs.size();
-        g.tiles.push_back(t);
-    };
-    for (int L = 0; L < D; ++L) {
-        g.tile_ptr[L] = (int64_t)g.tiles.size();
-        const int64_t lo = g.slot_ptr[L], hi = g.slot_ptr[L + 1];
-        TileH cur{lo, lo, (int32_t)g.segs.size(), (int32_t)g.segs.size(), 0, 0, 0, 0, 0, 0};
-        int64_t cur_ch = 0;
-        auto close = [&]() {
-            if (cur.s1 > cur.s0) finish_tile(cur);
-            cur = TileH{cur.s1, cur.s1, (int32_t)g.segs.size(), (int32_t)g.segs.size(), 0, 0, 0, 0, 0, 0};
-            cur_ch = 0;
-        };
-        int64_t s = lo;
-        while (s < hi) {
-            int64_t e = s + 1;
-            const int64_t h = slot_h[s];
-            if (h >= 0)
-                while (e < hi && slot_h[e] == h) ++e;
-            const int64_t m = e - s;
-            const int32_t n = (h >= 0) ? (int32_t)(g.qbase_int[h + 1] - g.qbase_int[h]) : 0;
-            int64_t gch = 0;
-            for (int64_t x = s; x < e; ++x) gch += row_elems(x);
-            if (m > kTileSlots || n > kTilePairs) {
-                // split group: its own chunks, accumulated globally (deferred)
-                close();
-                g.deferred[h] = 1;
-                for (int64_t c0 = s; c0 < e; c0 += kTileSlots) {
-                    const int64_t c1 = std::min(e, c0 + kTileSlots);
-                    TileH t{c0, c1, (int32_t)g.segs.size(), 0, n, 0, 0, 0, 0, 0};
-                    g.segs.push_back(SegH{h, c0, c1, 0, 0});
-                    finish_tile(t);
-                }
-                cur = TileH{e, e, (int32_t)g.segs.size(), (int32_t)g.segs.size(), 0, 0, 0, 0, 0, 0};
-                cur_ch = 0;
-                s = e;
-                continue;
-            }
-            const int64_t segs_in = (int64_t)g.segs.size() - cur.seg0;
-            if ((cur.s1 - cur.s0) + m > kTileSlots || cur.npairs + n > kTilePairs ||
-                (h >= 0 && segs_in + 1 > kTileSegs) || (cur.s1 > cur.s0 && cur_ch + gch > kTileChildren))
-                close();
-            if (h >= 0) {
-                g.segs.push_back(SegH{h, s, e, cur.npairs, g.deferred[h] ? 0 : 1});
-                cur.npairs += n;
-            }
-            cur.s1 = e;
-            cur_ch += gch;
-            s = e;
-        }
-        close();
-    }
-    g.tile_ptr[D] = (int64_t)g.tiles.size();
-    for (auto& sg : g.segs)
-        if (g.deferred[sg.h]) sg.fused = 0;
-    g.deferred_list.clear();
-    for (int64_t h = 0; h < H; ++h)
-        if (g.deferred[h]) g.deferred_list.push_back(h);
-
+    build_tiles(g, slot_h);
     tm.mark("tiles");
     // ------------------------------------------------------------------ values
     g.util_c.resize((size_t)V * Pc);

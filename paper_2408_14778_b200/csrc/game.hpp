@@ -3,6 +3,8 @@
 // layout), uploaded by solver.cu.  Not part of the C ABI.
 #pragma once
 #include <cstdint>
+#include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -34,7 +36,7 @@ struct SegH {
 constexpr int kTileSlots = 128;     // parents per tile (= threads per CTA)
 constexpr int kTilePairs = 512;     // (infoset, action) pairs per tile
 constexpr int kTileSegs = 64;       // segments (infosets) per tile
-constexpr int kTileChildren = 2560; // staged child values (R elements, padded rows)
+constexpr int kTileChildren = 2816; // staged child values (R elements, padded rows)
 
 struct Game {
     // ---- input-level facts
@@ -77,7 +79,9 @@ struct Game {
     std::vector<int64_t> qbase_caller;    // [H+1]
     std::vector<uint8_t> owner_int;       // [H]
     std::vector<uint8_t> deferred;        // [H] 1: accumulate globally, update after the pass
-    std::vector<int64_t> deferred_list;
+    std::vector<int64_t> deferred_list;   // internal ids, ascending
+    std::vector<int64_t> dpos;            // [H] index in deferred_list or -1
+    std::vector<int64_t> dqbase;          // [ndef + 1] compact pair base of each deferred infoset
     std::vector<double> chance_vals;      // [C], sigma_ext[Q + c]
 
     // ---- backward tiles
@@ -89,8 +93,31 @@ struct Game {
     std::vector<double> util_c;           // [V * Pc] canonical rows (terminals; 0 elsewhere)
 };
 
+// Multi-GPU level sharding.  Depths 0..cut are
+// the replicated trunk; every deeper node belongs to the rank that owns its
+// depth-`cut` ancestor.  The per-rank view is itself a Game (local canonical
+// numbering), plus the exchange metadata below.
+struct ShardInfo {
+    int rank = 0, world = 1;
+    int cut = -1;                          // -1: nothing sharded (every rank redundant)
+    std::vector<int64_t> cut_row;          // local U row of every cut-level decision node
+    std::vector<uint8_t> cut_owned;        // 1 if this rank computes it
+    std::vector<uint8_t> tile_contrib;     // per local tile: adds deferred partial sums
+    std::vector<uint8_t> report;           // [H] 1 if this rank reports the infoset in readbacks
+    std::vector<int64_t> local_level_nodes;// nodes per depth on this rank
+    int64_t owned_nodes = 0;               // nodes of depths > cut owned here
+};
+bool build_shard(const Game& full, int rank, int world, Game& local, ShardInfo& info, std::string& err);
+// store.cpp: shard files
+std::string shard_path(const std::string& prefix, int rank, int world);
+bool save_shard(const std::string& path, const Game& full, const Game& local, const ShardInfo& info, std::string& err);
+bool load_shard(const std::string& path, Game& head, Game& local, ShardInfo& info, std::string& err);
+
 // flatten.cpp
 bool build_game(const cfr_game_desc* d, Game& g, std::string& err);
+// (re)build tiles + segments + deferred list from the slot arrays; slot_h[s] =
+// internal infoset of player slot s, -1 for chance
+void build_tiles(Game& g, const std::vector<int64_t>& slot_h);
 // E = 1 + ceil(log2(2 max|u|)) (exact-accumulation exponent)
 int game_exponent(double max_abs_u);
 
@@ -98,6 +125,14 @@ int game_exponent(double max_abs_u);
 
 struct cfr_game {
     cfrb::Game g;
+    // per (rank, world) shard views, built on first use (solver workspace sizing
+    // and creation share them)
+    struct Shard {
+        cfrb::Game local;
+        cfrb::ShardInfo info;
+    };
+    std::map<std::pair<int, int>, std::shared_ptr<Shard>> shards;
+    bool shard_only = false;   // loaded from a shard file: `g` holds only the header facts
 };
 
 // error plumbing shared by the product's translation units

@@ -19,6 +19,7 @@
 //                              tiles (accumulated globally with int64 atomics).
 // No tensor cores: the path is a sparse gather/scatter at < 1 flop/byte.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <climits>
@@ -43,10 +44,13 @@ struct TileD {
     int cpr;             // chunks per row (mode 1)
     int stride;          // row stride in elements (mode 1)
     float inv_cpr;       // 1 / cpr
+    int contrib;         // 1: add this tile's deferred partial sums (trunk tiles: rank 0 only)
+    int pad;
 };
 struct SegD {
     long long h, qb;     // internal infoset, qbase[h]
     long long sb, se;    // member slots
+    long long dq, dh;    // compact accumulator pair base / infoset index (deferred only)
     int pair_off, n, owner, fused;
 };
 
@@ -60,8 +64,9 @@ struct DG {
     R* regret;     // [Q] cumulative regret
     R* snum;       // [Q] sum_t w_t pi_bar sigma
     R* sden;       // [H] sum_t w_t pi_bar
-    unsigned long long* acc_r;  // [Q][3] exact slices (deferred infosets)
-    unsigned long long* acc_p;  // [H][3]
+    unsigned long long* acc_r;  // [ndef pairs][3] exact slices of the deferred infosets (compact)
+    unsigned long long* acc_p;  // [ndef][3]; acc_r and acc_p are one contiguous exchange block
+    const long long* dqbase;    // [ndef + 1] compact pair base of each deferred infoset
     const I* f_parent;            // [ND] forward pass (canonical decision order)
     const I* f_e;
     const unsigned char* f_pact;
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
 struct SegS {
     long long h;     // internal infoset
     long long qb;    // qbase[h]
+    long long dq, dh;  // compact accumulator indices (deferred)
     int sb, se;      // tile-local member slots
     int pair_off;    // first pair of the segment in the tile
     int n;           // |A(h)|
@@ -169,29 +175,45 @@ struct SegS {
     int fused;
 };
 
-template <class R, int PC>
-struct TileSmem {
-    R ch[kTileChildren];         // staged child rows (odd strides, conflict-free row reads)
-    R sv[kTileSlots * PC];       // node values of the tile's slots
-    R spc[kTileSlots];           // owner's pi_check per slot
-    R sph[kTileSlots];           // owner's pi_hat per slot
-    R ssig[kTilePairs];          // sigma of the tile's (h, a) pairs
-    R sreg[kTilePairs];          // regret of the tile's pairs (prefetched for the update)
-    R ssn[kTilePairs];           // S_num of the tile's pairs (prefetched)
-    R pib[kTileSegs];            // decoded pi_bar per segment
-    R zs[kTileSegs];             // sum of positive regrets per segment
-    R sden[kTileSegs];           // S_den per segment (prefetched)
-    SegS seg[kTileSegs];
-    int soff[kTileSegs + 1];     // pair offsets of the segments
-    int best[kTileSegs];         // BR argmax per segment
-    int scoff[kTileSlots];       // staged row offset per slot
-    int spoff[kTileSlots];       // pair offset of the slot's segment (-1 chance)
-    long long scb[kTileSlots];   // first child per slot
-    int sn[kTileSlots];          // children per slot
-    unsigned char pseg[kTilePairs];  // segment of each pair
+// Shared-memory layout of one backward launch (per level: sized by the
+// level's largest tile so small tiles leave room for more resident CTAs).
+struct SmemLayout {
+    int ch, sv, spc, sph, ssig, sreg, ssn, pib, zs, sden, seg, soff, best, scoff, spoff, sn, scb, pseg;
+    int bytes;
 };
-// rt / pos alias ch after phase B
-static_assert(kTileChildren >= 2 * kTilePairs, "alias");
+template <class R>
+struct TileView {
+    R *ch, *sv, *spc, *sph, *ssig, *sreg, *ssn, *pib, *zs, *sden;
+    SegS* seg;
+    int *soff, *best, *scoff, *spoff, *sn;
+    long long* scb;
+    unsigned char* pseg;
+};
+template <class R>
+__device__ __forceinline__ TileView<R> make_view(unsigned char* b, const SmemLayout& L) {
+    TileView<R> v;
+    v.ch = (R*)(b + L.ch);
+    v.sv = (R*)(b + L.sv);
+    v.spc = (R*)(b + L.spc);
+    v.sph = (R*)(b + L.sph);
+    v.ssig = (R*)(b + L.ssig);
+    v.sreg = (R*)(b + L.sreg);
+    v.ssn = (R*)(b + L.ssn);
+    v.pib = (R*)(b + L.pib);
+    v.zs = (R*)(b + L.zs);
+    v.sden = (R*)(b + L.sden);
+    v.seg = (SegS*)(b + L.seg);
+    v.soff = (int*)(b + L.soff);
+    v.best = (int*)(b + L.best);
+    v.scoff = (int*)(b + L.scoff);
+    v.spoff = (int*)(b + L.spoff);
+    v.sn = (int*)(b + L.sn);
+    v.scb = (long long*)(b + L.scb);
+    v.pseg = (unsigned char*)(b + L.pseg);
+    return v;
+}
+
+// rt / pos alias ch after phase B (the host sizes ch >= 2 * pairs)
 
 __device__ __forceinline__ int seg_of_pair(const int* soff, int nseg, int p) {
     int lo = 0, hi = nseg - 1;
@@ -204,9 +226,9 @@ __device__ __forceinline__ int seg_of_pair(const int* soff, int nseg, int p) {
 
 template <class R, class I, int PC, int MODE>
 __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restrict__ sig, long long tile0,
-                                                    int br_player, int last) {
+                                                    int br_player, int last, SmemLayout lay) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileSmem<R, PC>& sm = *reinterpret_cast<TileSmem<R, PC>*>(smem_raw);
+    const TileView<R> sm = make_view<R>(smem_raw, lay);
     const TileD T = g.tiles[tile0 + blockIdx.x];
     const int nslot = (int)(T.s1 - T.s0);
     const int nseg = T.seg1 - T.seg0;
@@ -214,7 +236,7 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
     const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
     const int P = g.P;
     R* const rt = sm.ch;                  // valid after phase B
-    R* const pos = sm.ch + kTilePairs;
+    R* const pos = sm.ch + (lay.ssn - lay.ssig) / (int)sizeof(R);   // = ch + (pairs capacity)
     const bool sig_staged = T.npairs <= kTilePairs;
     const bool staged = T.staged != 0;
     constexpr int CH = (sizeof(R) == 8) ? 16 : 8;     // cp.async chunk (bytes) of uniform tiles
@@ -246,6 +268,8 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
         SegS ss;
         ss.h = sg.h;
         ss.qb = sg.qb;
+        ss.dq = sg.dq;
+        ss.dh = sg.dh;
         ss.n = sg.n;
         ss.owner = sg.owner;
         ss.sb = (int)(sg.sb - T.s0);
@@ -392,14 +416,14 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
                 else if (rd == 2) kr2 = x;
                 else if (rd == 3) kr3 = x;
                 else kr4 = x;
-            } else if (MODE == MODE_CFR) {
+            } else if (MODE == MODE_CFR && T.contrib) {
                 if (is_pair) {
-                    const long long q = sm.seg[k].qb + a;
+                    const long long q = sm.seg[k].dq + a;
                     atomicAdd(&g.acc_r[q * 3 + 0], (unsigned long long)(long long)c0);
                     atomicAdd(&g.acc_r[q * 3 + 1], (unsigned long long)(long long)c1);
                     atomicAdd(&g.acc_r[q * 3 + 2], (unsigned long long)(long long)c2);
                 } else {
-                    const long long h = sm.seg[k].h;
+                    const long long h = sm.seg[k].dh;
                     atomicAdd(&g.acc_p[h * 3 + 0], (unsigned long long)(long long)c0);
                     atomicAdd(&g.acc_p[h * 3 + 1], (unsigned long long)(long long)c1);
                     atomicAdd(&g.acc_p[h * 3 + 2], (unsigned long long)(long long)c2);
@@ -516,21 +540,23 @@ __global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
         const long long h = (long long)g.deferred[idx];
         const long long qb = (long long)g.qbase[h];
         const int n = (int)((long long)g.qbase[h + 1] - qb);
-        const long long p0 = (long long)g.acc_p[h * 3 + 0], p1 = (long long)g.acc_p[h * 3 + 1],
-                        p2 = (long long)g.acc_p[h * 3 + 2];
-        g.acc_p[h * 3 + 0] = 0;
-        g.acc_p[h * 3 + 1] = 0;
-        g.acc_p[h * 3 + 2] = 0;
+        const long long dq = g.dqbase[idx];
+        const long long p0 = (long long)g.acc_p[idx * 3 + 0], p1 = (long long)g.acc_p[idx * 3 + 1],
+                        p2 = (long long)g.acc_p[idx * 3 + 2];
+        g.acc_p[idx * 3 + 0] = 0;
+        g.acc_p[idx * 3 + 1] = 0;
+        g.acc_p[idx * 3 + 2] = 0;
         const R pib = (R)xdec_ll(p0, p1, p2, g.rcp);
         const R wp = w * pib;
         R z = (R)0;
         for (int a = 0; a < n; ++a) {
             const long long q = qb + a;
-            const long long c0 = (long long)g.acc_r[q * 3 + 0], c1 = (long long)g.acc_r[q * 3 + 1],
-                            c2 = (long long)g.acc_r[q * 3 + 2];
-            g.acc_r[q * 3 + 0] = 0;
-            g.acc_r[q * 3 + 1] = 0;
-            g.acc_r[q * 3 + 2] = 0;
+            const long long cq = dq + a;
+            const long long c0 = (long long)g.acc_r[cq * 3 + 0], c1 = (long long)g.acc_r[cq * 3 + 1],
+                            c2 = (long long)g.acc_r[cq * 3 + 2];
+            g.acc_r[cq * 3 + 0] = 0;
+            g.acc_r[cq * 3 + 1] = 0;
+            g.acc_r[cq * 3 + 2] = 0;
             const R rt = (R)xdec_ll(c0, c1, c2, g.rc);
             R r;
             if (g.variant == 0) {
@@ -584,6 +610,34 @@ __global__ void k_average(DG<R, I> g, R* out, long long H, long long Q, long lon
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < C; c += stride) out[Q + c] = g.sig[Q + c];
 }
 
+// Multi-GPU exchange 1: cut-level decision values.  Each row is
+// written by exactly one rank (others contribute zeros), so a sum-allreduce is exact.
+template <class R>
+__global__ void k_cut_pack(const R* __restrict__ U, const long long* __restrict__ rows,
+                           const unsigned char* __restrict__ owned, R* __restrict__ buf, long long n, int Pc) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        for (int j = 0; j < Pc; ++j) buf[i * Pc + j] = owned[i] ? U[rows[i] * Pc + j] : (R)0;
+}
+template <class R>
+__global__ void k_cut_unpack(R* __restrict__ U, const long long* __restrict__ rows, const R* __restrict__ buf, long long n,
+                             int Pc) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        for (int j = 0; j < Pc; ++j) U[rows[i] * Pc + j] = buf[i * Pc + j];
+}
+// Readback combination: zero the (h, a) entries this rank does not report.
+template <class R, class I>
+__global__ void k_mask_q(R* __restrict__ out, const I* __restrict__ qbase, const unsigned char* __restrict__ report,
+                         long long H) {
+    for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < H; h += (long long)gridDim.x * blockDim.x)
+        if (!report[h])
+            for (long long q = (long long)qbase[h]; q < (long long)qbase[h + 1]; ++q) out[q] = (R)0;
+}
+template <class R>
+__global__ void k_mask_h(R* __restrict__ out, const unsigned char* __restrict__ report, long long H) {
+    for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < H; h += (long long)gridDim.x * blockDim.x)
+        if (!report[h]) out[h] = (R)0;
+}
+
 // --------------------------------------------------------------- host side
 #define CU(call)                                                                                   \
     do {                                                                                           \
@@ -606,6 +660,10 @@ struct SolverBase {
     virtual cfr_status launches(int64_t* n) = 0;
     virtual cfr_status profile(int64_t iters, double* out) = 0;
     virtual cfr_status model_bytes(double* out) = 0;
+    virtual cfr_status phase(int ph, double* out) = 0;
+    virtual cfr_status exchange_size(int which, size_t* bytes) = 0;
+    virtual cfr_status exchange(int which, int put, void* host, size_t bytes) = 0;
+    virtual cfr_status shard_info(int64_t* out) = 0;
 };
 
 struct Layout {
@@ -636,12 +694,13 @@ static std::vector<int64_t> u_layout(const Game& g, size_t elem) {
 
 template <class R, class I>
 struct Plan {
-    size_t U, reach, sig, sig_eval, regret, snum, sden, acc_r, acc_p;
+    size_t U, reach, sig, sig_eval, regret, snum, sden, acc_r, acc_p, dqbase;
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, ctrl, out;
+    size_t cutbuf, cutrow, cutown, report;
     size_t total;
-    explicit Plan(const Game& g) {
+    explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
         Layout L;
         const size_t NS = (size_t)g.NS, ND = (size_t)g.ND, Q = (size_t)g.Q, H = (size_t)g.H, C = (size_t)g.C;
         U = L.take<R>((size_t)u_layout(g, sizeof(R)).back() * g.Pc + 8);
@@ -651,8 +710,10 @@ struct Plan {
         regret = L.take<R>(Q);
         snum = L.take<R>(Q);
         sden = L.take<R>(H);
-        acc_r = L.take<unsigned long long>(3 * Q);
-        acc_p = L.take<unsigned long long>(3 * H);
+        const size_t ndq = g.dqbase.empty() ? 0 : (size_t)g.dqbase.back();
+        acc_r = L.take<unsigned long long>(3 * ndq + 3 * g.deferred_list.size());   // one exchange block
+        acc_p = acc_r + 3 * ndq * sizeof(unsigned long long);
+        dqbase = L.take<long long>(g.deferred_list.size() + 1);
         f_parent = L.take<I>(ND);
         f_e = L.take<I>(ND);
         f_pact = L.take<unsigned char>(ND);
@@ -670,6 +731,11 @@ struct Plan {
         deferred = L.take<I>(g.deferred_list.size());
         ctrl = L.take<long long>(8);
         out = L.take<R>(std::max<size_t>(Q + C, (size_t)g.P * 2 + 8));
+        const size_t ncut = sh ? sh->cut_row.size() : 0;
+        cutbuf = L.take<R>(ncut * g.Pc + 1);
+        cutrow = L.take<long long>(ncut + 1);
+        cutown = L.take<unsigned char>(ncut + 1);
+        report = L.take<unsigned char>(H + 1);
         total = L.off + 256;
     }
 };
@@ -683,25 +749,36 @@ static std::vector<T> narrow(const std::vector<S>& v) {
 
 template <class R, class I>
 struct Solver final : SolverBase {
-    const Game* gp;
+    const Game* gp;               // the (local) game this rank iterates
+    const Game* full;             // the whole game (caller order readbacks)
     cfr_solver_config cfg;
     cudaStream_t stream;
     cudaStream_t cap_stream = nullptr;
     unsigned char* ws;
+    const ShardInfo* sh;          // multi-GPU view (cut = -1 on one GPU)
     Plan<R, I> plan;
     DG<R, I> dg;
     cudaGraphExec_t gexec = nullptr;
     int E = 1;
     int64_t launches_per_iter = 0;
     bool use_graph = true;
+    int world = 1, rank = 0;
+    bool external = false;        // world > 1 without NCCL: the caller runs the exchanges
+    ncclComm_t comm = nullptr;
 
-    Solver(const Game* g, const cfr_solver_config& c, void* w, cudaStream_t s)
-        : gp(g), cfg(c), stream(s), ws((unsigned char*)w), plan(*g) {}
+    Solver(const Game* g, const Game* f, const ShardInfo* s_, const cfr_solver_config& c, void* w, cudaStream_t s)
+        : gp(g), full(f), cfg(c), stream(s), ws((unsigned char*)w), sh(s_), plan(*g, s_) {
+        world = sh->world;
+        rank = sh->rank;
+    }
 
     ~Solver() override {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (cap_stream) cudaStreamDestroy(cap_stream);
+        if (comm) ncclCommDestroy(comm);
     }
+    bool sharded() const { return sh->cut >= 0; }
+    int64_t ncut() const { return (int64_t)sh->cut_row.size(); }
 
     template <class T>
     T* at(size_t off) { return reinterpret_cast<T*>(ws + off); }
@@ -712,17 +789,88 @@ struct Solver final : SolverBase {
         return CFR_OK;
     }
 
-    size_t smem_bytes() const {
-        switch (gp->Pc) {
-            case 1: return sizeof(TileSmem<R, 1>);
-            case 2: return sizeof(TileSmem<R, 2>);
-            case 3: return sizeof(TileSmem<R, 3>);
-            default: return sizeof(TileSmem<R, 4>);
+    size_t acc_bytes() const {
+        const size_t ndq = gp->dqbase.empty() ? 0 : (size_t)gp->dqbase.back();
+        return (3 * ndq + 3 * gp->deferred_list.size()) * sizeof(unsigned long long);
+    }
+    std::vector<uint8_t> tile_contrib_;   // set by the sharded path; empty = all tiles contribute
+    int contrib_of_tile(size_t t) const { return tile_contrib_.empty() ? 1 : (int)tile_contrib_[t]; }
+    std::vector<SmemLayout> lay_;   // per parent level
+    int max_smem_ = 0;
+
+    SmemLayout make_layout(int maxch, int maxslot, int maxpairs, int maxseg) const {
+        const int Pc = gp->Pc;
+        const int w = (int)sizeof(R);
+        int off = 0;
+        auto take = [&](int bytes) {
+            const int o = off;
+            off = (off + bytes + 15) & ~15;
+            return o;
+        };
+        const int pairs_b = ((maxpairs * w + 15) & ~15);
+        SmemLayout L{};
+        L.ch = take(std::max(maxch * w, 2 * pairs_b));
+        L.sv = take(maxslot * Pc * w);
+        L.spc = take(maxslot * w);
+        L.sph = take(maxslot * w);
+        L.ssig = take(pairs_b);
+        L.sreg = take(pairs_b);
+        L.ssn = take(pairs_b);
+        L.pib = take(maxseg * w);
+        L.zs = take(maxseg * w);
+        L.sden = take(maxseg * w);
+        L.seg = take(maxseg * (int)sizeof(SegS));
+        L.soff = take((maxseg + 1) * 4);
+        L.best = take(maxseg * 4);
+        L.scoff = take(maxslot * 4);
+        L.spoff = take(maxslot * 4);
+        L.sn = take(maxslot * 4);
+        L.scb = take(maxslot * 8);
+        L.pseg = take(maxpairs);
+        L.bytes = off;
+        return L;
+    }
+
+    void build_layouts(const std::vector<TileD>& tiles) {
+        const Game& g = *gp;
+        lay_.assign(g.D, SmemLayout{});
+        max_smem_ = 0;
+        for (int L = 0; L < g.D; ++L) {
+            int maxch = 0, maxslot = 1, maxpairs = 1, maxseg = 1;
+            for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1]; ++t) {
+                const TileD& td = tiles[t];
+                const int nslot = (int)(td.s1 - td.s0);
+                maxslot = std::max(maxslot, nslot);
+                maxseg = std::max(maxseg, td.seg1 - td.seg0);
+                if (td.npairs <= kTilePairs) maxpairs = std::max(maxpairs, td.npairs);
+                int ch = 0;
+                if (td.staged == 1) ch = nslot * td.stride;
+                else if (td.staged == 2) {
+                    for (int64_t s = td.s0; s < td.s1; ++s) ch += (g.s_n[s] * g.Pc) | 1;
+                }
+                maxch = std::max(maxch, ch);
+            }
+            lay_[L] = make_layout(maxch, maxslot, maxpairs, maxseg);
+            max_smem_ = std::max(max_smem_, lay_[L].bytes);
         }
     }
 
-    cfr_status init() {
+    cfr_status init(const void* nccl_id) {
         const Game& g = *gp;
+        tile_contrib_ = sh->tile_contrib;
+        if (world > 1) {
+            if (nccl_id) {
+                ncclUniqueId id;
+                std::memcpy(&id, nccl_id, sizeof(id));
+                const ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
+                if (r != ncclSuccess) {
+                    cfrb_set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+                    return CFR_ERR_NCCL;
+                }
+            } else {
+                external = true;   // the caller performs the two exchanges (cfr_solver_phase)
+            }
+        }
         if (g.Pc > 4) {
             cfrb_set_error("non-zero-sum games with more than 4 players are not supported by the device kernels");
             return CFR_ERR_UNSUPPORTED;
@@ -741,6 +889,7 @@ struct Solver final : SolverBase {
         dg.sden = at<R>(plan.sden);
         dg.acc_r = at<unsigned long long>(plan.acc_r);
         dg.acc_p = at<unsigned long long>(plan.acc_p);
+        dg.dqbase = at<long long>(plan.dqbase);
         dg.f_parent = at<I>(plan.f_parent);
         dg.f_e = at<I>(plan.f_e);
         dg.f_pact = at<unsigned char>(plan.f_pact);
@@ -801,6 +950,7 @@ struct Solver final : SolverBase {
                 td.seg1 = th.seg1;
                 td.npairs = th.npairs;
                 td.staged = th.staged ? 2 : 0;
+                td.contrib = contrib_of_tile(t);
                 if (th.staged) {
                     const int rowlen = g.s_n[th.s0] * g.Pc;
                     bool uni = (rowlen % CE) == 0;
@@ -833,6 +983,8 @@ struct Solver final : SolverBase {
             sd.owner = g.owner_int[sh.h];
             sd.sb = sh.sb;
             sd.se = sh.se;
+            sd.dq = g.dpos[sh.h] >= 0 ? g.dqbase[g.dpos[sh.h]] : -1;
+            sd.dh = g.dpos[sh.h];
             sd.pair_off = sh.pair_off;
             sd.fused = sh.fused;
             segs[k] = sd;
@@ -850,8 +1002,22 @@ struct Solver final : SolverBase {
         if ((st = up(plan.qbase, narrow<I>(g.qbase_int)))) return st;
         if ((st = up(plan.owner, g.owner_int))) return st;
         if ((st = up(plan.tiles, tiles))) return st;
+        build_layouts(tiles);
         if ((st = up(plan.segs, segs))) return st;
         if ((st = up(plan.deferred, narrow<I>(g.deferred_list)))) return st;
+        if ((st = up(plan.dqbase, narrow<long long>(g.dqbase)))) return st;
+        if (ncut() > 0) {
+            // cut rows are local canonical indices of depth `cut`: map to U rows
+            std::vector<long long> rows(sh->cut_row.size());
+            for (size_t i = 0; i < rows.size(); ++i)
+                rows[i] = uoff[sh->cut] + (sh->cut_row[i] - g.level_ptr[sh->cut]);
+            if ((st = up(plan.cutrow, rows))) return st;
+            if ((st = up(plan.cutown, sh->cut_owned))) return st;
+        }
+        if (world > 1 && g.H > 0) {
+            // report mask in internal infoset order
+            if ((st = up(plan.report, sh->report))) return st;
+        }
         // sigma^(1) = 1/|A(h)| and chance probabilities (rounded once, Q14)
         {
             std::vector<R> s0(g.Q + g.C);
@@ -866,8 +1032,7 @@ struct Solver final : SolverBase {
         CU(cudaMemsetAsync(ws + plan.regret, 0, g.Q * sizeof(R), stream));
         CU(cudaMemsetAsync(ws + plan.snum, 0, g.Q * sizeof(R), stream));
         CU(cudaMemsetAsync(ws + plan.sden, 0, g.H * sizeof(R), stream));
-        CU(cudaMemsetAsync(ws + plan.acc_r, 0, 3 * g.Q * sizeof(unsigned long long), stream));
-        CU(cudaMemsetAsync(ws + plan.acc_p, 0, 3 * g.H * sizeof(unsigned long long), stream));
+        CU(cudaMemsetAsync(ws + plan.acc_r, 0, acc_bytes(), stream));
         CU(cudaMemsetAsync(ws + plan.reach, 0, 2 * (size_t)g.P * g.ND * sizeof(R), stream));
         {
             // root reach factors = 1 (Eq 2 / Eq 4 base case); the root is decision 0
@@ -879,10 +1044,21 @@ struct Solver final : SolverBase {
         }
         CU(cudaStreamSynchronize(stream));
         // kernel attributes (dynamic smem above 48 KB needs opt-in)
-        const int sm = (int)smem_bytes();
-        CU(set_smem_attr(sm));
+        // The attribute is per kernel function, shared by every solver of the
+        // process: opt in to the device maximum once (occupancy depends only on the
+        // dynamic size requested at launch).
+        {
+            int dev = 0, optin = 0;
+            CU(cudaGetDevice(&dev));
+            CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            if (max_smem_ > optin) {
+                cfrb_set_error("tile shared-memory layout exceeds the device limit");
+                return CFR_ERR_UNSUPPORTED;
+            }
+            CU(set_smem_attr(optin));
+        }
         launches_per_iter = count_launches();
-        if (use_graph && g.NS > 0) {
+        if (use_graph && g.NS > 0 && !external) {
             CU(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
             cudaGraph_t graph;
             CU(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -947,13 +1123,14 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         const long long t0 = g.tile_ptr[L], t1 = g.tile_ptr[L + 1];
         if (t1 <= t0) return;
-        const size_t sm = smem_bytes();
+        const SmemLayout lay = lay_[L];
+        const size_t sm = (size_t)lay.bytes;
         const unsigned nb = (unsigned)(t1 - t0);
         switch (g.Pc) {
-            case 1: k_bwd<R, I, 1, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last); break;
-            case 2: k_bwd<R, I, 2, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last); break;
-            case 3: k_bwd<R, I, 3, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last); break;
-            default: k_bwd<R, I, 4, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last); break;
+            case 1: k_bwd<R, I, 1, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last, lay); break;
+            case 2: k_bwd<R, I, 2, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last, lay); break;
+            case 3: k_bwd<R, I, 3, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last, lay); break;
+            default: k_bwd<R, I, 4, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last, lay); break;
         }
     }
 
@@ -963,38 +1140,101 @@ struct Solver final : SolverBase {
         k_deferred<R, I><<<blocks, 256, 0, st>>>(dg, last);
     }
 
-    // One iteration: forward levels, backward levels (fused update), deferred update.
-    // `ev` (optional) receives events around each launch for profiling.
-    cfr_status launch_iteration(cudaStream_t st, std::vector<cudaEvent_t>* ev) {
+    // ---- iteration phases.  One iteration = lower (forward + backward of the
+    // owned levels, down to the cut) -> [exchange 1: cut values] -> upper (trunk
+    // backward) -> [exchange 2: deferred exact sums] -> deferred update.  On one
+    // GPU the cut is -1: lower is the whole pass and both exchanges vanish.
+    // `ev` (optional) collects (tag, level, event) for profiling: tag 0 forward,
+    // 1 backward, 2 deferred update, 3 exchange.
+    struct Mark {
+        int tag, level;
+        cudaEvent_t e;
+    };
+    void mark(cudaStream_t st, std::vector<Mark>* ev, int tag, int level) {
+        if (!ev) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        ev->push_back(Mark{tag, level, e});
+    }
+    bool has_def() const { return !gp->deferred_list.empty(); }
+
+    void launch_lower(cudaStream_t st, int mode, const R* sig, std::vector<Mark>* ev) {
         const Game& g = *gp;
-        const bool has_def = !g.deferred_list.empty();
-        auto mark = [&]() {
-            if (ev) {
-                cudaEvent_t e;
-                cudaEventCreate(&e);
-                cudaEventRecord(e, st);
-                ev->push_back(e);
+        if (mode == MODE_CFR)
+            for (int l = 1; l < g.D; ++l) {
+                fwd_level(st, sig, l);
+                mark(st, ev, 0, l);
             }
-        };
-        mark();
-        for (int l = 1; l < g.D; ++l) {
-            fwd_level(st, dg.sig, l);
-            mark();
+        const int stop = sharded() ? sh->cut : 0;
+        for (int L = g.D - 1; L >= stop; --L) {
+            const int last = (mode == MODE_CFR && L == 0 && !has_def()) ? 1 : 0;
+            if (mode == MODE_CFR) bwd_level<MODE_CFR>(st, sig, L, 0, last);
+            else bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
+            mark(st, ev, 1, L);
         }
-        for (int L = g.D - 1; L >= 0; --L) {
-            bwd_level<MODE_CFR>(st, dg.sig, L, 0, (L == 0 && !has_def) ? 1 : 0);
-            mark();
+        if (sharded()) {
+            const long long n = ncut();
+            const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148));
+            k_cut_pack<R><<<nb, 256, 0, st>>>(dg.U, at<long long>(plan.cutrow), at<unsigned char>(plan.cutown),
+                                              at<R>(plan.cutbuf), n, g.Pc);
         }
-        if (has_def) {
+    }
+    void launch_upper(cudaStream_t st, int mode, const R* sig, std::vector<Mark>* ev) {
+        const Game& g = *gp;
+        if (!sharded()) return;
+        const long long n = ncut();
+        const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148));
+        k_cut_unpack<R><<<nb, 256, 0, st>>>(dg.U, at<long long>(plan.cutrow), at<R>(plan.cutbuf), n, g.Pc);
+        for (int L = sh->cut - 1; L >= 0; --L) {
+            const int last = (mode == MODE_CFR && L == 0 && !has_def()) ? 1 : 0;
+            if (mode == MODE_CFR) bwd_level<MODE_CFR>(st, sig, L, 0, last);
+            else bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
+            mark(st, ev, 1, L);
+        }
+    }
+    void launch_update(cudaStream_t st, std::vector<Mark>* ev) {
+        if (has_def()) {
             deferred_update(st, 1);
-            mark();
+            mark(st, ev, 2, -1);
         }
+    }
+    cfr_status nccl_sum(cudaStream_t st, void* buf, size_t count, ncclDataType_t t) {
+        if (!comm || count == 0) return CFR_OK;
+        const ncclResult_t r = ncclAllReduce(buf, buf, count, t, ncclSum, comm, st);
+        if (r != ncclSuccess) {
+            cfrb_set_error(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+            return CFR_ERR_NCCL;
+        }
+        return CFR_OK;
+    }
+    static ncclDataType_t rtype() { return sizeof(R) == 8 ? ncclFloat64 : ncclFloat32; }
+
+    cfr_status launch_iteration(cudaStream_t st, std::vector<Mark>* ev) {
+        const Game& g = *gp;
+        cfr_status s;
+        mark(st, ev, -1, 0);
+        launch_lower(st, MODE_CFR, dg.sig, ev);
+        if (sharded()) {
+            if ((s = nccl_sum(st, at<R>(plan.cutbuf), (size_t)ncut() * g.Pc, rtype()))) return s;
+            mark(st, ev, 3, -1);
+            launch_upper(st, MODE_CFR, dg.sig, ev);
+        }
+        if (world > 1 && has_def()) {
+            if ((s = nccl_sum(st, dg.acc_r, acc_bytes() / 8, ncclInt64))) return s;
+            mark(st, ev, 3, -1);
+        }
+        launch_update(st, ev);
         CU(cudaGetLastError());
         return CFR_OK;
     }
 
     cfr_status enqueue(int64_t iters) override {
         if (gp->NS == 0) return CFR_OK;   // one-node game: nothing to iterate
+        if (external) {
+            cfrb_set_error("world_size > 1 without an NCCL id: drive the iteration with cfr_solver_phase");
+            return CFR_ERR_UNSUPPORTED;
+        }
         for (int64_t k = 0; k < iters; ++k) {
             if (gexec) CU(cudaGraphLaunch(gexec, stream));
             else {
@@ -1025,10 +1265,36 @@ struct Solver final : SolverBase {
     }
 
     // device buffer (internal q order) -> host doubles in caller order
+    // Multi-GPU readback combination: every rank zeroes what it does not report
+    // (trunk + deferred infosets: rank 0; shard-local infosets: their owner) and a
+    // sum-allreduce completes the array (exact: one nonzero contribution).  In the
+    // external mode the caller sums the partial arrays itself.
+    cfr_status combine_q(R* dptr) {
+        const Game& g = *gp;
+        if (world <= 1) return CFR_OK;
+        const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((g.H + 255) / 256, 148LL * 8));
+        if (g.H) k_mask_q<R, I><<<nb, 256, 0, stream>>>(dptr, dg.qbase, at<unsigned char>(plan.report), g.H);
+        CU(cudaGetLastError());
+        return nccl_sum(stream, dptr, (size_t)g.Q, rtype());
+    }
+    cfr_status combine_h(R* dptr) {
+        const Game& g = *gp;
+        if (world <= 1) return CFR_OK;
+        const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((g.H + 255) / 256, 148LL * 8));
+        if (g.H) k_mask_h<R><<<nb, 256, 0, stream>>>(dptr, at<unsigned char>(plan.report), g.H);
+        CU(cudaGetLastError());
+        return nccl_sum(stream, dptr, (size_t)g.H, rtype());
+    }
+
+    // device buffer (internal q order) -> combined -> host doubles in caller order
     cfr_status read_q(const R* dptr, double* out) {
         const Game& g = *gp;
+        R* tmpd = at<R>(plan.out);
+        if (g.Q) CU(cudaMemcpyAsync(tmpd, dptr, g.Q * sizeof(R), cudaMemcpyDeviceToDevice, stream));
+        cfr_status s = combine_q(tmpd);
+        if (s) return s;
         std::vector<R> tmp(g.Q);
-        if (g.Q) CU(cudaMemcpyAsync(tmp.data(), dptr, g.Q * sizeof(R), cudaMemcpyDeviceToHost, stream));
+        if (g.Q) CU(cudaMemcpyAsync(tmp.data(), tmpd, g.Q * sizeof(R), cudaMemcpyDeviceToHost, stream));
         CU(cudaStreamSynchronize(stream));
         for (int64_t hc = 0; hc < g.H; ++hc) {
             const int64_t hi = g.h_int_of_caller[hc];
@@ -1063,19 +1329,19 @@ struct Solver final : SolverBase {
         if (regret && (s = read_q(dg.regret, regret))) return s;
         if (snum && (s = read_q(dg.snum, snum))) return s;
         if (sden) {
+            R* tmpd = at<R>(plan.out);
+            if (g.H) CU(cudaMemcpyAsync(tmpd, dg.sden, g.H * sizeof(R), cudaMemcpyDeviceToDevice, stream));
+            if ((s = combine_h(tmpd))) return s;
             std::vector<R> tmp(g.H);
-            if (g.H) CU(cudaMemcpyAsync(tmp.data(), dg.sden, g.H * sizeof(R), cudaMemcpyDeviceToHost, stream));
+            if (g.H) CU(cudaMemcpyAsync(tmp.data(), tmpd, g.H * sizeof(R), cudaMemcpyDeviceToHost, stream));
             CU(cudaStreamSynchronize(stream));
             for (int64_t hc = 0; hc < g.H; ++hc) sden[hc] = (double)tmp[g.h_int_of_caller[hc]];
         }
         return CFR_OK;
     }
 
-    // values-only backward pass under `sig` -> root values (P entries, double)
-    cfr_status root_values(const R* sig, double* out) {
+    cfr_status read_root(double* out) {
         const Game& g = *gp;
-        for (int L = g.D - 1; L >= 0; --L) bwd_level<MODE_VALUES>(stream, sig, L, 0, 0);
-        CU(cudaGetLastError());
         std::vector<R> r(g.Pc);
         CU(cudaMemcpyAsync(r.data(), dg.U, g.Pc * sizeof(R), cudaMemcpyDeviceToHost, stream));
         CU(cudaStreamSynchronize(stream));
@@ -1088,7 +1354,24 @@ struct Solver final : SolverBase {
         return CFR_OK;
     }
 
+    // values-only backward pass under `sig` -> root values (P entries, double)
+    cfr_status root_values(const R* sig, double* out) {
+        const Game& g = *gp;
+        launch_lower(stream, MODE_VALUES, sig, nullptr);
+        if (sharded()) {
+            cfr_status s = nccl_sum(stream, at<R>(plan.cutbuf), (size_t)ncut() * g.Pc, rtype());
+            if (s) return s;
+            launch_upper(stream, MODE_VALUES, sig, nullptr);
+        }
+        CU(cudaGetLastError());
+        return read_root(out);
+    }
+
     cfr_status expected_values(int which, double* out) override {
+        if (external) {
+            cfrb_set_error("world_size > 1 without an NCCL id: use cfr_solver_phase (EV phases)");
+            return CFR_ERR_UNSUPPORTED;
+        }
         CU(cudaStreamSynchronize(stream));
         const R* sig = dg.sig;
         if (which == CFR_EV_AVERAGE) {
@@ -1101,6 +1384,10 @@ struct Solver final : SolverBase {
 
     cfr_status exploitability(double* nc, double* ex, double* br) override {
         const Game& g = *gp;
+        if (world > 1) {
+            cfrb_set_error("device best response is single-GPU in this version (DESIGN.md §9)");
+            return CFR_ERR_UNSUPPORTED;
+        }
         if (!g.depth_homogeneous || !g.deferred_list.empty()) {
             cfrb_set_error("device best response needs every infoset on one depth and inside one tile (reading Q17)");
             return CFR_ERR_UNSUPPORTED;
@@ -1142,30 +1429,27 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         for (int k = 0; k < 5; ++k) out[k] = 0.0;
         if (g.NS == 0 || iters <= 0) return CFR_OK;
+        if (external) {
+            cfrb_set_error("profile needs NCCL or a single GPU");
+            return CFR_ERR_UNSUPPORTED;
+        }
         std::vector<double> per_bwd(g.D, 0.0);
         for (int64_t it = 0; it < iters; ++it) {
-            std::vector<cudaEvent_t> ev;
+            std::vector<Mark> ev;
             cfr_status s = launch_iteration(stream, &ev);
             if (s) return s;
             CU(cudaStreamSynchronize(stream));
-            size_t e = 1;
-            for (int l = 1; l < g.D; ++l, ++e) {
+            for (size_t e = 1; e < ev.size(); ++e) {
                 float ms = 0;
-                cudaEventElapsedTime(&ms, ev[e - 1], ev[e]);
-                out[0] += ms;
+                cudaEventElapsedTime(&ms, ev[e - 1].e, ev[e].e);
+                switch (ev[e].tag) {
+                    case 0: out[0] += ms; break;
+                    case 1: out[1] += ms; per_bwd[ev[e].level] += ms; break;
+                    case 2: out[2] += ms; break;
+                    default: out[2] += ms; break;   // exchanges are reported with the update
+                }
             }
-            for (int L = g.D - 1; L >= 0; --L, ++e) {
-                float ms = 0;
-                cudaEventElapsedTime(&ms, ev[e - 1], ev[e]);
-                out[1] += ms;
-                per_bwd[L] += ms;
-            }
-            if (!g.deferred_list.empty()) {
-                float ms = 0;
-                cudaEventElapsedTime(&ms, ev[e - 1], ev[e]);
-                out[2] += ms;
-            }
-            for (auto x : ev) cudaEventDestroy(x);
+            for (auto& m : ev) cudaEventDestroy(m.e);
         }
         int dom = 0;
         for (int L = 0; L < g.D; ++L)
@@ -1177,6 +1461,73 @@ struct Solver final : SolverBase {
         out[4] = dom;
         dom_level = dom;
         return sync();
+    }
+
+    // ---- externally driven multi-GPU iteration (tests; world > 1 without NCCL)
+    cfr_status phase(int ph, double* out) override {
+        const Game& g = *gp;
+        if (g.NS == 0) return CFR_OK;
+        switch (ph) {
+            case 0: launch_lower(stream, MODE_CFR, dg.sig, nullptr); break;
+            case 1: launch_upper(stream, MODE_CFR, dg.sig, nullptr); break;
+            case 2: launch_update(stream, nullptr); break;
+            case 3: {
+                cfr_status s = compute_average();
+                if (s) return s;
+                launch_lower(stream, MODE_VALUES, at<R>(plan.sig_eval), nullptr);
+                break;
+            }
+            case 4: {
+                launch_upper(stream, MODE_VALUES, at<R>(plan.sig_eval), nullptr);
+                if (out) {
+                    cfr_status s = read_root(out);
+                    if (s) return s;
+                }
+                break;
+            }
+            default:
+                cfrb_set_error("bad phase");
+                return CFR_ERR_INVALID_ARG;
+        }
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(stream));
+        return CFR_OK;
+    }
+    cfr_status exchange_size(int which, size_t* bytes) override {
+        if (which == 0) *bytes = (size_t)ncut() * gp->Pc * sizeof(R);
+        else if (which == 1) *bytes = acc_bytes();
+        else {
+            cfrb_set_error("bad exchange id");
+            return CFR_ERR_INVALID_ARG;
+        }
+        return CFR_OK;
+    }
+    cfr_status exchange(int which, int put, void* host, size_t bytes) override {
+        size_t need = 0;
+        cfr_status s = exchange_size(which, &need);
+        if (s) return s;
+        if (bytes != need) {
+            cfrb_set_error("exchange buffer size mismatch: need " + std::to_string(need));
+            return CFR_ERR_INVALID_ARG;
+        }
+        if (need == 0) return CFR_OK;
+        unsigned char* dev = (which == 0) ? ws + plan.cutbuf : (unsigned char*)dg.acc_r;
+        CU(cudaStreamSynchronize(stream));
+        if (put) CU(cudaMemcpy(dev, host, need, cudaMemcpyHostToDevice));
+        else CU(cudaMemcpy(host, dev, need, cudaMemcpyDeviceToHost));
+        return CFR_OK;
+    }
+    cfr_status shard_info(int64_t* out) override {
+        const Game& g = *gp;
+        out[0] = sh->cut;
+        out[1] = ncut();
+        out[2] = sh->owned_nodes;
+        out[3] = g.V;
+        out[4] = g.NS;
+        out[5] = (int64_t)g.deferred_list.size();
+        out[6] = g.dqbase.empty() ? 0 : g.dqbase.back();
+        out[7] = world;
+        return CFR_OK;
     }
 
     // Algorithmic DRAM bytes per iteration (DESIGN.md §6 byte model).
@@ -1239,11 +1590,50 @@ static bool use_idx32(const Game& g) {
     return g.V < lim && (g.Q + g.C) < lim && g.NS < lim;
 }
 
-static cfr_status bytes_for(const Game& g, int precision, size_t* out) {
-    const bool i32 = use_idx32(g);
-    if (precision == 64) *out = i32 ? Plan<double, int>(g).total : Plan<double, long long>(g).total;
-    else *out = i32 ? Plan<float, int>(g).total : Plan<float, long long>(g).total;
+// The game a rank iterates + its shard metadata (world 1: the whole game).
+static cfr_status view_for(cfr_game* G, const cfr_dist* dist, const Game** local, const ShardInfo** info,
+                           std::shared_ptr<cfr_game::Shard>* keep) {
+    static const ShardInfo single{};
+    const int world = dist ? dist->world_size : 1;
+    const int rank = dist ? dist->rank : 0;
+    if (world < 1 || rank < 0 || rank >= world) {
+        cfrb_set_error("bad cfr_dist (rank / world_size)");
+        return CFR_ERR_INVALID_ARG;
+    }
+    if (world == 1) {
+        if (G->shard_only) {
+            cfrb_set_error("a game loaded from a shard file needs its (rank, world_size)");
+            return CFR_ERR_INVALID_ARG;
+        }
+        *local = &G->g;
+        *info = &single;
+        return CFR_OK;
+    }
+    auto key = std::make_pair(rank, world);
+    auto it = G->shards.find(key);
+    if (it == G->shards.end() && G->shard_only) {
+        cfrb_set_error("this game was loaded from a shard file for another (rank, world_size)");
+        return CFR_ERR_INVALID_ARG;
+    }
+    if (it == G->shards.end()) {
+        auto sh = std::make_shared<cfr_game::Shard>();
+        std::string err;
+        if (!build_shard(G->g, rank, world, sh->local, sh->info, err)) {
+            cfrb_set_error("shard: " + err);
+            return CFR_ERR_INVALID_TREE;
+        }
+        it = G->shards.emplace(key, sh).first;
+    }
+    *local = &it->second->local;
+    *info = &it->second->info;
+    *keep = it->second;
     return CFR_OK;
+}
+
+static size_t bytes_for(const Game& g, const ShardInfo* sh, int precision) {
+    const bool i32 = use_idx32(g);
+    if (precision == 64) return i32 ? Plan<double, int>(g, sh).total : Plan<double, long long>(g, sh).total;
+    return i32 ? Plan<float, int>(g, sh).total : Plan<float, long long>(g, sh).total;
 }
 
 }  // namespace cfrb
@@ -1252,6 +1642,7 @@ using namespace cfrb;
 
 struct cfr_solver {
     std::unique_ptr<SolverBase> impl;
+    std::shared_ptr<cfr_game::Shard> keep;   // shard view the solver iterates
 };
 
 extern "C" {
@@ -1260,8 +1651,13 @@ cfr_status cfr_solver_workspace_bytes(const cfr_game* g, const cfr_solver_config
                                       size_t* bytes) {
     if (!g || !cfg || !bytes) { cfrb_set_error("NULL argument"); return CFR_ERR_INVALID_ARG; }
     if (cfg->precision != 64 && cfg->precision != 32) { cfrb_set_error("precision must be 64 or 32"); return CFR_ERR_INVALID_ARG; }
-    if (dist && dist->world_size > 1) { cfrb_set_error("multi-GPU sharding not built in this version"); return CFR_ERR_UNSUPPORTED; }
-    return bytes_for(g->g, cfg->precision, bytes);
+    const Game* local = nullptr;
+    const ShardInfo* info = nullptr;
+    std::shared_ptr<cfr_game::Shard> keep;
+    cfr_status s = view_for(const_cast<cfr_game*>(g), dist, &local, &info, &keep);
+    if (s) return s;
+    *bytes = bytes_for(*local, info, cfg->precision);
+    return CFR_OK;
 }
 
 cfr_status cfr_solver_create(const cfr_game* g, const cfr_solver_config* cfg, void* workspace, size_t workspace_bytes,
@@ -1270,27 +1666,30 @@ cfr_status cfr_solver_create(const cfr_game* g, const cfr_solver_config* cfg, vo
     *out = nullptr;
     if (cfg->variant != CFR_VANILLA && cfg->variant != CFR_PLUS) { cfrb_set_error("bad variant"); return CFR_ERR_INVALID_ARG; }
     if (cfg->precision != 64 && cfg->precision != 32) { cfrb_set_error("precision must be 64 or 32"); return CFR_ERR_INVALID_ARG; }
-    if (dist && dist->world_size > 1) { cfrb_set_error("multi-GPU sharding not built in this version"); return CFR_ERR_UNSUPPORTED; }
-    size_t need = 0;
-    bytes_for(g->g, cfg->precision, &need);
+    const Game* local = nullptr;
+    const ShardInfo* info = nullptr;
+    std::shared_ptr<cfr_game::Shard> keep;
+    cfr_status s = view_for(const_cast<cfr_game*>(g), dist, &local, &info, &keep);
+    if (s) return s;
+    const size_t need = bytes_for(*local, info, cfg->precision);
     if (workspace_bytes < need) {
         cfrb_set_error("workspace too small: need " + std::to_string(need) + " bytes");
         return CFR_ERR_OOM;
     }
     if (((uintptr_t)workspace & 255) != 0) { cfrb_set_error("workspace must be 256-byte aligned"); return CFR_ERR_INVALID_ARG; }
-    const bool i32 = use_idx32(g->g);
+    const bool i32 = use_idx32(*local);
     std::unique_ptr<SolverBase> impl;
     cudaStream_t st = (cudaStream_t)stream;
-    cfr_status s;
+    const void* nid = (dist && dist->world_size > 1) ? dist->nccl_unique_id : nullptr;
     if (cfg->precision == 64) {
-        if (i32) { auto p = new Solver<double, int>(&g->g, *cfg, workspace, st); impl.reset(p); s = p->init(); }
-        else { auto p = new Solver<double, long long>(&g->g, *cfg, workspace, st); impl.reset(p); s = p->init(); }
+        if (i32) { auto p = new Solver<double, int>(local, &g->g, info, *cfg, workspace, st); impl.reset(p); s = p->init(nid); }
+        else { auto p = new Solver<double, long long>(local, &g->g, info, *cfg, workspace, st); impl.reset(p); s = p->init(nid); }
     } else {
-        if (i32) { auto p = new Solver<float, int>(&g->g, *cfg, workspace, st); impl.reset(p); s = p->init(); }
-        else { auto p = new Solver<float, long long>(&g->g, *cfg, workspace, st); impl.reset(p); s = p->init(); }
+        if (i32) { auto p = new Solver<float, int>(local, &g->g, info, *cfg, workspace, st); impl.reset(p); s = p->init(nid); }
+        else { auto p = new Solver<float, long long>(local, &g->g, info, *cfg, workspace, st); impl.reset(p); s = p->init(nid); }
     }
     if (s != CFR_OK) return s;
-    *out = new cfr_solver{std::move(impl)};
+    *out = new cfr_solver{std::move(impl), keep};
     return CFR_OK;
 }
 
@@ -1359,9 +1758,57 @@ cfr_status cfr_solver_model_bytes(cfr_solver* s, double* out) {
     return s->impl->model_bytes(out);
 }
 cfr_status cfr_nccl_unique_id(void* out) {
-    (void)out;
-    cfrb_set_error("multi-GPU sharding not built in this version");
-    return CFR_ERR_UNSUPPORTED;
+    if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        cfrb_set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+        return CFR_ERR_NCCL;
+    }
+    std::memcpy(out, &id, sizeof(id));
+    return CFR_OK;
+}
+cfr_status cfr_game_shard_info(const cfr_game* g, int32_t rank, int32_t world, int64_t* out) {
+    if (!g || !out) { cfrb_set_error("NULL argument"); return CFR_ERR_INVALID_ARG; }
+    cfr_dist d{rank, world, nullptr};
+    const Game* local = nullptr;
+    const ShardInfo* info = nullptr;
+    std::shared_ptr<cfr_game::Shard> keep;
+    cfr_status s = view_for(const_cast<cfr_game*>(g), &d, &local, &info, &keep);
+    if (s) return s;
+    out[0] = info->cut;
+    out[1] = (int64_t)info->cut_row.size();
+    out[2] = info->owned_nodes;
+    out[3] = local->V;
+    out[4] = local->NS;
+    out[5] = (int64_t)local->deferred_list.size();
+    out[6] = local->dqbase.empty() ? 0 : local->dqbase.back();
+    out[7] = world;
+    int64_t owned_cut = 0, reported = 0;
+    for (auto o : info->cut_owned) owned_cut += o;
+    for (auto r : info->report) reported += r;
+    out[8] = owned_cut;
+    out[9] = world > 1 ? reported : g->g.H;
+    return CFR_OK;
+}
+cfr_status cfr_solver_phase(cfr_solver* s, int32_t phase, double* out) {
+    CHK_S(s);
+    return s->impl->phase(phase, out);
+}
+cfr_status cfr_solver_exchange_size(cfr_solver* s, int32_t which, size_t* bytes) {
+    CHK_S(s);
+    if (!bytes) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->exchange_size(which, bytes);
+}
+cfr_status cfr_solver_exchange(cfr_solver* s, int32_t which, int32_t put, void* host, size_t bytes) {
+    CHK_S(s);
+    if (!host && bytes) { cfrb_set_error("NULL buffer"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->exchange(which, put, host, bytes);
+}
+cfr_status cfr_solver_shard_info(cfr_solver* s, int64_t* out) {
+    CHK_S(s);
+    if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->shard_info(out);
 }
 
 }  // extern "C"

@@ -1,0 +1,95 @@
+"""Level-sharded multi-GPU path on ONE GPU: `world` solver ranks in
+one process, the two per-iteration exchanges done here with exact host sums
+(the NCCL mode performs the same sums with ncclAllReduce inside the graph).
+Results must be bit-identical to the oracle for every world size."""
+import numpy as np
+import pytest
+
+import gamegen
+import oracle
+import paper_2408_14778_b200 as pb
+from tests.parity import assert_same
+
+pytestmark = pytest.mark.gpu
+
+
+def run_world(desc, variant, precision, T, world, shard_prefix=None):
+    g = pb.Game(desc)
+    games = [g] * world
+    if shard_prefix is not None:      # ranks load their own view from shard files
+        g.save_shards(world, shard_prefix)
+        games = [pb.Game.load_shard(shard_prefix, r, world) for r in range(world)]
+    ss = [pb.Solver(games[r], variant="cfr+" if variant else "cfr", precision=precision, rank=r, world_size=world)
+          for r in range(world)]
+
+    def allreduce(which):
+        bufs = [s.exchange_get(which) for s in ss]
+        tot = bufs[0].copy()
+        for b in bufs[1:]:
+            tot = tot + b          # int64 (exact) or values with one nonzero contribution (exact)
+        for s in ss:
+            s.exchange_put(which, tot)
+
+    for _ in range(T):
+        for s in ss:
+            s.phase(pb.Solver.PHASE_LOWER)
+        allreduce(pb.Solver.XCHG_CUT)
+        for s in ss:
+            s.phase(pb.Solver.PHASE_UPPER)
+        allreduce(pb.Solver.XCHG_ACC)
+        for s in ss:
+            s.phase(pb.Solver.PHASE_UPDATE)
+    for s in ss:
+        assert s.iteration == T
+    # readbacks: every rank returns the infosets it reports, zeros elsewhere
+    avg = sum(s.average_strategy() for s in ss)
+    cur = sum(s.current_strategy() for s in ss)
+    st = [s.state() for s in ss]
+    reg = sum(x["regret"] for x in st)
+    sden = sum(x["sden"] for x in st)
+    # EV under sigma_bar through the sharded values pass
+    for s in ss:
+        s.phase(pb.Solver.PHASE_EV_LOWER)
+    allreduce(pb.Solver.XCHG_CUT)
+    evs = [s.phase(pb.Solver.PHASE_EV_UPPER) for s in ss]
+    return dict(avg=avg, cur=cur, regret=reg, sden=sden, ev=evs, info=[s.shard_info() for s in ss])
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+@pytest.mark.parametrize("name,variant,precision,T", [("leduc", 1, 64, 30), ("leduc", 0, 32, 30),
+                                                       ("goofspiel", 1, 64, 10), ("kuhn3", 0, 64, 20)])
+def test_sharded_bit_identical_to_oracle(cuda, name, variant, precision, T, world):
+    desc = gamegen.by_name(name)
+    o = oracle.Oracle(desc, precision=precision).run(T, variant)
+    r = run_world(desc, variant, precision, T, world)
+    os_ = o.state()
+    assert_same("average strategy", r["avg"], os_["avg"], precision)
+    assert_same("current strategy", r["cur"], os_["sigma"], precision)
+    assert_same("regret", r["regret"], os_["regret"], precision)
+    assert_same("S_den", r["sden"], os_["sden"], precision)
+    for ev in r["ev"]:
+        assert_same("EV(avg)", ev, o.expected_values(), precision)
+    if name != "kuhn3":
+        assert r["info"][0]["cut"] >= 1
+
+
+def test_sharded_liars_dice_and_random(cuda):
+    desc = gamegen.liars_dice()
+    o = oracle.Oracle(desc).run(3, 1)
+    r = run_world(desc, 1, 64, 3, 4)
+    assert_same("average strategy", r["avg"], o.state()["avg"], 64)
+    for seed in range(6):
+        d = gamegen.random_game(seed, num_players=2 + seed % 2, max_depth=7, max_nodes=6000)
+        o = oracle.Oracle(d).run(8, seed % 2)
+        r = run_world(d, seed % 2, 64, 8, 2 + seed % 3)
+        assert_same("avg", r["avg"], o.state()["avg"], 64)
+        assert_same("regret", r["regret"], o.state()["regret"], 64)
+
+
+def test_sharded_from_shard_files(cuda, tmp_path):
+    desc = gamegen.goofspiel()
+    o = oracle.Oracle(desc).run(6, 1)
+    r = run_world(desc, 1, 64, 6, 3, shard_prefix=str(tmp_path / "g"))
+    assert_same("average strategy", r["avg"], o.state()["avg"], 64)
+    for ev in r["ev"]:
+        assert_same("EV(avg)", ev, o.expected_values(), 64)

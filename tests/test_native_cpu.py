@@ -158,3 +158,21 @@ def test_solver_refuses_without_gpu():
     g = pb.Game(gamegen.kuhn(2))
     with pytest.raises(RuntimeError, match="CUDA"):
         pb.Solver(g)
+
+
+def test_shard_files_roundtrip(tmp_path):
+    """DESIGN.md §9 shard files: one writer, each rank loads its own view."""
+    g = pb.Game(gamegen.goofspiel())
+    prefix = str(tmp_path / "goof")
+    g.save_shards(4, prefix)
+    for r in range(4):
+        h = pb.Game.load_shard(prefix, r, 4)
+        assert (h.V, h.H, h.Q, h.D) == (g.V, g.H, g.Q, g.D)
+        assert np.array_equal(h.qbase(), g.qbase())
+        assert h.shard_info(r, 4) == g.shard_info(r, 4)
+        with pytest.raises(pb.NativeError):
+            h.shard_info((r + 1) % 4, 4)
+        with pytest.raises(pb.NativeError):
+            h.canonical()
+    with pytest.raises(pb.NativeError):
+        pb.Game.load_shard(str(tmp_path / "missing"), 0, 4)
