@@ -114,12 +114,14 @@ typedef struct {
     int32_t variant;     /* cfr_variant: CFR (w_t = 1) or CFR+ (RM+, w_t = t)      */
     int32_t precision;   /* 64 (binary64) or 32 (binary32) working precision      */
     int32_t flags;       /* bit 0: disable CUDA-Graph capture (debug);            */
-                         /* bit 1: force the multi-CTA level path for tiny games  */
+                         /* bit 1: reserved; bit 2: disable the pipelined         */
+                         /* (persistent) backward kernel (A/B comparisons)        */
     int32_t reserved;
 } cfr_solver_config;
 
 #define CFR_FLAG_NO_GRAPH 1
 #define CFR_FLAG_NO_PERSISTENT 2
+#define CFR_FLAG_NO_PIPELINE 4
 
 /* Multi-GPU level sharding.  NULL or world_size == 1 means a
  * single GPU.  nccl_unique_id points to the 128-byte ncclUniqueId that rank 0

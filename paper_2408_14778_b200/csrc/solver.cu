@@ -528,6 +528,316 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
     }
 }
 
+// ------------------------------------------------- pipelined backward pass
+// Persistent variant of k_bwd (MODE_CFR) for levels whose tiles are all "fast":
+// uniform child rows staged in 16/8-byte chunks, every infoset complete in its
+// tile (fused update), no chance nodes.  Each CTA walks tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ... with a three-stage cp.async pipeline: while tile i
+// is computed, the data of tile i+1 and the metadata record of tile i+2 are in
+// flight, so the global-memory latency of one tile hides behind another's work.
+// The arithmetic is the same as k_bwd's (same order of every FP operation).
+struct FastHdr {
+    long long s0;    // first slot
+    int nslot, nseg, npairs, pad;
+};
+struct FastSeg {
+    long long h, qb;
+    int pair_off, n, owner, sb, se, pad;
+};
+struct FastLevel {
+    long long tile0, ntiles;   // tiles of the level
+    long long rec;             // byte offset of the level's records in the record pool
+    int recsize;               // bytes per record (16-byte multiple)
+    int maxslot, maxseg, maxpairs, maxch;
+    int rowlen, cpr, stride;   // uniform child rows
+    float inv_cpr;
+    int last;                  // 1: this launch ends the iteration
+    int pad;
+};
+
+// Shared-memory plan of k_bwd_fast: 3 metadata records, 2 data buffers (each
+// holding ch | ssig | sreg | ssn | spc | sph | sden), then per-tile work arrays.
+// Buffers are addressed as base + index * stride (no dynamically indexed
+// pointer arrays, which would live in local memory).
+struct FastPlan {
+    int meta, mstride;        // meta record k at meta + k * mstride
+    int data, dstride;        // data buffer k at data + k * dstride
+    int o_ssig, o_sreg, o_ssn, o_spc, o_sph, o_sden;   // offsets inside a data buffer
+    int sv, pib, zs, spoff, pseg;
+    int bytes;
+};
+__host__ __device__ inline FastPlan fast_plan(const FastLevel& L, int Pc, int w) {
+    FastPlan f;
+    auto al = [](int x) { return (x + 15) & ~15; };
+    const int pairs_b = al(L.maxpairs * w);
+    f.meta = 0;
+    f.mstride = al(L.recsize);
+    f.data = 3 * f.mstride;
+    int o = al(L.maxch * w > 2 * pairs_b ? L.maxch * w : 2 * pairs_b);
+    f.o_ssig = o; o += pairs_b;
+    f.o_sreg = o; o += pairs_b;
+    f.o_ssn = o; o += pairs_b;
+    f.o_spc = o; o += al(L.maxslot * w);
+    f.o_sph = o; o += al(L.maxslot * w);
+    f.o_sden = o; o += al(L.maxseg * w);
+    f.dstride = o;
+    int x = f.data + 2 * f.dstride;
+    f.sv = x; x += al(L.maxslot * Pc * w);
+    f.pib = x; x += al(L.maxseg * w);
+    f.zs = x; x += al(L.maxseg * w);
+    f.spoff = x; x += al(L.maxslot * 4);
+    f.pseg = x; x += al(L.maxpairs);
+    f.bytes = x;
+    return f;
+}
+
+// t = tile index within the level (records are level-local)
+template <class R, class I, int PC>
+__device__ __forceinline__ void fast_issue_meta(const unsigned char* __restrict__ pool, const FastLevel& L, long long t,
+                                                unsigned char* dst) {
+    const unsigned char* src = pool + L.rec + t * (long long)L.recsize;
+    for (int c = threadIdx.x; c < L.recsize / 16; c += blockDim.x) cp_async<16>(dst + c * 16, src + c * 16);
+}
+
+template <class R, class I, int PC>
+__device__ __forceinline__ void fast_issue_data(const DG<R, I>& g, const FastLevel& L, const unsigned char* meta,
+                                                R* ch, R* ssig, R* sreg, R* ssn, R* spc, R* sph, R* sden) {
+    constexpr int CH = (sizeof(R) == 8) ? 16 : 8;
+    constexpr int CE = CH / (int)sizeof(R);
+    const FastHdr& hd = *reinterpret_cast<const FastHdr*>(meta);
+    const FastSeg* seg = reinterpret_cast<const FastSeg*>(meta + 32);
+    const I* node = reinterpret_cast<const I*>(meta + 32 + hd.nseg * (int)sizeof(FastSeg));
+    const I* cb = node + hd.nslot;
+    const I* dec = cb + hd.nslot;
+    (void)node;
+    const int P = g.P;
+    const int tot = hd.nslot * L.cpr;
+    for (int c = threadIdx.x; c < tot; c += blockDim.x) {
+        const int row = __float2int_rd(((float)c + 0.5f) * L.inv_cpr);
+        const int k = c - row * L.cpr;
+        cp_async<CH>(ch + row * L.stride + k * CE, g.U + (long long)cb[row] * PC + k * CE);
+    }
+    for (int s = threadIdx.x; s < hd.nslot; s += blockDim.x) {
+        int k = 0;
+        while (k + 1 < hd.nseg && seg[k + 1].sb <= s) ++k;
+        const long long d = (long long)dec[s];
+        const int i = seg[k].owner;
+        cp_async<(int)sizeof(R)>(spc + s, g.reach + d * 2 * P + (i - 1));
+        cp_async<(int)sizeof(R)>(sph + s, g.reach + d * 2 * P + P + (i - 1));
+    }
+    for (int p = threadIdx.x; p < hd.npairs; p += blockDim.x) {
+        int k = 0;
+        while (k + 1 < hd.nseg && seg[k + 1].pair_off <= p) ++k;
+        const long long q = seg[k].qb + (p - seg[k].pair_off);
+        cp_async<(int)sizeof(R)>(ssig + p, g.sig + q);
+        cp_async<(int)sizeof(R)>(sreg + p, g.regret + q);
+        cp_async<(int)sizeof(R)>(ssn + p, g.snum + q);
+    }
+    for (int k = threadIdx.x; k < hd.nseg; k += blockDim.x) cp_async<(int)sizeof(R)>(sden + k, g.sden + seg[k].h);
+    asm volatile("cp.async.commit_group;\n" ::);
+}
+
+template <class R, class I, int PC>
+__global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsigned char* __restrict__ pool,
+                                                         FastLevel L) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const FastPlan F = fast_plan(L, PC, (int)sizeof(R));
+    unsigned char* const B = smem_raw;
+    auto META = [&](int k) { return B + F.meta + k * F.mstride; };
+    auto DATA = [&](int k) { return B + F.data + k * F.dstride; };
+    R* const sv_ = (R*)(B + F.sv);
+    R* const pib_ = (R*)(B + F.pib);
+    R* const zs_ = (R*)(B + F.zs);
+    int* const spoff_ = (int*)(B + F.spoff);
+    unsigned char* const pseg_ = B + F.pseg;
+    auto ISSUE = [&](int mk, int dk) {
+        unsigned char* d = DATA(dk);
+        fast_issue_data<R, I, PC>(g, L, META(mk), (R*)d, (R*)(d + F.o_ssig), (R*)(d + F.o_sreg), (R*)(d + F.o_ssn),
+                                  (R*)(d + F.o_spc), (R*)(d + F.o_sph), (R*)(d + F.o_sden));
+    };
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const long long t_iter = g.ctrl[0] + 1;
+    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
+    long long t = blockIdx.x;
+    if (t >= L.ntiles) return;
+    // prologue: meta(t) -> data(t), meta(t + G)
+    fast_issue_meta<R, I, PC>(pool, L, t, META(0));
+    asm volatile("cp.async.commit_group;\n" ::);
+    cp_async_wait_all();
+    __syncthreads();
+    ISSUE(0, 0);
+    if (t + gridDim.x < L.ntiles) fast_issue_meta<R, I, PC>(pool, L, t + gridDim.x, META(1));
+    asm volatile("cp.async.commit_group;\n" ::);
+    bool bad = false;
+    for (int it = 0;; ++it) {
+        const int mb = it % 3, db = it & 1;
+        const long long tn = t + gridDim.x, tnn = t + 2 * (long long)gridDim.x;
+        cp_async_wait_all();      // data(t) and meta(tn) have landed
+        __syncthreads();
+        if (tn < L.ntiles) {
+            ISSUE((it + 1) % 3, db ^ 1);
+            if (tnn < L.ntiles) fast_issue_meta<R, I, PC>(pool, L, tnn, META((it + 2) % 3));
+            asm volatile("cp.async.commit_group;\n" ::);
+        }
+        // ---- compute tile t
+        const unsigned char* meta = META(mb);
+        const FastHdr hd = *reinterpret_cast<const FastHdr*>(meta);
+        const FastSeg* seg = reinterpret_cast<const FastSeg*>(meta + 32);
+        const I* node = reinterpret_cast<const I*>(meta + 32 + hd.nseg * (int)sizeof(FastSeg));
+        unsigned char* dbuf = DATA(db);
+        R* ch = (R*)dbuf;
+        const R* ssig = (const R*)(dbuf + F.o_ssig);
+        const R* sreg = (const R*)(dbuf + F.o_sreg);
+        const R* ssn = (const R*)(dbuf + F.o_ssn);
+        const R* spc = (const R*)(dbuf + F.o_spc);
+        const R* sph = (const R*)(dbuf + F.o_sph);
+        const R* sden = (const R*)(dbuf + F.o_sden);
+        const int nslot = hd.nslot, nseg = hd.nseg, npairs = hd.npairs;
+        for (int p = tid; p < npairs; p += nth) {
+            int k = 0;
+            while (k + 1 < nseg && seg[k + 1].pair_off <= p) ++k;
+            pseg_[p] = (unsigned char)k;
+        }
+        for (int s = tid; s < nslot; s += nth) {
+            int k = 0;
+            while (k + 1 < nseg && seg[k + 1].sb <= s) ++k;
+            spoff_[s] = seg[k].pair_off;
+        }
+        __syncthreads();
+        // phase A: node values (Eq 1), ascending actions from +0
+        if (tid < nslot) {
+            R v[PC];
+#pragma unroll
+            for (int j = 0; j < PC; ++j) v[j] = (R)0;
+            const R* row = ch + tid * L.stride;
+            const R* sg = ssig + spoff_[tid];
+            const int n = L.rowlen / PC;
+            for (int a = 0; a < n; ++a) {
+                const R x = sg[a];
+#pragma unroll
+                for (int j = 0; j < PC; ++j) v[j] = v[j] + x * row[a * PC + j];
+            }
+            const long long nd = (long long)node[tid];
+#pragma unroll
+            for (int j = 0; j < PC; ++j) {
+                g.U[nd * PC + j] = v[j];
+                sv_[tid * PC + j] = v[j];
+            }
+        }
+        __syncthreads();
+        // phase B: exact sums (pairs, then one pi_bar item per segment)
+        const int nitems = npairs + nseg;
+        int ns = 1;
+        while (ns < 8 && nitems * ns * 2 <= nth) ns <<= 1;
+        const int rounds = (nitems * ns + nth - 1) / nth;
+        double kr0 = 0, kr1 = 0, kr2 = 0, kr3 = 0, kr4 = 0;
+        for (int rd = 0; rd < rounds; ++rd) {
+            const int wi = rd * nth + tid;
+            const int itm = wi / ns, part = wi - itm * ns;
+            double c0 = 0, c1 = 0, c2 = 0;
+            bool is_pair = false, neg = false;
+            int k = 0, a = 0;
+            if (itm < npairs) {
+                k = pseg_[itm];
+                a = itm - seg[k].pair_off;
+                is_pair = true;
+                neg = (PC == 1) && (seg[k].owner == 2);
+            } else if (itm < nitems) {
+                k = itm - npairs;
+            }
+            if (itm < nitems) {
+                const int col = (PC == 1) ? 0 : seg[k].owner - 1;
+                const int sb = seg[k].sb, se = seg[k].se;
+                if (!is_pair) {
+                    for (int ls = sb + part; ls < se; ls += ns) xadd(c0, c1, c2, (double)sph[ls], g.scp0);
+                } else {
+                    for (int ls = sb + part; ls < se; ls += ns) {
+                        const R uc = ch[ls * L.stride + a * PC + col];
+                        const R tt = spc[ls] * (uc - sv_[ls * PC + col]);
+                        xadd(c0, c1, c2, (double)tt, g.sc0);
+                    }
+                }
+                if (neg) { c0 = -c0; c1 = -c1; c2 = -c2; }
+            }
+            for (int o = 1; o < ns; o <<= 1) {
+                c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+                c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+                c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+            }
+            if (itm < nitems && part == 0) {
+                const double x = is_pair ? xdec(c0, c1, c2, g.rc) : xdec(c0, c1, c2, g.rcp);
+                if (rd == 0) kr0 = x;
+                else if (rd == 1) kr1 = x;
+                else if (rd == 2) kr2 = x;
+                else if (rd == 3) kr3 = x;
+                else kr4 = x;
+            }
+        }
+        __syncthreads();   // reads of ch done: rt / pos alias it
+        R* rt = ch;
+        R* pos = ch + (((npairs * (int)sizeof(R) + 15) & ~15) / (int)sizeof(R));
+        for (int rd = 0; rd < rounds && rd < 5; ++rd) {
+            const int wi = rd * nth + tid;
+            const int itm = wi / ns, part = wi - itm * ns;
+            if (itm < nitems && part == 0) {
+                const double x = rd == 0 ? kr0 : rd == 1 ? kr1 : rd == 2 ? kr2 : rd == 3 ? kr3 : kr4;
+                if (itm < npairs) rt[itm] = (R)x;
+                else pib_[itm - npairs] = (R)x;
+            }
+        }
+        __syncthreads();
+        // phase C: fused update (Eq 8/15 or CFR+, Eq 10, Eq 9)
+        for (int p = tid; p < npairs; p += nth) {
+            const int k = pseg_[p];
+            const long long q = seg[k].qb + (p - seg[k].pair_off);
+            const R r_t = rt[p];
+            R r;
+            if (g.variant == 0) {
+                r = sreg[p] + r_t;
+            } else {
+                const R x = sreg[p] + r_t;
+                r = (x > (R)0) ? x : (R)0;
+                if (!finite_(x)) r = x;
+            }
+            g.regret[q] = r;
+            const R wp = w * pib_[k];
+            g.snum[q] = ssn[p] + wp * ssig[p];
+            pos[p] = (r > (R)0) ? r : (R)0;
+        }
+        __syncthreads();
+        for (int k = tid; k < nseg; k += nth) {
+            g.sden[seg[k].h] = sden[k] + w * pib_[k];
+            R z = (R)0;
+            for (int p = seg[k].pair_off; p < seg[k].pair_off + seg[k].n; ++p) z = z + pos[p];
+            zs_[k] = z;
+        }
+        __syncthreads();
+        for (int p = tid; p < npairs; p += nth) {
+            const int k = pseg_[p];
+            const int a = p - seg[k].pair_off;
+            const R z = zs_[k];
+            const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)seg[k].n;
+            g.sig[seg[k].qb + a] = nsig;
+            if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
+        }
+        __syncthreads();   // buffers of tile t may be refilled from here on
+        t = tn;
+        if (t >= L.ntiles) break;
+    }
+    if (bad) atomicMin(&g.ctrl[1], t_iter);
+    if (L.last) {
+        // last-block-done: the iteration counter advances once every CTA is done
+        if (tid == 0) {
+            __threadfence();
+            const unsigned long long prev = atomicAdd((unsigned long long*)&g.ctrl[2], 1ULL);
+            if (prev == gridDim.x - 1) {
+                g.ctrl[0] = t_iter;
+                g.ctrl[2] = 0;
+            }
+        }
+    }
+}
+
 // Update of deferred infosets (span several depths / tiles): decode the global
 // exact sums, then the same Eq 8/15, Eq 10, Eq 9 steps; zero the accumulators.
 template <class R, class I>
@@ -692,13 +1002,133 @@ static std::vector<int64_t> u_layout(const Game& g, size_t elem) {
     return off;
 }
 
+// U rows of the slots' nodes and first children (u_layout offsets).
+static void u_rows(const Game& g, const std::vector<int64_t>& uoff, std::vector<int64_t>& node_u,
+                   std::vector<int64_t>& cb_u) {
+    node_u.resize(g.NS);
+    cb_u.resize(g.NS);
+    for (int L = 0; L < g.D; ++L)
+        for (int64_t s = g.slot_ptr[L]; s < g.slot_ptr[L + 1]; ++s) {
+            node_u[s] = uoff[L] + (g.s_node[s] - g.level_ptr[L]);
+            cb_u[s] = uoff[L + 1] + (g.s_cb[s] - g.level_ptr[L + 1]);
+        }
+}
+
+// Staging layout per tile (precision dependent): uniform rows whose starts and
+// lengths are multiples of the cp.async chunk use chunked copies with an odd
+// number of chunks per row stride (<= 2-way bank conflicts); others fall back to
+// generic rows (odd element strides) or, if too large, to global reads.
+template <class R>
+static void stage_tiles(const Game& g, const std::vector<int64_t>& cb_u, const std::vector<uint8_t>& contrib,
+                        std::vector<TileD>& tiles, std::vector<int32_t>& s_coff) {
+    const int CH = (sizeof(R) == 8) ? 16 : 8;
+    const int CE = CH / (int)sizeof(R);
+    s_coff = g.s_coff;
+    tiles.assign(g.tiles.size(), TileD{});
+    for (size_t t = 0; t < g.tiles.size(); ++t) {
+        const TileH& th = g.tiles[t];
+        TileD td{};
+        td.s0 = th.s0;
+        td.s1 = th.s1;
+        td.seg0 = th.seg0;
+        td.seg1 = th.seg1;
+        td.npairs = th.npairs;
+        td.staged = th.staged ? 2 : 0;
+        td.contrib = contrib.empty() ? 1 : (int)contrib[t];
+        if (th.staged) {
+            const int rowlen = g.s_n[th.s0] * g.Pc;
+            bool uni = (rowlen % CE) == 0;
+            for (int64_t s = th.s0; s < th.s1 && uni; ++s)
+                uni = (g.s_n[s] * g.Pc == rowlen) && ((cb_u[s] * g.Pc) % CE == 0);
+            if (uni) {
+                const int cpr = rowlen / CE;
+                const int cstride = (cpr % 2 == 0) ? cpr + 1 : cpr;
+                const int64_t need = (int64_t)(th.s1 - th.s0) * cstride * CE;
+                if (need <= kTileChildren) {
+                    td.staged = 1;
+                    td.rowlen = rowlen;
+                    td.cpr = cpr;
+                    td.stride = cstride * CE;
+                    td.inv_cpr = 1.0f / (float)cpr;
+                    for (int64_t s = th.s0; s < th.s1; ++s) s_coff[s] = (int32_t)((s - th.s0) * td.stride);
+                }
+            }
+        }
+        tiles[t] = td;
+    }
+}
+
+// Levels served by the pipelined k_bwd_fast: every tile chunk-staged, fused,
+// player-only, one row length across the level, and enough tiles to pipeline.
+template <class R, class I>
+static std::vector<FastLevel> fast_levels(const Game& g, const std::vector<TileD>& tiles, size_t* pool_bytes) {
+    std::vector<FastLevel> out(g.D, FastLevel{});
+    size_t pool = 0;
+    for (int L = 0; L < g.D; ++L) {
+        FastLevel f{};
+        f.tile0 = g.tile_ptr[L];
+        f.ntiles = g.tile_ptr[L + 1] - g.tile_ptr[L];
+        f.recsize = 0;
+        bool ok = f.ntiles >= 2 * 148;
+        int rowlen = -1, maxslot = 1, maxseg = 1, maxpairs = 1, maxch = 0;
+        for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1] && ok; ++t) {
+            const TileD& td = tiles[t];
+            if (td.staged != 1 || td.npairs > kTilePairs) { ok = false; break; }
+            if (rowlen < 0) rowlen = td.rowlen;
+            if (td.rowlen != rowlen) { ok = false; break; }
+            int64_t members = 0;
+            for (int k = td.seg0; k < td.seg1; ++k) {
+                if (!g.segs[k].fused) ok = false;
+                members += g.segs[k].se - g.segs[k].sb;
+            }
+            if (members != td.s1 - td.s0) ok = false;   // a chance slot
+            const int nslot = (int)(td.s1 - td.s0);
+            maxslot = std::max(maxslot, nslot);
+            maxseg = std::max(maxseg, td.seg1 - td.seg0);
+            maxpairs = std::max(maxpairs, td.npairs);
+            maxch = std::max(maxch, nslot * td.stride);
+        }
+        if (ok && f.ntiles > 0) {
+            const TileD& t0 = tiles[g.tile_ptr[L]];
+            f.maxslot = maxslot;
+            f.maxseg = maxseg;
+            f.maxpairs = maxpairs;
+            f.maxch = maxch;
+            f.rowlen = t0.rowlen;
+            f.cpr = t0.cpr;
+            f.stride = t0.stride;
+            f.inv_cpr = t0.inv_cpr;
+            f.recsize = (int)((32 + (int64_t)maxseg * sizeof(FastSeg) + 3 * sizeof(I) * (int64_t)maxslot + 15) & ~int64_t(15));
+            f.rec = (long long)pool;
+            pool += (size_t)f.recsize * (size_t)f.ntiles;
+        }
+        out[L] = f;
+    }
+    *pool_bytes = pool;
+    return out;
+}
+
+template <class R, class I>
+static size_t fast_pool_bytes(const Game& g, const ShardInfo* sh) {
+    const std::vector<int64_t> uoff = u_layout(g, sizeof(R));
+    std::vector<int64_t> nu, cu;
+    u_rows(g, uoff, nu, cu);
+    std::vector<TileD> tiles;
+    std::vector<int32_t> coff;
+    static const std::vector<uint8_t> none;
+    stage_tiles<R>(g, cu, sh ? sh->tile_contrib : none, tiles, coff);
+    size_t pool = 0;
+    fast_levels<R, I>(g, tiles, &pool);
+    return pool;
+}
+
 template <class R, class I>
 struct Plan {
     size_t U, reach, sig, sig_eval, regret, snum, sden, acc_r, acc_p, dqbase;
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, ctrl, out;
-    size_t cutbuf, cutrow, cutown, report;
+    size_t cutbuf, cutrow, cutown, report, pool;
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
         Layout L;
@@ -736,6 +1166,7 @@ struct Plan {
         cutrow = L.take<long long>(ncut + 1);
         cutown = L.take<unsigned char>(ncut + 1);
         report = L.take<unsigned char>(H + 1);
+        pool = L.take<unsigned char>(fast_pool_bytes<R, I>(g, sh) + 16);
         total = L.off + 256;
     }
 };
@@ -762,6 +1193,8 @@ struct Solver final : SolverBase {
     int E = 1;
     int64_t launches_per_iter = 0;
     bool use_graph = true;
+    bool use_fast_ = true;
+    int num_sms_ = 148;
     int world = 1, rank = 0;
     bool external = false;        // world > 1 without NCCL: the caller runs the exchanges
     ncclComm_t comm = nullptr;
@@ -797,6 +1230,7 @@ struct Solver final : SolverBase {
     int contrib_of_tile(size_t t) const { return tile_contrib_.empty() ? 1 : (int)tile_contrib_[t]; }
     std::vector<SmemLayout> lay_;   // per parent level
     int max_smem_ = 0;
+    std::vector<FastLevel> fast_;   // per parent level: recsize > 0 -> pipelined kernel
 
     SmemLayout make_layout(int maxch, int maxslot, int maxpairs, int maxseg) const {
         const int Pc = gp->Pc;
@@ -876,6 +1310,12 @@ struct Solver final : SolverBase {
             return CFR_ERR_UNSUPPORTED;
         }
         use_graph = !(cfg.flags & CFR_FLAG_NO_GRAPH);
+        use_fast_ = !(cfg.flags & CFR_FLAG_NO_PIPELINE);
+        {
+            int dev = 0;
+            CU(cudaGetDevice(&dev));
+            CU(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, dev));
+        }
         // exact-accumulation exponent from the utilities in working precision
         double m = 0.0;
         for (double u : g.util_c) m = std::max(m, std::fabs((double)(R)u));
@@ -927,51 +1367,48 @@ struct Solver final : SolverBase {
                         u[(size_t)(uoff[l] + k - g.level_ptr[l]) * g.Pc + j] = (R)g.util_c[(size_t)k * g.Pc + j];
             if ((st = up(plan.U, u))) return st;
         }
-        std::vector<int64_t> s_node_u(g.NS), s_cb_u(g.NS);
-        for (int L = 0; L < g.D; ++L)
-            for (int64_t s = g.slot_ptr[L]; s < g.slot_ptr[L + 1]; ++s) {
-                s_node_u[s] = uoff[L] + (g.s_node[s] - g.level_ptr[L]);
-                s_cb_u[s] = uoff[L + 1] + (g.s_cb[s] - g.level_ptr[L + 1]);
-            }
-        // ---- staging layout per tile (precision dependent): uniform rows whose
-        // starts and lengths are multiples of the cp.async chunk use chunked copies
-        // with an odd number of chunks per row stride (<= 2-way bank conflicts)
-        std::vector<int32_t> s_coff = g.s_coff;
-        std::vector<TileD> tiles(g.tiles.size());
+        std::vector<int64_t> s_node_u, s_cb_u;
+        u_rows(g, uoff, s_node_u, s_cb_u);
+        std::vector<int32_t> s_coff;
+        std::vector<TileD> tiles;
+        stage_tiles<R>(g, s_cb_u, tile_contrib_, tiles, s_coff);
         {
-            const int CH = (sizeof(R) == 8) ? 16 : 8;
-            const int CE = CH / (int)sizeof(R);
-            for (size_t t = 0; t < g.tiles.size(); ++t) {
-                const TileH& th = g.tiles[t];
-                TileD td{};
-                td.s0 = th.s0;
-                td.s1 = th.s1;
-                td.seg0 = th.seg0;
-                td.seg1 = th.seg1;
-                td.npairs = th.npairs;
-                td.staged = th.staged ? 2 : 0;
-                td.contrib = contrib_of_tile(t);
-                if (th.staged) {
-                    const int rowlen = g.s_n[th.s0] * g.Pc;
-                    bool uni = (rowlen % CE) == 0;
-                    for (int64_t s = th.s0; s < th.s1 && uni; ++s)
-                        uni = (g.s_n[s] * g.Pc == rowlen) && ((s_cb_u[s] * g.Pc) % CE == 0);
-                    if (uni) {
-                        const int cpr = rowlen / CE;
-                        const int cstride = (cpr % 2 == 0) ? cpr + 1 : cpr;
-                        const int64_t need = (int64_t)(th.s1 - th.s0) * cstride * CE;
-                        if (need <= kTileChildren) {
-                            td.staged = 1;
-                            td.rowlen = rowlen;
-                            td.cpr = cpr;
-                            td.stride = cstride * CE;
-                            td.inv_cpr = 1.0f / (float)cpr;
-                            for (int64_t s = th.s0; s < th.s1; ++s) s_coff[s] = (int32_t)((s - th.s0) * td.stride);
-                        }
+            // records of the pipelined levels
+            size_t pool = 0;
+            fast_ = fast_levels<R, I>(g, tiles, &pool);
+            std::vector<unsigned char> rec(pool, 0);
+            for (int L = 0; L < g.D; ++L) {
+                const FastLevel& f = fast_[L];
+                if (f.recsize == 0) continue;
+                for (int64_t t = 0; t < f.ntiles; ++t) {
+                    const TileH& th = g.tiles[f.tile0 + t];
+                    unsigned char* r = rec.data() + f.rec + t * f.recsize;
+                    FastHdr hd{th.s0, (int)(th.s1 - th.s0), th.seg1 - th.seg0, th.npairs, 0};
+                    std::memcpy(r, &hd, sizeof(hd));
+                    FastSeg* sg = reinterpret_cast<FastSeg*>(r + 32);
+                    for (int k = th.seg0; k < th.seg1; ++k) {
+                        const SegH& shh = g.segs[k];
+                        FastSeg fs{};
+                        fs.h = shh.h;
+                        fs.qb = g.qbase_int[shh.h];
+                        fs.pair_off = shh.pair_off;
+                        fs.n = (int)(g.qbase_int[shh.h + 1] - g.qbase_int[shh.h]);
+                        fs.owner = g.owner_int[shh.h];
+                        fs.sb = (int)(shh.sb - th.s0);
+                        fs.se = (int)(shh.se - th.s0);
+                        sg[k - th.seg0] = fs;
+                    }
+                    I* node = reinterpret_cast<I*>(r + 32 + (th.seg1 - th.seg0) * sizeof(FastSeg));
+                    I* cb = node + (th.s1 - th.s0);
+                    I* dec = cb + (th.s1 - th.s0);
+                    for (int64_t s = th.s0; s < th.s1; ++s) {
+                        node[s - th.s0] = (I)s_node_u[s];
+                        cb[s - th.s0] = (I)s_cb_u[s];
+                        dec[s - th.s0] = (I)g.s_dec[s];
                     }
                 }
-                tiles[t] = td;
             }
+            if ((st = up(plan.pool, rec))) return st;
         }
         std::vector<SegD> segs(g.segs.size());
         for (size_t k = 0; k < g.segs.size(); ++k) {
@@ -1080,6 +1517,8 @@ struct Solver final : SolverBase {
 #define SETA(PC)                                                                                        \
     e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_CFR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
     if (e) return e;                                                                                    \
+    e = cudaFuncSetAttribute(k_bwd_fast<R, I, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);     \
+    if (e) return e;                                                                                    \
     e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_VALUES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
     if (e) return e;                                                                                    \
     e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
@@ -1123,6 +1562,27 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         const long long t0 = g.tile_ptr[L], t1 = g.tile_ptr[L + 1];
         if (t1 <= t0) return;
+        if (MODE == MODE_CFR && sig == dg.sig && use_fast_ && fast_[L].recsize > 0) {
+            FastLevel f = fast_[L];
+            f.last = last;
+            const int bytes = fast_plan(f, g.Pc, (int)sizeof(R)).bytes;
+            int per_sm = 1;
+            switch (g.Pc) {
+                case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 1>, kTileSlots, bytes); break;
+                case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 2>, kTileSlots, bytes); break;
+                case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 3>, kTileSlots, bytes); break;
+                default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 4>, kTileSlots, bytes); break;
+            }
+            per_sm = std::max(1, per_sm);
+            const unsigned nb = (unsigned)std::min<long long>(f.ntiles, (long long)num_sms_ * per_sm);
+            switch (g.Pc) {
+                case 1: k_bwd_fast<R, I, 1><<<nb, kTileSlots, bytes, st>>>(dg, at<unsigned char>(plan.pool), f); break;
+                case 2: k_bwd_fast<R, I, 2><<<nb, kTileSlots, bytes, st>>>(dg, at<unsigned char>(plan.pool), f); break;
+                case 3: k_bwd_fast<R, I, 3><<<nb, kTileSlots, bytes, st>>>(dg, at<unsigned char>(plan.pool), f); break;
+                default: k_bwd_fast<R, I, 4><<<nb, kTileSlots, bytes, st>>>(dg, at<unsigned char>(plan.pool), f); break;
+            }
+            return;
+        }
         const SmemLayout lay = lay_[L];
         const size_t sm = (size_t)lay.bytes;
         const unsigned nb = (unsigned)(t1 - t0);
