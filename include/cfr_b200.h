@@ -115,13 +115,15 @@ typedef struct {
     int32_t precision;   /* 64 (binary64) or 32 (binary32) working precision      */
     int32_t flags;       /* bit 0: disable CUDA-Graph capture (debug);            */
                          /* bit 1: reserved; bit 2: disable the pipelined         */
-                         /* (persistent) backward kernel (A/B comparisons)        */
+                         /* (persistent) backward kernel; bit 3: disable          */
+                         /* programmatic dependent launch (A/B comparisons)       */
     int32_t reserved;
 } cfr_solver_config;
 
 #define CFR_FLAG_NO_GRAPH 1
 #define CFR_FLAG_NO_PERSISTENT 2
 #define CFR_FLAG_NO_PIPELINE 4
+#define CFR_FLAG_NO_PDL 8
 
 /* Multi-GPU level sharding.  NULL or world_size == 1 means a
  * single GPU.  nccl_unique_id points to the 128-byte ncclUniqueId that rank 0

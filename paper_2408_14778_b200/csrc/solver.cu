@@ -128,6 +128,13 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// Programmatic dependent launch (PDL): a kernel lets its successor launch early
+// (launch_dependents) and waits for its predecessor's completion + memory flush
+// (wait) only before touching data the predecessor may write.  Both are no-ops
+// without a programmatic dependency.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 template <class R>
 __device__ __forceinline__ bool finite_(R x) {
     return isfinite(x);
@@ -143,6 +150,8 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
                                              long long d_end) {
     const int P = (PT > 0) ? PT : g.P;
     const long long stride = (long long)gridDim.x * blockDim.x;
+    pdl_trigger();
+    pdl_wait();
     for (long long d = d_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; d < d_end; d += stride) {
         const long long p = (long long)g.f_parent[d];
         const R x = sig[g.f_e[d]];
@@ -241,10 +250,11 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
     const bool staged = T.staged != 0;
     constexpr int CH = (sizeof(R) == 8) ? 16 : 8;     // cp.async chunk (bytes) of uniform tiles
     constexpr int CE = CH / (int)sizeof(R);            // elements per chunk
-    const long long t_iter = (MODE == MODE_CFR) ? g.ctrl[0] + 1 : 0;
 
     // ---- step 1: per-slot metadata (thread = slot), owner reach, segment + run tables
-    long long my_node = 0, my_cb = 0, my_eb = 0;
+    // (metadata is constant: loaded before waiting for the previous kernel)
+    pdl_trigger();
+    long long my_node = 0, my_cb = 0, my_eb = 0, my_dec = 0;
     int my_n = 0, my_actor = 0;
     if (tid < nslot) {
         const long long s = T.s0 + tid;
@@ -253,15 +263,17 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
         my_n = g.s_n[s];
         my_eb = (long long)g.s_ebase[s];
         my_actor = g.s_actor[s];
+        my_dec = (long long)g.s_dec[s];
         sm.scoff[tid] = g.s_coff[s];
         sm.scb[tid] = my_cb;
         sm.sn[tid] = my_n;
         sm.spoff[tid] = -1;
-        if (MODE != MODE_VALUES && my_actor >= 1) {
-            const long long dd = (long long)g.s_dec[s];
-            sm.spc[tid] = g.reach[dd * 2 * P + (my_actor - 1)];
-            sm.sph[tid] = g.reach[dd * 2 * P + P + (my_actor - 1)];
-        }
+    }
+    pdl_wait();
+    const long long t_iter = (MODE == MODE_CFR) ? g.ctrl[0] + 1 : 0;
+    if (tid < nslot && MODE != MODE_VALUES && my_actor >= 1) {
+        sm.spc[tid] = g.reach[my_dec * 2 * P + (my_actor - 1)];
+        sm.sph[tid] = g.reach[my_dec * 2 * P + P + (my_actor - 1)];
     }
     if (tid < nseg) {
         const SegD sg = g.segs[T.seg0 + tid];
@@ -361,12 +373,13 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
     // zero-sum storage (u2 = -u1) is applied to the sums: slices of -t are -slices of t.
     const int nitems = T.npairs + ((MODE == MODE_CFR) ? nseg : 0);
     int ns = 1;
-    while (ns < 8 && nitems * ns * 2 <= nth) ns <<= 1;
+    int lns = 0;                      // ns = 2^lns (shifts, no integer division)
+    while (ns < 8 && nitems * ns * 2 <= nth) { ns <<= 1; ++lns; }
     const int rounds = (nitems * ns + nth - 1) / nth;
     double kr0 = 0, kr1 = 0, kr2 = 0, kr3 = 0, kr4 = 0;
     for (int rd = 0; rd < rounds; ++rd) {
         const int wi = rd * nth + tid;
-        const int it = wi / ns, part = wi - it * ns;
+        const int it = wi >> lns, part = wi & (ns - 1);
         double c0 = 0, c1 = 0, c2 = 0;
         int k = 0, a = 0;
         bool is_pair = false, neg = false, active = false;
@@ -387,11 +400,25 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
             if (!is_pair) {
                 for (int ls = sg.sb + part; ls < sg.se; ls += ns) xadd(c0, c1, c2, (double)sm.sph[ls], g.scp0);
             } else if (staged) {
-                for (int ls = sg.sb + part; ls < sg.se; ls += ns) {
-                    const R uc = sm.ch[sm.scoff[ls] + a * PC + col];
-                    const R t = (MODE == MODE_CFR) ? sm.spc[ls] * (uc - sm.sv[ls * PC + col]) : sm.spc[ls] * uc;
-                    xadd(c0, c1, c2, (double)t, g.sc0);
+                double e0 = 0, e1 = 0, e2 = 0;   // second independent chain (ILP)
+                int ls = sg.sb + part;
+                for (; ls + ns < sg.se; ls += 2 * ns) {
+                    const R ua = sm.ch[sm.scoff[ls] + a * PC + col];
+                    const R ub = sm.ch[sm.scoff[ls + ns] + a * PC + col];
+                    const R ta = (MODE == MODE_CFR) ? sm.spc[ls] * (ua - sm.sv[ls * PC + col]) : sm.spc[ls] * ua;
+                    const R tb = (MODE == MODE_CFR) ? sm.spc[ls + ns] * (ub - sm.sv[(ls + ns) * PC + col])
+                                                    : sm.spc[ls + ns] * ub;
+                    xadd(c0, c1, c2, (double)ta, g.sc0);
+                    xadd(e0, e1, e2, (double)tb, g.sc0);
                 }
+                if (ls < sg.se) {
+                    const R ua = sm.ch[sm.scoff[ls] + a * PC + col];
+                    const R ta = (MODE == MODE_CFR) ? sm.spc[ls] * (ua - sm.sv[ls * PC + col]) : sm.spc[ls] * ua;
+                    xadd(c0, c1, c2, (double)ta, g.sc0);
+                }
+                c0 += e0;
+                c1 += e1;
+                c2 += e2;
             } else {
                 for (int ls = sg.sb + part; ls < sg.se; ls += ns) {
                     const R uc = g.U[(sm.scb[ls] + a) * PC + col];
@@ -435,7 +462,7 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
     if (sig_staged) {
         for (int rd = 0; rd < rounds && rd < 5; ++rd) {
             const int wi = rd * nth + tid;
-            const int it = wi / ns, part = wi - it * ns;
+            const int it = wi >> lns, part = wi & (ns - 1);
             if (it < nitems && part == 0) {
                 const double x = rd == 0 ? kr0 : rd == 1 ? kr1 : rd == 2 ? kr2 : rd == 3 ? kr3 : kr4;
                 if (it < T.npairs) rt[it] = (R)x;
@@ -609,25 +636,27 @@ __device__ __forceinline__ void fast_issue_data(const DG<R, I>& g, const FastLev
     const I* node = reinterpret_cast<const I*>(meta + 32 + hd.nseg * (int)sizeof(FastSeg));
     const I* cb = node + hd.nslot;
     const I* dec = cb + hd.nslot;
+    const unsigned char* sseg = reinterpret_cast<const unsigned char*>(dec + hd.nslot);
+    const unsigned char* pseg = sseg + hd.nslot;
     (void)node;
     const int P = g.P;
-    const int tot = hd.nslot * L.cpr;
-    for (int c = threadIdx.x; c < tot; c += blockDim.x) {
-        const int row = __float2int_rd(((float)c + 0.5f) * L.inv_cpr);
-        const int k = c - row * L.cpr;
-        cp_async<CH>(ch + row * L.stride + k * CE, g.U + (long long)cb[row] * PC + k * CE);
+    {
+        // 2-D walk: thread -> (row r0 + j * rpp, chunk k), no per-chunk division
+        const int rpp = blockDim.x / L.cpr;
+        const int r0 = threadIdx.x / L.cpr, k = threadIdx.x - r0 * L.cpr;
+        if (r0 < rpp)
+            for (int row = r0; row < hd.nslot; row += rpp)
+                cp_async<CH>(ch + row * L.stride + k * CE, g.U + (long long)cb[row] * PC + k * CE);
     }
     for (int s = threadIdx.x; s < hd.nslot; s += blockDim.x) {
-        int k = 0;
-        while (k + 1 < hd.nseg && seg[k + 1].sb <= s) ++k;
+        const int k = sseg[s];
         const long long d = (long long)dec[s];
         const int i = seg[k].owner;
         cp_async<(int)sizeof(R)>(spc + s, g.reach + d * 2 * P + (i - 1));
         cp_async<(int)sizeof(R)>(sph + s, g.reach + d * 2 * P + P + (i - 1));
     }
     for (int p = threadIdx.x; p < hd.npairs; p += blockDim.x) {
-        int k = 0;
-        while (k + 1 < hd.nseg && seg[k + 1].pair_off <= p) ++k;
+        const int k = pseg[p];
         const long long q = seg[k].qb + (p - seg[k].pair_off);
         cp_async<(int)sizeof(R)>(ssig + p, g.sig + q);
         cp_async<(int)sizeof(R)>(sreg + p, g.regret + q);
@@ -638,7 +667,7 @@ __device__ __forceinline__ void fast_issue_data(const DG<R, I>& g, const FastLev
 }
 
 template <class R, class I, int PC>
-__global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsigned char* __restrict__ pool,
+__global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, const unsigned char* __restrict__ pool,
                                                          FastLevel L) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const FastPlan F = fast_plan(L, PC, (int)sizeof(R));
@@ -656,13 +685,15 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsig
                                   (R*)(d + F.o_spc), (R*)(d + F.o_sph), (R*)(d + F.o_sden));
     };
     const int tid = threadIdx.x, nth = blockDim.x;
-    const long long t_iter = g.ctrl[0] + 1;
-    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
+    pdl_trigger();
     long long t = blockIdx.x;
     if (t >= L.ntiles) return;
-    // prologue: meta(t) -> data(t), meta(t + G)
+    // prologue: meta(t) (constant records: before the PDL wait) -> data(t), meta(t + G)
     fast_issue_meta<R, I, PC>(pool, L, t, META(0));
     asm volatile("cp.async.commit_group;\n" ::);
+    pdl_wait();
+    const long long t_iter = g.ctrl[0] + 1;
+    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
     cp_async_wait_all();
     __syncthreads();
     ISSUE(0, 0);
@@ -684,6 +715,8 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsig
         const FastHdr hd = *reinterpret_cast<const FastHdr*>(meta);
         const FastSeg* seg = reinterpret_cast<const FastSeg*>(meta + 32);
         const I* node = reinterpret_cast<const I*>(meta + 32 + hd.nseg * (int)sizeof(FastSeg));
+        const unsigned char* rsseg = reinterpret_cast<const unsigned char*>(node + 3 * hd.nslot);
+        const unsigned char* rpseg = rsseg + hd.nslot;
         unsigned char* dbuf = DATA(db);
         R* ch = (R*)dbuf;
         const R* ssig = (const R*)(dbuf + F.o_ssig);
@@ -693,24 +726,15 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsig
         const R* sph = (const R*)(dbuf + F.o_sph);
         const R* sden = (const R*)(dbuf + F.o_sden);
         const int nslot = hd.nslot, nseg = hd.nseg, npairs = hd.npairs;
-        for (int p = tid; p < npairs; p += nth) {
-            int k = 0;
-            while (k + 1 < nseg && seg[k + 1].pair_off <= p) ++k;
-            pseg_[p] = (unsigned char)k;
-        }
-        for (int s = tid; s < nslot; s += nth) {
-            int k = 0;
-            while (k + 1 < nseg && seg[k + 1].sb <= s) ++k;
-            spoff_[s] = seg[k].pair_off;
-        }
-        __syncthreads();
+        (void)pseg_;
+        (void)spoff_;
         // phase A: node values (Eq 1), ascending actions from +0
         if (tid < nslot) {
             R v[PC];
 #pragma unroll
             for (int j = 0; j < PC; ++j) v[j] = (R)0;
             const R* row = ch + tid * L.stride;
-            const R* sg = ssig + spoff_[tid];
+            const R* sg = ssig + seg[rsseg[tid]].pair_off;
             const int n = L.rowlen / PC;
             for (int a = 0; a < n; ++a) {
                 const R x = sg[a];
@@ -728,17 +752,18 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsig
         // phase B: exact sums (pairs, then one pi_bar item per segment)
         const int nitems = npairs + nseg;
         int ns = 1;
-        while (ns < 8 && nitems * ns * 2 <= nth) ns <<= 1;
+        int lns = 0;                  // ns = 2^lns (shifts, no integer division)
+        while (ns < 8 && nitems * ns * 2 <= nth) { ns <<= 1; ++lns; }
         const int rounds = (nitems * ns + nth - 1) / nth;
         double kr0 = 0, kr1 = 0, kr2 = 0, kr3 = 0, kr4 = 0;
         for (int rd = 0; rd < rounds; ++rd) {
             const int wi = rd * nth + tid;
-            const int itm = wi / ns, part = wi - itm * ns;
+            const int itm = wi >> lns, part = wi & (ns - 1);
             double c0 = 0, c1 = 0, c2 = 0;
             bool is_pair = false, neg = false;
             int k = 0, a = 0;
             if (itm < npairs) {
-                k = pseg_[itm];
+                k = rpseg[itm];
                 a = itm - seg[k].pair_off;
                 is_pair = true;
                 neg = (PC == 1) && (seg[k].owner == 2);
@@ -751,11 +776,26 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsig
                 if (!is_pair) {
                     for (int ls = sb + part; ls < se; ls += ns) xadd(c0, c1, c2, (double)sph[ls], g.scp0);
                 } else {
-                    for (int ls = sb + part; ls < se; ls += ns) {
-                        const R uc = ch[ls * L.stride + a * PC + col];
-                        const R tt = spc[ls] * (uc - sv_[ls * PC + col]);
-                        xadd(c0, c1, c2, (double)tt, g.sc0);
+                    // two independent slice chains (ILP); integer-valued partial sums
+                    // combine exactly
+                    double e0 = 0, e1 = 0, e2 = 0;
+                    int ls = sb + part;
+                    for (; ls + ns < se; ls += 2 * ns) {
+                        const R ua = ch[ls * L.stride + a * PC + col];
+                        const R ub = ch[(ls + ns) * L.stride + a * PC + col];
+                        const R ta = spc[ls] * (ua - sv_[ls * PC + col]);
+                        const R tb = spc[ls + ns] * (ub - sv_[(ls + ns) * PC + col]);
+                        xadd(c0, c1, c2, (double)ta, g.sc0);
+                        xadd(e0, e1, e2, (double)tb, g.sc0);
                     }
+                    if (ls < se) {
+                        const R ua = ch[ls * L.stride + a * PC + col];
+                        const R ta = spc[ls] * (ua - sv_[ls * PC + col]);
+                        xadd(c0, c1, c2, (double)ta, g.sc0);
+                    }
+                    c0 += e0;
+                    c1 += e1;
+                    c2 += e2;
                 }
                 if (neg) { c0 = -c0; c1 = -c1; c2 = -c2; }
             }
@@ -778,7 +818,7 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsig
         R* pos = ch + (((npairs * (int)sizeof(R) + 15) & ~15) / (int)sizeof(R));
         for (int rd = 0; rd < rounds && rd < 5; ++rd) {
             const int wi = rd * nth + tid;
-            const int itm = wi / ns, part = wi - itm * ns;
+            const int itm = wi >> lns, part = wi & (ns - 1);
             if (itm < nitems && part == 0) {
                 const double x = rd == 0 ? kr0 : rd == 1 ? kr1 : rd == 2 ? kr2 : rd == 3 ? kr3 : kr4;
                 if (itm < npairs) rt[itm] = (R)x;
@@ -788,7 +828,7 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsig
         __syncthreads();
         // phase C: fused update (Eq 8/15 or CFR+, Eq 10, Eq 9)
         for (int p = tid; p < npairs; p += nth) {
-            const int k = pseg_[p];
+            const int k = rpseg[p];
             const long long q = seg[k].qb + (p - seg[k].pair_off);
             const R r_t = rt[p];
             R r;
@@ -813,7 +853,7 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsig
         }
         __syncthreads();
         for (int p = tid; p < npairs; p += nth) {
-            const int k = pseg_[p];
+            const int k = rpseg[p];
             const int a = p - seg[k].pair_off;
             const R z = zs_[k];
             const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)seg[k].n;
@@ -842,6 +882,8 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd_fast(DG<R, I> g, const unsig
 // exact sums, then the same Eq 8/15, Eq 10, Eq 9 steps; zero the accumulators.
 template <class R, class I>
 __global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
+    pdl_trigger();
+    pdl_wait();
     const long long t_iter = g.ctrl[0] + 1;
     const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
     bool bad = false;
@@ -925,12 +967,16 @@ __global__ void k_average(DG<R, I> g, R* out, long long H, long long Q, long lon
 template <class R>
 __global__ void k_cut_pack(const R* __restrict__ U, const long long* __restrict__ rows,
                            const unsigned char* __restrict__ owned, R* __restrict__ buf, long long n, int Pc) {
+    pdl_trigger();
+    pdl_wait();
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         for (int j = 0; j < Pc; ++j) buf[i * Pc + j] = owned[i] ? U[rows[i] * Pc + j] : (R)0;
 }
 template <class R>
 __global__ void k_cut_unpack(R* __restrict__ U, const long long* __restrict__ rows, const R* __restrict__ buf, long long n,
                              int Pc) {
+    pdl_trigger();
+    pdl_wait();
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         for (int j = 0; j < Pc; ++j) U[rows[i] * Pc + j] = buf[i * Pc + j];
 }
@@ -957,6 +1003,23 @@ __global__ void k_mask_h(R* __restrict__ out, const unsigned char* __restrict__ 
             return CFR_ERR_CUDA;                                                                   \
         }                                                                                          \
     } while (0)
+
+// Launch with the programmatic-stream-serialization attribute (PDL) when `pdl`.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+}
 
 struct SolverBase {
     virtual ~SolverBase() {}
@@ -1073,7 +1136,7 @@ static std::vector<FastLevel> fast_levels(const Game& g, const std::vector<TileD
         int rowlen = -1, maxslot = 1, maxseg = 1, maxpairs = 1, maxch = 0;
         for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1] && ok; ++t) {
             const TileD& td = tiles[t];
-            if (td.staged != 1 || td.npairs > kTilePairs) { ok = false; break; }
+            if (td.staged != 1 || td.npairs > kTilePairs || td.cpr > 2 * kTileSlots) { ok = false; break; }
             if (rowlen < 0) rowlen = td.rowlen;
             if (td.rowlen != rowlen) { ok = false; break; }
             int64_t members = 0;
@@ -1098,7 +1161,8 @@ static std::vector<FastLevel> fast_levels(const Game& g, const std::vector<TileD
             f.cpr = t0.cpr;
             f.stride = t0.stride;
             f.inv_cpr = t0.inv_cpr;
-            f.recsize = (int)((32 + (int64_t)maxseg * sizeof(FastSeg) + 3 * sizeof(I) * (int64_t)maxslot + 15) & ~int64_t(15));
+            f.recsize = (int)((32 + (int64_t)maxseg * sizeof(FastSeg) + 3 * sizeof(I) * (int64_t)maxslot + maxslot +
+                               maxpairs + 15) & ~int64_t(15));
             f.rec = (long long)pool;
             pool += (size_t)f.recsize * (size_t)f.ntiles;
         }
@@ -1194,6 +1258,7 @@ struct Solver final : SolverBase {
     int64_t launches_per_iter = 0;
     bool use_graph = true;
     bool use_fast_ = true;
+    bool pdl_ = true;
     int num_sms_ = 148;
     int world = 1, rank = 0;
     bool external = false;        // world > 1 without NCCL: the caller runs the exchanges
@@ -1311,6 +1376,7 @@ struct Solver final : SolverBase {
         }
         use_graph = !(cfg.flags & CFR_FLAG_NO_GRAPH);
         use_fast_ = !(cfg.flags & CFR_FLAG_NO_PIPELINE);
+        pdl_ = !(cfg.flags & CFR_FLAG_NO_PDL);
         {
             int dev = 0;
             CU(cudaGetDevice(&dev));
@@ -1405,6 +1471,15 @@ struct Solver final : SolverBase {
                         node[s - th.s0] = (I)s_node_u[s];
                         cb[s - th.s0] = (I)s_cb_u[s];
                         dec[s - th.s0] = (I)g.s_dec[s];
+                    }
+                    // segment of every slot and of every pair (no searches on the device)
+                    unsigned char* sseg = reinterpret_cast<unsigned char*>(dec + (th.s1 - th.s0));
+                    unsigned char* pseg = sseg + (th.s1 - th.s0);
+                    for (int k = th.seg0; k < th.seg1; ++k) {
+                        const SegH& shh = g.segs[k];
+                        for (int64_t s = shh.sb; s < shh.se; ++s) sseg[s - th.s0] = (unsigned char)(k - th.seg0);
+                        const int n = (int)(g.qbase_int[shh.h + 1] - g.qbase_int[shh.h]);
+                        for (int a = 0; a < n; ++a) pseg[shh.pair_off + a] = (unsigned char)(k - th.seg0);
                     }
                 }
             }
@@ -1552,9 +1627,9 @@ struct Solver final : SolverBase {
         const int threads = 256;
         const long long blocks = std::min<long long>((n + threads - 1) / threads, 148LL * 16);
         if (g.P == 2)
-            k_fwd<R, I, 2><<<(unsigned)blocks, threads, 0, st>>>(dg, sig, s0, s1);
+            launch(pdl_, k_fwd<R, I, 2>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1);
         else
-            k_fwd<R, I, 0><<<(unsigned)blocks, threads, 0, st>>>(dg, sig, s0, s1);
+            launch(pdl_, k_fwd<R, I, 0>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1);
     }
 
     template <int MODE>
@@ -1562,24 +1637,25 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         const long long t0 = g.tile_ptr[L], t1 = g.tile_ptr[L + 1];
         if (t1 <= t0) return;
-        if (MODE == MODE_CFR && sig == dg.sig && use_fast_ && fast_[L].recsize > 0) {
+        // pipelined kernel: measured faster for f64 only (f32 tiles move half the bytes)
+        if (MODE == MODE_CFR && sizeof(R) == 8 && sig == dg.sig && use_fast_ && fast_[L].recsize > 0) {
             FastLevel f = fast_[L];
             f.last = last;
             const int bytes = fast_plan(f, g.Pc, (int)sizeof(R)).bytes;
             int per_sm = 1;
             switch (g.Pc) {
-                case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 1>, kTileSlots, bytes); break;
-                case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 2>, kTileSlots, bytes); break;
-                case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 3>, kTileSlots, bytes); break;
-                default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 4>, kTileSlots, bytes); break;
+                case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 1>, 2 * kTileSlots, bytes); break;
+                case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 2>, 2 * kTileSlots, bytes); break;
+                case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 3>, 2 * kTileSlots, bytes); break;
+                default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 4>, 2 * kTileSlots, bytes); break;
             }
             per_sm = std::max(1, per_sm);
             const unsigned nb = (unsigned)std::min<long long>(f.ntiles, (long long)num_sms_ * per_sm);
             switch (g.Pc) {
-                case 1: k_bwd_fast<R, I, 1><<<nb, kTileSlots, bytes, st>>>(dg, at<unsigned char>(plan.pool), f); break;
-                case 2: k_bwd_fast<R, I, 2><<<nb, kTileSlots, bytes, st>>>(dg, at<unsigned char>(plan.pool), f); break;
-                case 3: k_bwd_fast<R, I, 3><<<nb, kTileSlots, bytes, st>>>(dg, at<unsigned char>(plan.pool), f); break;
-                default: k_bwd_fast<R, I, 4><<<nb, kTileSlots, bytes, st>>>(dg, at<unsigned char>(plan.pool), f); break;
+                case 1: launch(pdl_, k_bwd_fast<R, I, 1>, dim3(nb), dim3(2 * kTileSlots), (size_t)bytes, st, dg, (const unsigned char*)at<unsigned char>(plan.pool), f); break;
+                case 2: launch(pdl_, k_bwd_fast<R, I, 2>, dim3(nb), dim3(2 * kTileSlots), (size_t)bytes, st, dg, (const unsigned char*)at<unsigned char>(plan.pool), f); break;
+                case 3: launch(pdl_, k_bwd_fast<R, I, 3>, dim3(nb), dim3(2 * kTileSlots), (size_t)bytes, st, dg, (const unsigned char*)at<unsigned char>(plan.pool), f); break;
+                default: launch(pdl_, k_bwd_fast<R, I, 4>, dim3(nb), dim3(2 * kTileSlots), (size_t)bytes, st, dg, (const unsigned char*)at<unsigned char>(plan.pool), f); break;
             }
             return;
         }
@@ -1587,17 +1663,17 @@ struct Solver final : SolverBase {
         const size_t sm = (size_t)lay.bytes;
         const unsigned nb = (unsigned)(t1 - t0);
         switch (g.Pc) {
-            case 1: k_bwd<R, I, 1, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last, lay); break;
-            case 2: k_bwd<R, I, 2, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last, lay); break;
-            case 3: k_bwd<R, I, 3, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last, lay); break;
-            default: k_bwd<R, I, 4, MODE><<<nb, kTileSlots, sm, st>>>(dg, sig, t0, br_player, last, lay); break;
+            case 1: launch(pdl_, k_bwd<R, I, 1, MODE>, dim3(nb), dim3(kTileSlots), sm, st, dg, sig, (long long)t0, br_player, last, lay); break;
+            case 2: launch(pdl_, k_bwd<R, I, 2, MODE>, dim3(nb), dim3(kTileSlots), sm, st, dg, sig, (long long)t0, br_player, last, lay); break;
+            case 3: launch(pdl_, k_bwd<R, I, 3, MODE>, dim3(nb), dim3(kTileSlots), sm, st, dg, sig, (long long)t0, br_player, last, lay); break;
+            default: launch(pdl_, k_bwd<R, I, 4, MODE>, dim3(nb), dim3(kTileSlots), sm, st, dg, sig, (long long)t0, br_player, last, lay); break;
         }
     }
 
     void deferred_update(cudaStream_t st, int last) {
         const long long n = dg.ndef;
         const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 8));
-        k_deferred<R, I><<<blocks, 256, 0, st>>>(dg, last);
+        launch(pdl_, k_deferred<R, I>, dim3(blocks), dim3(256), 0, st, dg, last);
     }
 
     // ---- iteration phases.  One iteration = lower (forward + backward of the

@@ -1,4 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_bwd_fast -s 2 -c 1 -o gpurun_out/prof_fast_n40 -f python tools/ncu_target.py 40 64 3 > gpurun_out/ncu_fast.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_bwd_fast -s 0 -c 1 -o gpurun_out/prof_fast_n40 -f python tools/ncu_target.py 40 64 3 > gpurun_out/ncu_fast.log 2>&1
 tail -3 gpurun_out/ncu_fast.log
