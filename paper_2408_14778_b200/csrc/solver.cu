@@ -187,7 +187,7 @@ struct SegS {
 // Shared-memory layout of one backward launch (per level: sized by the
 // level's largest tile so small tiles leave room for more resident CTAs).
 struct SmemLayout {
-    int ch, sv, spc, sph, ssig, sreg, ssn, pib, zs, sden, seg, soff, best, scoff, spoff, sn, scb, pseg;
+    int ch, sv, spc, sph, ssig, sreg, ssn, pib, zs, sden, seg, soff, best, scoff, spoff, sn, scb, pseg, cm, ccnt;
     int bytes;
 };
 template <class R>
@@ -197,6 +197,8 @@ struct TileView {
     int *soff, *best, *scoff, *spoff, *sn;
     long long* scb;
     unsigned char* pseg;
+    short* cm;     // per segment: members with nonzero pi_check (tile-local slots)
+    int* ccnt;
 };
 template <class R>
 __device__ __forceinline__ TileView<R> make_view(unsigned char* b, const SmemLayout& L) {
@@ -219,6 +221,8 @@ __device__ __forceinline__ TileView<R> make_view(unsigned char* b, const SmemLay
     v.sn = (int*)(b + L.sn);
     v.scb = (long long*)(b + L.scb);
     v.pseg = (unsigned char*)(b + L.pseg);
+    v.cm = (short*)(b + L.cm);
+    v.ccnt = (int*)(b + L.ccnt);
     return v;
 }
 
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
     const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
     const int P = g.P;
     R* const rt = sm.ch;                  // valid after phase B
-    R* const pos = sm.ch + (lay.ssn - lay.ssig) / (int)sizeof(R);   // = ch + (pairs capacity)
+    R* const pos = sm.ch + (lay.sreg - lay.ssig) / (int)sizeof(R);  // = ch + (pairs capacity)
     const bool sig_staged = T.npairs <= kTilePairs;
     const bool staged = T.staged != 0;
     constexpr int CH = (sizeof(R) == 8) ? 16 : 8;     // cp.async chunk (bytes) of uniform tiles
@@ -364,6 +368,19 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
         for (int j = 0; j < PC; ++j) sm.sv[tid * PC + j] = v[j];
     }
     if (MODE == MODE_VALUES) return;
+    // members with pi_check == 0 add exact zeros to every sum: compact them away
+    for (int k = warp; k < nseg; k += nwarps) {
+        const int sb = sm.seg[k].sb, se = sm.seg[k].se;
+        int cnt = 0;
+        for (int base = sb; base < se; base += 32) {
+            const int s2 = base + lane;
+            const bool f = (s2 < se) && (sm.spc[s2] != (R)0);
+            const unsigned m = __ballot_sync(0xffffffffu, f);
+            if (f) sm.cm[sb + cnt + __popc(m & ((1u << lane) - 1u))] = (short)s2;
+            cnt += __popc(m);
+        }
+        if (lane == 0) sm.ccnt[k] = cnt;
+    }
     __syncthreads();
 
     // ---- phase B: exact sums.  Work items: every (infoset, action) pair (r~ or BR
@@ -401,26 +418,31 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
                 for (int ls = sg.sb + part; ls < sg.se; ls += ns) xadd(c0, c1, c2, (double)sm.sph[ls], g.scp0);
             } else if (staged) {
                 double e0 = 0, e1 = 0, e2 = 0;   // second independent chain (ILP)
-                int ls = sg.sb + part;
-                for (; ls + ns < sg.se; ls += 2 * ns) {
-                    const R ua = sm.ch[sm.scoff[ls] + a * PC + col];
-                    const R ub = sm.ch[sm.scoff[ls + ns] + a * PC + col];
-                    const R ta = (MODE == MODE_CFR) ? sm.spc[ls] * (ua - sm.sv[ls * PC + col]) : sm.spc[ls] * ua;
-                    const R tb = (MODE == MODE_CFR) ? sm.spc[ls + ns] * (ub - sm.sv[(ls + ns) * PC + col])
-                                                    : sm.spc[ls + ns] * ub;
+                const short* mem = sm.cm + sg.sb;
+                const int cnt = sm.ccnt[k];
+                int j = part;
+                for (; j + ns < cnt; j += 2 * ns) {
+                    const int la = mem[j], lb = mem[j + ns];
+                    const R ua = sm.ch[sm.scoff[la] + a * PC + col];
+                    const R ub = sm.ch[sm.scoff[lb] + a * PC + col];
+                    const R ta = (MODE == MODE_CFR) ? sm.spc[la] * (ua - sm.sv[la * PC + col]) : sm.spc[la] * ua;
+                    const R tb = (MODE == MODE_CFR) ? sm.spc[lb] * (ub - sm.sv[lb * PC + col]) : sm.spc[lb] * ub;
                     xadd(c0, c1, c2, (double)ta, g.sc0);
                     xadd(e0, e1, e2, (double)tb, g.sc0);
                 }
-                if (ls < sg.se) {
-                    const R ua = sm.ch[sm.scoff[ls] + a * PC + col];
-                    const R ta = (MODE == MODE_CFR) ? sm.spc[ls] * (ua - sm.sv[ls * PC + col]) : sm.spc[ls] * ua;
+                if (j < cnt) {
+                    const int la = mem[j];
+                    const R ua = sm.ch[sm.scoff[la] + a * PC + col];
+                    const R ta = (MODE == MODE_CFR) ? sm.spc[la] * (ua - sm.sv[la * PC + col]) : sm.spc[la] * ua;
                     xadd(c0, c1, c2, (double)ta, g.sc0);
                 }
                 c0 += e0;
                 c1 += e1;
                 c2 += e2;
             } else {
-                for (int ls = sg.sb + part; ls < sg.se; ls += ns) {
+                const short* mem = sm.cm + sg.sb;
+                for (int j = part; j < sm.ccnt[k]; j += ns) {
+                    const int ls = mem[j];
                     const R uc = g.U[(sm.scb[ls] + a) * PC + col];
                     const R t = (MODE == MODE_CFR) ? sm.spc[ls] * (uc - sm.sv[ls * PC + col]) : sm.spc[ls] * uc;
                     xadd(c0, c1, c2, (double)t, g.sc0);
@@ -590,7 +612,7 @@ struct FastPlan {
     int meta, mstride;        // meta record k at meta + k * mstride
     int data, dstride;        // data buffer k at data + k * dstride
     int o_ssig, o_sreg, o_ssn, o_spc, o_sph, o_sden;   // offsets inside a data buffer
-    int sv, pib, zs, spoff, pseg;
+    int sv, pib, zs, spoff, pseg, cm, ccnt;
     int bytes;
 };
 __host__ __device__ inline FastPlan fast_plan(const FastLevel& L, int Pc, int w) {
@@ -614,6 +636,8 @@ __host__ __device__ inline FastPlan fast_plan(const FastLevel& L, int Pc, int w)
     f.zs = x; x += al(L.maxseg * w);
     f.spoff = x; x += al(L.maxslot * 4);
     f.pseg = x; x += al(L.maxpairs);
+    f.cm = x; x += al(L.maxslot * 2);
+    f.ccnt = x; x += al(L.maxseg * 4);
     f.bytes = x;
     return f;
 }
@@ -679,6 +703,8 @@ __global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, cons
     R* const zs_ = (R*)(B + F.zs);
     int* const spoff_ = (int*)(B + F.spoff);
     unsigned char* const pseg_ = B + F.pseg;
+    short* const cm_ = (short*)(B + F.cm);      // members with nonzero pi_check, per segment
+    int* const ccnt_ = (int*)(B + F.ccnt);
     auto ISSUE = [&](int mk, int dk) {
         unsigned char* d = DATA(dk);
         fast_issue_data<R, I, PC>(g, L, META(mk), (R*)d, (R*)(d + F.o_ssig), (R*)(d + F.o_sreg), (R*)(d + F.o_ssn),
@@ -748,6 +774,23 @@ __global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, cons
                 sv_[tid * PC + j] = v[j];
             }
         }
+        // members whose pi_check is zero contribute exact zeros to every r~ sum
+        // (slices of +-0 are 0): compact them away (warp ballot per segment)
+        {
+            const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+            for (int k = warp; k < nseg; k += nwarps) {
+                const int sb = seg[k].sb, se = seg[k].se;
+                int cnt = 0;
+                for (int base = sb; base < se; base += 32) {
+                    const int s2 = base + lane;
+                    const bool f = (s2 < se) && (spc[s2] != (R)0);
+                    const unsigned m = __ballot_sync(0xffffffffu, f);
+                    if (f) cm_[sb + cnt + __popc(m & ((1u << lane) - 1u))] = (short)s2;
+                    cnt += __popc(m);
+                }
+                if (lane == 0) ccnt_[k] = cnt;
+            }
+        }
         __syncthreads();
         // phase B: exact sums (pairs, then one pi_bar item per segment)
         const int nitems = npairs + nseg;
@@ -779,18 +822,22 @@ __global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, cons
                     // two independent slice chains (ILP); integer-valued partial sums
                     // combine exactly
                     double e0 = 0, e1 = 0, e2 = 0;
-                    int ls = sb + part;
-                    for (; ls + ns < se; ls += 2 * ns) {
-                        const R ua = ch[ls * L.stride + a * PC + col];
-                        const R ub = ch[(ls + ns) * L.stride + a * PC + col];
-                        const R ta = spc[ls] * (ua - sv_[ls * PC + col]);
-                        const R tb = spc[ls + ns] * (ub - sv_[(ls + ns) * PC + col]);
+                    const short* mem = cm_ + sb;
+                    const int cnt = ccnt_[k];
+                    int j = part;
+                    for (; j + ns < cnt; j += 2 * ns) {
+                        const int la = mem[j], lb = mem[j + ns];
+                        const R ua = ch[la * L.stride + a * PC + col];
+                        const R ub = ch[lb * L.stride + a * PC + col];
+                        const R ta = spc[la] * (ua - sv_[la * PC + col]);
+                        const R tb = spc[lb] * (ub - sv_[lb * PC + col]);
                         xadd(c0, c1, c2, (double)ta, g.sc0);
                         xadd(e0, e1, e2, (double)tb, g.sc0);
                     }
-                    if (ls < se) {
-                        const R ua = ch[ls * L.stride + a * PC + col];
-                        const R ta = spc[ls] * (ua - sv_[ls * PC + col]);
+                    if (j < cnt) {
+                        const int la = mem[j];
+                        const R ua = ch[la * L.stride + a * PC + col];
+                        const R ta = spc[la] * (ua - sv_[la * PC + col]);
                         xadd(c0, c1, c2, (double)ta, g.sc0);
                     }
                     c0 += e0;
@@ -1326,6 +1373,8 @@ struct Solver final : SolverBase {
         L.sn = take(maxslot * 4);
         L.scb = take(maxslot * 8);
         L.pseg = take(maxpairs);
+        L.cm = take(maxslot * 2);
+        L.ccnt = take(maxseg * 4);
         L.bytes = off;
         return L;
     }
