@@ -27,6 +27,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "game.hpp"
@@ -151,6 +152,52 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
     const int P = (PT > 0) ? PT : g.P;
     const long long stride = (long long)gridDim.x * blockDim.x;
     pdl_trigger();
+    if (PT == 2) {
+        // two players: 4-value rows (32 B) moved as two 16-byte vectors; FW rows
+        // per thread with every load issued before the first use (the parent rows
+        // are gathers: memory-level parallelism, not bandwidth, bounds this pass)
+        constexpr int FW = 4;
+        using V2 = typename std::conditional<sizeof(R) == 8, double2, float2>::type;
+        const long long n = d_end - d_begin;
+        const long long chunk = (long long)blockDim.x * FW;
+        pdl_wait();
+        for (long long base = (long long)blockIdx.x * chunk; base < n; base += (long long)gridDim.x * chunk) {
+            long long p[FW];
+            long long e[FW];
+            int act[FW];
+#pragma unroll
+            for (int k = 0; k < FW; ++k) {
+                const long long i = base + k * blockDim.x + threadIdx.x;
+                const long long d = d_begin + (i < n ? i : 0);
+                p[k] = (long long)g.f_parent[d];
+                e[k] = (long long)g.f_e[d];
+                act[k] = g.f_pact[d];
+            }
+            V2 a[FW], b[FW];
+            R x[FW];
+#pragma unroll
+            for (int k = 0; k < FW; ++k) {
+                const V2* src = reinterpret_cast<const V2*>(g.reach + p[k] * 4);
+                a[k] = src[0];   // pi_check(1), pi_check(2)
+                b[k] = src[1];   // pi_hat(1), pi_hat(2)
+                x[k] = sig[e[k]];
+            }
+#pragma unroll
+            for (int k = 0; k < FW; ++k) {
+                const long long i = base + k * blockDim.x + threadIdx.x;
+                if (i >= n) continue;
+                V2 ca, cb;
+                ca.x = (act[k] != 1) ? a[k].x * x[k] : a[k].x;
+                ca.y = (act[k] != 2) ? a[k].y * x[k] : a[k].y;
+                cb.x = (act[k] == 1) ? b[k].x * x[k] : b[k].x;
+                cb.y = (act[k] == 2) ? b[k].y * x[k] : b[k].y;
+                V2* dst = reinterpret_cast<V2*>(g.reach + (d_begin + i) * 4);
+                dst[0] = ca;
+                dst[1] = cb;
+            }
+        }
+        return;
+    }
     pdl_wait();
     for (long long d = d_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; d < d_end; d += stride) {
         const long long p = (long long)g.f_parent[d];
@@ -1112,16 +1159,34 @@ static std::vector<int64_t> u_layout(const Game& g, size_t elem) {
     return off;
 }
 
-// U rows of the slots' nodes and first children (u_layout offsets).
+// Device row order.  Row 0 is the root; the rows of depth L+1 are
+// the children of the depth-L slots taken in SLOT order (each slot's children
+// contiguous, in action order).  A backward tile's child rows are then one
+// contiguous block, as are its reach rows (reach is indexed by slot) and its
+// (h, a) state: every stream of the backward pass is sequential.  Only the
+// per-node value write (into the parent's row) scatters.
+// node_u[s] / cb_u[s]: U row of slot s's node / first child.
 static void u_rows(const Game& g, const std::vector<int64_t>& uoff, std::vector<int64_t>& node_u,
                    std::vector<int64_t>& cb_u) {
-    node_u.resize(g.NS);
-    cb_u.resize(g.NS);
-    for (int L = 0; L < g.D; ++L)
+    node_u.assign(g.NS, 0);
+    cb_u.assign(g.NS, 0);
+    std::vector<int64_t> sod(g.ND, -1);   // slot of each dec index
+    for (int64_t s = 0; s < g.NS; ++s) sod[g.s_dec[s]] = s;
+    for (int L = 0; L < g.D; ++L) {
+        int64_t run = 0;
         for (int64_t s = g.slot_ptr[L]; s < g.slot_ptr[L + 1]; ++s) {
-            node_u[s] = uoff[L] + (g.s_node[s] - g.level_ptr[L]);
-            cb_u[s] = uoff[L + 1] + (g.s_cb[s] - g.level_ptr[L + 1]);
+            cb_u[s] = uoff[L + 1] + run;
+            run += g.s_n[s];
         }
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < g.NS; ++s) {
+        const int64_t d = g.s_dec[s];
+        const int64_t pd = g.f_parent[d];
+        if (pd < 0) { node_u[s] = 0; continue; }   // the root
+        const int64_t ps = sod[pd];
+        node_u[s] = cb_u[ps] + (g.f_e[d] - g.s_ebase[ps]);   // f_e = parent's edge base + action
+    }
 }
 
 // Staging layout per tile (precision dependent): uniform rows whose starts and
@@ -1472,18 +1537,37 @@ struct Solver final : SolverBase {
         }
         // ---- uploads
         cfr_status st;
-        // ---- U rows with per-level 32-byte alignment (u_layout)
+        // ---- U in device row order (u_rows), per-level 32-byte alignment (u_layout)
         const std::vector<int64_t> uoff = u_layout(g, sizeof(R));
-        {
-            std::vector<R> u((size_t)uoff.back() * g.Pc + 8, (R)0);
-            for (int l = 0; l <= g.D; ++l)
-                for (int64_t k = g.level_ptr[l]; k < g.level_ptr[l + 1]; ++k)
-                    for (int j = 0; j < g.Pc; ++j)
-                        u[(size_t)(uoff[l] + k - g.level_ptr[l]) * g.Pc + j] = (R)g.util_c[(size_t)k * g.Pc + j];
-            if ((st = up(plan.U, u))) return st;
-        }
         std::vector<int64_t> s_node_u, s_cb_u;
         u_rows(g, uoff, s_node_u, s_cb_u);
+        {
+            std::vector<R> u((size_t)uoff.back() * g.Pc + 8, (R)0);
+            for (int j = 0; j < g.Pc; ++j) u[j] = (R)g.util_c[j];   // the root (a one-node game)
+            const int Pc = g.Pc;
+#pragma omp parallel for schedule(static)
+            for (int64_t s = 0; s < g.NS; ++s)
+                for (int64_t a = 0; a < g.s_n[s]; ++a)
+                    for (int j = 0; j < Pc; ++j)
+                        u[(size_t)(s_cb_u[s] + a) * Pc + j] = (R)g.util_c[(size_t)(g.s_cb[s] + a) * Pc + j];
+            if ((st = up(plan.U, u))) return st;
+        }
+        // reach rows are indexed by slot: the forward pass walks each level in slot
+        // order (parent slot, incoming edge, parent actor per slot)
+        std::vector<int64_t> fs_parent(g.NS, -1), fs_e(g.NS, -1), fs_dec(g.NS);
+        std::vector<uint8_t> fs_pact(g.NS, 0);
+        {
+            std::vector<int64_t> sod(g.ND, -1);
+            for (int64_t s = 0; s < g.NS; ++s) sod[g.s_dec[s]] = s;
+#pragma omp parallel for schedule(static)
+            for (int64_t s = 0; s < g.NS; ++s) {
+                const int64_t d = g.s_dec[s];
+                fs_dec[s] = s;
+                fs_parent[s] = g.f_parent[d] < 0 ? -1 : sod[g.f_parent[d]];
+                fs_e[s] = g.f_e[d];
+                fs_pact[s] = g.f_pact[d];
+            }
+        }
         std::vector<int32_t> s_coff;
         std::vector<TileD> tiles;
         stage_tiles<R>(g, s_cb_u, tile_contrib_, tiles, s_coff);
@@ -1519,7 +1603,7 @@ struct Solver final : SolverBase {
                     for (int64_t s = th.s0; s < th.s1; ++s) {
                         node[s - th.s0] = (I)s_node_u[s];
                         cb[s - th.s0] = (I)s_cb_u[s];
-                        dec[s - th.s0] = (I)g.s_dec[s];
+                        dec[s - th.s0] = (I)s;   // reach row = slot
                     }
                     // segment of every slot and of every pair (no searches on the device)
                     unsigned char* sseg = reinterpret_cast<unsigned char*>(dec + (th.s1 - th.s0));
@@ -1550,15 +1634,15 @@ struct Solver final : SolverBase {
             sd.fused = sh.fused;
             segs[k] = sd;
         }
-        if ((st = up(plan.f_parent, narrow<I>(g.f_parent)))) return st;
-        if ((st = up(plan.f_e, narrow<I>(g.f_e)))) return st;
-        if ((st = up(plan.f_pact, g.f_pact))) return st;
+        if ((st = up(plan.f_parent, narrow<I>(fs_parent)))) return st;
+        if ((st = up(plan.f_e, narrow<I>(fs_e)))) return st;
+        if ((st = up(plan.f_pact, fs_pact))) return st;
         if ((st = up(plan.s_node, narrow<I>(s_node_u)))) return st;
         if ((st = up(plan.s_cb, narrow<I>(s_cb_u)))) return st;
         if ((st = up(plan.s_n, g.s_n))) return st;
         if ((st = up(plan.s_ebase, narrow<I>(g.s_ebase)))) return st;
         if ((st = up(plan.s_actor, g.s_actor))) return st;
-        if ((st = up(plan.s_dec, narrow<I>(g.s_dec)))) return st;
+        if ((st = up(plan.s_dec, narrow<I>(fs_dec)))) return st;
         if ((st = up(plan.s_coff, s_coff))) return st;
         if ((st = up(plan.qbase, narrow<I>(g.qbase_int)))) return st;
         if ((st = up(plan.owner, g.owner_int))) return st;
@@ -1568,10 +1652,25 @@ struct Solver final : SolverBase {
         if ((st = up(plan.deferred, narrow<I>(g.deferred_list)))) return st;
         if ((st = up(plan.dqbase, narrow<long long>(g.dqbase)))) return st;
         if (ncut() > 0) {
-            // cut rows are local canonical indices of depth `cut`: map to U rows
+            // cut rows are local canonical indices of depth-`cut` nodes (owned or
+            // not): their U row is inside their parent slot's child row
+            const int cut = sh->cut;
+            std::vector<std::pair<int64_t, int64_t>> cb_slot;   // (canonical first child, slot) of depth cut-1
+            if (cut >= 1)
+                for (int64_t s = g.slot_ptr[cut - 1]; s < g.slot_ptr[cut]; ++s) cb_slot.emplace_back(g.s_cb[s], s);
+            std::sort(cb_slot.begin(), cb_slot.end());
             std::vector<long long> rows(sh->cut_row.size());
-            for (size_t i = 0; i < rows.size(); ++i)
-                rows[i] = uoff[sh->cut] + (sh->cut_row[i] - g.level_ptr[sh->cut]);
+            for (size_t i = 0; i < rows.size(); ++i) {
+                const int64_t k = sh->cut_row[i];
+                if (cut == 0) { rows[i] = 0; continue; }
+                auto it = std::upper_bound(cb_slot.begin(), cb_slot.end(), std::make_pair(k, INT64_MAX));
+                if (it == cb_slot.begin() || k >= (it - 1)->first + g.s_n[(it - 1)->second]) {
+                    cfrb_set_error("internal: cut node without a parent slot");
+                    return CFR_ERR_INVALID_ARG;
+                }
+                --it;
+                rows[i] = s_cb_u[it->second] + (k - it->first);
+            }
             if ((st = up(plan.cutrow, rows))) return st;
             if ((st = up(plan.cutown, sh->cut_owned))) return st;
         }
@@ -1661,7 +1760,7 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         int64_t n = 0;
         for (int l = 1; l < g.D; ++l)
-            if (g.dec_ptr[l + 1] > g.dec_ptr[l]) ++n;
+            if (g.slot_ptr[l + 1] > g.slot_ptr[l]) ++n;
         for (int L = g.D - 1; L >= 0; --L)
             if (g.tile_ptr[L + 1] > g.tile_ptr[L]) ++n;
         if (!g.deferred_list.empty()) ++n;
@@ -1670,11 +1769,12 @@ struct Solver final : SolverBase {
 
     void fwd_level(cudaStream_t st, const R* sig, int l) {
         const Game& g = *gp;
-        const long long s0 = g.dec_ptr[l], s1 = g.dec_ptr[l + 1];
+        const long long s0 = g.slot_ptr[l], s1 = g.slot_ptr[l + 1];   // reach rows = slots
         if (s1 <= s0) return;
         const long long n = s1 - s0;
         const int threads = 256;
-        const long long blocks = std::min<long long>((n + threads - 1) / threads, 148LL * 16);
+        const long long per_block = (g.P == 2) ? threads * 4 : threads;
+        const long long blocks = std::min<long long>((n + per_block - 1) / per_block, 148LL * 16);
         if (g.P == 2)
             launch(pdl_, k_fwd<R, I, 2>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1);
         else
