@@ -116,7 +116,10 @@ typedef struct {
     int32_t flags;       /* bit 0: disable CUDA-Graph capture (debug);            */
                          /* bit 1: reserved; bit 2: disable the pipelined         */
                          /* (persistent) backward kernel; bit 3: disable          */
-                         /* programmatic dependent launch (A/B comparisons)       */
+                         /* programmatic dependent launch; bit 4: disable the     */
+                         /* streaming (TMA) backward kernel (A/B comparisons);    */
+                         /* bit 5: use the streaming kernel on every eligible     */
+                         /* level, however small (tests)                          */
     int32_t reserved;
 } cfr_solver_config;
 
@@ -124,6 +127,8 @@ typedef struct {
 #define CFR_FLAG_NO_PERSISTENT 2
 #define CFR_FLAG_NO_PIPELINE 4
 #define CFR_FLAG_NO_PDL 8
+#define CFR_FLAG_NO_STREAM 16
+#define CFR_FLAG_FORCE_STREAM 32
 
 /* Multi-GPU level sharding.  NULL or world_size == 1 means a
  * single GPU.  nccl_unique_id points to the 128-byte ncclUniqueId that rank 0
@@ -189,6 +194,11 @@ cfr_status cfr_solver_profile(cfr_solver* s, int64_t iterations, double* out_ms 
 /* Algorithmic DRAM bytes of one iteration by the DESIGN.md §6 model: out[0]
  * total, [1] forward, [2] backward, [3] update, [4] dominant backward level. */
 cfr_status cfr_solver_model_bytes(cfr_solver* s, double* out /* [5] */);
+/* Which backward kernel serves each parent level L = 0..D-1 of the CFR iteration:
+ * out[L] = 0 (no slots), 1 k_bwd (tile per CTA), 2 k_bwd_fast (pipelined
+ * cp.async), 3 k_bwd_stream (TMA bulk-copy ring).  `max_levels` bounds out[];
+ * *num_levels receives D. */
+cfr_status cfr_solver_level_kernels(cfr_solver* s, int32_t* out, int32_t max_levels, int32_t* num_levels);
 
 /* Writes a fresh ncclUniqueId (128 bytes) to `out` (rank 0 only). */
 cfr_status cfr_nccl_unique_id(void* out /* 128 bytes */);

@@ -30,7 +30,12 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 CFR, CFR_PLUS = 0, 1
+# cfr_solver_config.flags (include/cfr_b200.h)
 FLAG_NO_GRAPH = 1
+FLAG_NO_PIPELINE = 4
+FLAG_NO_PDL = 8
+FLAG_NO_STREAM = 16
+FLAG_FORCE_STREAM = 32
 
 
 def _ptr(a: np.ndarray) -> ctypes.c_void_p:
@@ -250,6 +255,15 @@ class Solver:
         _native.check(self._L.cfr_solver_shard_info(self._h, _ptr(out)))
         keys = ("cut", "n_cut", "owned_nodes", "local_nodes", "local_decision", "deferred", "deferred_pairs", "world")
         return {k: int(v) for k, v in zip(keys, out)}
+
+    KERNEL_NAMES = {0: None, 1: "k_bwd", 2: "k_bwd_fast", 3: "k_bwd_stream"}
+
+    def level_kernels(self) -> list:
+        """Backward kernel of each parent level (include/cfr_b200.h cfr_solver_level_kernels)."""
+        out = np.zeros(64, dtype=np.int32)
+        nl = ctypes.c_int32()
+        _native.check(self._L.cfr_solver_level_kernels(self._h, _ptr(out), 64, ctypes.byref(nl)))
+        return [self.KERNEL_NAMES[int(x)] for x in out[:min(nl.value, 64)]]
 
     def model_bytes(self) -> dict:
         out = np.zeros(5)

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -972,6 +973,357 @@ __global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, cons
     }
 }
 
+// ------------------------------------------------- streaming backward pass
+// k_bwd_stream (MODE_CFR) serves levels whose slots are all player nodes with one
+// |A(h)| = n and whose infosets are complete in the level (fused update).  In the
+// slot-ordered device layout (u_rows) a tile of whole infosets reads ONE
+// contiguous block from every stream: child rows, reach rows, sigma / R / S_num of
+// its (h, a) pairs, S_den / owner of its infosets and the infosets' member starts.
+// A producer warp moves the blocks with TMA bulk copies (cp.async.bulk, mbarrier
+// complete_tx) into an S-stage ring; eight consumer warps compute the tile: Eq 1
+// values (phase A), exact sums of the cancelled-form regret terms (Eq 7, matrix
+// form P:313) and of pi_hat (Eq 5) (phase B), and the fused update Eq 8/15 + Eq 10
+// + Eq 9 (phase C).  Every FP operation and its order is k_bwd's.
+struct StreamLevel {
+    long long s0;           // first slot of the level
+    long long h0, q0;       // first internal infoset of the level, qbase[h0]
+    long long row0;         // U row of the level's first child row
+    long long ntiles;
+    long long rec;          // int4 offset of the level's tile records {k0, k1, m0, m1} in the pool
+    long long hs;           // int offset of the level's infoset member starts hs[nh + 1] in the pool
+    int n, rowlen;          // |A(h)|, n * Pc
+    int maxm, maxseg;       // per-tile maxima (members, infosets)
+    int stages, stage_bytes;
+    int o_rows, o_reach, o_sig, o_reg, o_snum, o_sden, o_own, o_hs;   // byte offsets inside a stage
+    int o_sv, o_cm, o_rt, o_pos, o_pib, o_zs, o_ccnt, o_bar;          // work arrays / barriers
+    int bytes;              // dynamic shared memory
+    int last;
+};
+constexpr int kStreamConsumers = 256;   // 8 consumer warps
+constexpr int kStreamThreads = kStreamConsumers + 32;   // + 1 producer warp
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(void* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(void* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy of a 16-byte-aligned window; completes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, void* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kStreamConsumers) : "memory"); }
+
+// 16-byte window [lo, hi) around [p, p + bytes): returns lo, sets the window size
+// and the element offset of p inside it
+template <class T>
+__device__ __forceinline__ const unsigned char* window16(const T* p, long long count, unsigned* wbytes, int* off) {
+    const unsigned long long a = (unsigned long long)p;
+    const unsigned long long lo = a & ~15ull;
+    const unsigned long long hi = (a + (unsigned long long)count * sizeof(T) + 15ull) & ~15ull;
+    *wbytes = (unsigned)(hi - lo);
+    *off = (int)((a - lo) / sizeof(T));
+    return reinterpret_cast<const unsigned char*>(lo);
+}
+
+struct StreamHdr {
+    int k0, nseg, m0, M;        // first infoset (level-relative), infosets, first member, members
+    int po, ho, oo, hso;        // element offsets inside the windows: pairs, S_den, owner, hs
+};
+
+template <class R, class I, int PC>
+__global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, const int* __restrict__ pool,
+                                                                   StreamLevel L) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char* const B = smem_raw;
+    unsigned long long* const full = reinterpret_cast<unsigned long long*>(B + L.o_bar);
+    unsigned long long* const empty = full + L.stages;
+    const int tid = threadIdx.x;
+    const int P = g.P;
+    const int n = L.n;
+    pdl_trigger();
+    if (tid == 0) {
+        for (int s = 0; s < L.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    {
+        int* ccnt = reinterpret_cast<int*>(B + L.o_ccnt);
+        for (int k = tid; k < L.maxseg; k += blockDim.x) ccnt[k] = 0;
+    }
+    __syncthreads();
+    pdl_wait();
+    const long long G = gridDim.x;
+
+    if (tid >= kStreamConsumers) {
+        // ------------------------------------------------------------ producer
+        if (tid != kStreamConsumers) return;
+        const int4* recs = reinterpret_cast<const int4*>(pool) + L.rec;
+        const int* hs = pool + L.hs;
+        long long t = blockIdx.x;
+        int4 rec = (t < L.ntiles) ? recs[t] : make_int4(0, 0, 0, 0);
+        for (int it = 0; t < L.ntiles; ++it, t += G) {
+            const int4 cur = rec;
+            if (t + G < L.ntiles) rec = recs[t + G];    // next record in flight during the wait
+            const int st = it % L.stages;
+            if (it >= L.stages) mbar_wait(&empty[st], ((unsigned)(it / L.stages) - 1u) & 1u);
+            unsigned char* S = B + (size_t)st * L.stage_bytes;
+            const int k0 = cur.x, k1 = cur.y, m0 = cur.z, m1 = cur.w;
+            const int nseg = k1 - k0, M = m1 - m0;
+            const long long slot = L.s0 + m0;
+            const long long q = L.q0 + (long long)k0 * n;
+            const long long h = L.h0 + k0;
+            unsigned b_rows, b_reach, b_sig, b_reg, b_snum, b_sden, b_own, b_hs;
+            int o_rows, o_reach, po, po2, po3, ho, oo, hso;
+            const unsigned char* w_rows = window16(g.U + (L.row0 + (long long)m0 * n) * PC, (long long)M * L.rowlen, &b_rows, &o_rows);
+            const unsigned char* w_reach = window16(g.reach + slot * 2 * P, (long long)M * 2 * P, &b_reach, &o_reach);
+            const unsigned char* w_sig = window16(g.sig + q, (long long)nseg * n, &b_sig, &po);
+            const unsigned char* w_reg = window16(g.regret + q, (long long)nseg * n, &b_reg, &po2);
+            const unsigned char* w_snum = window16(g.snum + q, (long long)nseg * n, &b_snum, &po3);
+            const unsigned char* w_sden = window16(g.sden + h, nseg, &b_sden, &ho);
+            const unsigned char* w_own = window16(g.owner + h, nseg, &b_own, &oo);
+            const unsigned char* w_hs = window16(hs + k0, nseg + 1, &b_hs, &hso);
+            StreamHdr* hd = reinterpret_cast<StreamHdr*>(S);
+            hd->k0 = k0;
+            hd->nseg = nseg;
+            hd->m0 = m0;
+            hd->M = M;
+            hd->po = po;
+            hd->ho = ho;
+            hd->oo = oo;
+            hd->hso = hso;
+            (void)o_rows; (void)o_reach; (void)po2; (void)po3;   // rows / reach windows are aligned (host check)
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs);
+            bulk_g2s(S + L.o_rows, w_rows, b_rows, &full[st]);
+            bulk_g2s(S + L.o_reach, w_reach, b_reach, &full[st]);
+            bulk_g2s(S + L.o_sig, w_sig, b_sig, &full[st]);
+            bulk_g2s(S + L.o_reg, w_reg, b_reg, &full[st]);
+            bulk_g2s(S + L.o_snum, w_snum, b_snum, &full[st]);
+            bulk_g2s(S + L.o_sden, w_sden, b_sden, &full[st]);
+            bulk_g2s(S + L.o_own, w_own, b_own, &full[st]);
+            bulk_g2s(S + L.o_hs, w_hs, b_hs, &full[st]);
+        }
+        return;
+    }
+
+    // -------------------------------------------------------------- consumers
+    const int lane = tid & 31;
+    R* const sv = reinterpret_cast<R*>(B + L.o_sv);
+    short* const cm = reinterpret_cast<short*>(B + L.o_cm);
+    R* const rt = reinterpret_cast<R*>(B + L.o_rt);
+    R* const pos = reinterpret_cast<R*>(B + L.o_pos);
+    R* const pib = reinterpret_cast<R*>(B + L.o_pib);
+    R* const zs = reinterpret_cast<R*>(B + L.o_zs);
+    int* const ccnt = reinterpret_cast<int*>(B + L.o_ccnt);
+    const long long t_iter = g.ctrl[0] + 1;
+    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
+    bool bad = false;
+    long long t = blockIdx.x;
+    for (int it = 0; t < L.ntiles; ++it, t += G) {
+        const int st = it % L.stages;
+        unsigned char* S = B + (size_t)st * L.stage_bytes;
+        // node rows of this tile's members (constant metadata): in flight during the wait
+        const StreamHdr* hdp = reinterpret_cast<const StreamHdr*>(S);
+        mbar_wait(&full[st], (unsigned)(it / L.stages) & 1u);
+        const StreamHdr hd = *hdp;
+        const R* rows = reinterpret_cast<const R*>(S + L.o_rows);
+        const R* reach = reinterpret_cast<const R*>(S + L.o_reach);
+        const R* ssig = reinterpret_cast<const R*>(S + L.o_sig) + hd.po;
+        const R* sreg = reinterpret_cast<const R*>(S + L.o_reg) + hd.po;
+        const R* ssn = reinterpret_cast<const R*>(S + L.o_snum) + hd.po;
+        const R* sden = reinterpret_cast<const R*>(S + L.o_sden) + hd.ho;
+        const unsigned char* own = reinterpret_cast<const unsigned char*>(S + L.o_own) + hd.oo;
+        const int* hs = reinterpret_cast<const int*>(S + L.o_hs) + hd.hso;   // level-relative member starts
+        const int nseg = hd.nseg, M = hd.M, m0 = hd.m0;
+        const int npairs = nseg * n;
+
+        // ---- phase A: node values (Eq 1, ascending actions from +0); compaction of
+        // the members with nonzero pi_check (their regret terms are exact zeros)
+        for (int base = 0; base < M; base += kStreamConsumers) {
+            const int m = base + tid;
+            const bool active = m < M;
+            int k = 0;
+            R pc = (R)0;
+            if (active) {
+                const long long node = (long long)g.s_node[L.s0 + m0 + m];
+                int lo = 0, hi = nseg - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (hs[mid] - m0 <= m) lo = mid; else hi = mid - 1;
+                }
+                k = lo;
+                R v[PC];
+#pragma unroll
+                for (int j = 0; j < PC; ++j) v[j] = (R)0;
+                const R* row = rows + (long long)m * L.rowlen;
+                const R* sg = ssig + k * n;
+                for (int a = 0; a < n; ++a) {
+                    const R x = sg[a];
+#pragma unroll
+                    for (int j = 0; j < PC; ++j) v[j] = v[j] + x * row[a * PC + j];
+                }
+#pragma unroll
+                for (int j = 0; j < PC; ++j) {
+                    g.U[node * PC + j] = v[j];
+                    sv[m * PC + j] = v[j];
+                }
+                pc = reach[(long long)m * 2 * P + (own[k] - 1)];
+            }
+            const int key = active ? k : -1;
+            const unsigned grp = __match_any_sync(0xffffffffu, key);
+            const unsigned nz = __ballot_sync(0xffffffffu, active && pc != (R)0);
+            const unsigned mine = grp & nz;
+            const int leader = __ffs(grp) - 1;
+            int cbase = 0;
+            if (lane == leader && key >= 0 && mine) cbase = atomicAdd(&ccnt[k], __popc(mine));
+            cbase = __shfl_sync(0xffffffffu, cbase, leader);
+            if (active && pc != (R)0)
+                cm[(hs[k] - m0) + cbase + __popc(mine & ((1u << lane) - 1u))] = (short)m;
+        }
+        consumers_sync();
+
+        // ---- phase B: exact sums.  Items: every (h, a) pair (r~) then one pi_bar
+        // item per infoset, each split over ns adjacent lanes; partial slice sums
+        // are integer-valued doubles, combined exactly with shuffles.
+        {
+            const int nitems = npairs + nseg;
+            int ns = 1, lns = 0;
+            while (ns < 8 && nitems * ns * 2 <= kStreamConsumers) { ns <<= 1; ++lns; }
+            const int rounds = (nitems * ns + kStreamConsumers - 1) / kStreamConsumers;
+            for (int rd = 0; rd < rounds; ++rd) {
+                const int wi = rd * kStreamConsumers + tid;
+                const int itm = wi >> lns, part = wi & (ns - 1);
+                double c0 = 0, c1 = 0, c2 = 0;
+                const bool is_pair = itm < npairs;
+                int k = 0, a = 0;
+                if (is_pair) {
+                    k = itm / n;
+                    a = itm - k * n;
+                } else if (itm < nitems) {
+                    k = itm - npairs;
+                }
+                if (itm < nitems) {
+                    const int i = own[k];
+                    const int sb = hs[k] - m0;
+                    if (is_pair) {
+                        const int col = (PC == 1) ? 0 : i - 1;
+                        double e0 = 0, e1 = 0, e2 = 0;   // second independent slice chain (ILP)
+                        const short* mem = cm + sb;
+                        const int cnt = ccnt[k];
+                        int j = part;
+                        for (; j + ns < cnt; j += 2 * ns) {
+                            const int la = mem[j], lb = mem[j + ns];
+                            const R ua = rows[(long long)la * L.rowlen + a * PC + col];
+                            const R ub = rows[(long long)lb * L.rowlen + a * PC + col];
+                            const R ta = reach[(long long)la * 2 * P + (i - 1)] * (ua - sv[la * PC + col]);
+                            const R tb = reach[(long long)lb * 2 * P + (i - 1)] * (ub - sv[lb * PC + col]);
+                            xadd(c0, c1, c2, (double)ta, g.sc0);
+                            xadd(e0, e1, e2, (double)tb, g.sc0);
+                        }
+                        if (j < cnt) {
+                            const int la = mem[j];
+                            const R ua = rows[(long long)la * L.rowlen + a * PC + col];
+                            const R ta = reach[(long long)la * 2 * P + (i - 1)] * (ua - sv[la * PC + col]);
+                            xadd(c0, c1, c2, (double)ta, g.sc0);
+                        }
+                        c0 += e0;
+                        c1 += e1;
+                        c2 += e2;
+                        if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
+                    } else {
+                        const int se = hs[k + 1] - m0;
+                        for (int m = sb + part; m < se; m += ns)
+                            xadd(c0, c1, c2, (double)reach[(long long)m * 2 * P + P + (i - 1)], g.scp0);
+                    }
+                }
+                for (int o = 1; o < ns; o <<= 1) {
+                    c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+                    c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+                    c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+                }
+                if (itm < nitems && part == 0) {
+                    if (is_pair) rt[itm] = (R)xdec(c0, c1, c2, g.rc);
+                    else pib[k] = (R)xdec(c0, c1, c2, g.rcp);
+                }
+            }
+        }
+        consumers_sync();
+
+        // ---- phase C: fused update (Eq 8/15 or CFR+, Eq 10 numerator), then
+        // S_den and z, then regret matching (Eq 9)
+        const long long qt = L.q0 + (long long)hd.k0 * n;
+        const long long ht = L.h0 + hd.k0;
+        for (int p = tid; p < npairs; p += kStreamConsumers) {
+            const int k = p / n;
+            const R r_t = rt[p];
+            R r;
+            if (g.variant == 0) {
+                r = sreg[p] + r_t;
+            } else {
+                const R x = sreg[p] + r_t;
+                r = (x > (R)0) ? x : (R)0;
+                if (!finite_(x)) r = x;
+            }
+            g.regret[qt + p] = r;
+            const R wp = w * pib[k];
+            g.snum[qt + p] = ssn[p] + wp * ssig[p];
+            pos[p] = (r > (R)0) ? r : (R)0;
+        }
+        consumers_sync();
+        for (int k = tid; k < nseg; k += kStreamConsumers) {
+            g.sden[ht + k] = sden[k] + w * pib[k];
+            R z = (R)0;
+            for (int p = k * n; p < (k + 1) * n; ++p) z = z + pos[p];
+            zs[k] = z;
+            ccnt[k] = 0;   // compaction counters of the next tile
+        }
+        consumers_sync();
+        for (int p = tid; p < npairs; p += kStreamConsumers) {
+            const int k = p / n;
+            const R z = zs[k];
+            const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)n;
+            g.sig[qt + p] = nsig;
+            if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
+        }
+        consumers_sync();   // every read of this stage is done
+        if (tid == 0) mbar_arrive(&empty[st]);
+    }
+    if (bad) atomicMin(&g.ctrl[1], t_iter);
+    if (L.last) {
+        consumers_sync();
+        if (tid == 0) {
+            __threadfence();
+            const unsigned long long prev = atomicAdd((unsigned long long*)&g.ctrl[2], 1ULL);
+            if (prev == gridDim.x - 1) {
+                g.ctrl[0] = t_iter;
+                g.ctrl[2] = 0;
+            }
+        }
+    }
+}
+
 // Update of deferred infosets (span several depths / tiles): decode the global
 // exact sums, then the same Eq 8/15, Eq 10, Eq 9 steps; zero the accumulators.
 template <class R, class I>
@@ -1127,6 +1479,7 @@ struct SolverBase {
     virtual cfr_status launches(int64_t* n) = 0;
     virtual cfr_status profile(int64_t iters, double* out) = 0;
     virtual cfr_status model_bytes(double* out) = 0;
+    virtual cfr_status level_kernels(int32_t* out, int32_t max_levels, int32_t* num_levels) = 0;
     virtual cfr_status phase(int ph, double* out) = 0;
     virtual cfr_status exchange_size(int which, size_t* bytes) = 0;
     virtual cfr_status exchange(int which, int put, void* host, size_t bytes) = 0;
@@ -1284,6 +1637,112 @@ static std::vector<FastLevel> fast_levels(const Game& g, const std::vector<TileD
     return out;
 }
 
+// Shared-memory plan of k_bwd_stream for one level (stage ring + work arrays +
+// barriers).  Every block is 16-byte aligned; windows get 16 bytes of slack.
+static void stream_plan(StreamLevel& f, int P, int Pc, int w, int stages) {
+    auto al = [](long long x) { return (int)((x + 15) & ~15ll); };
+    const int maxpairs = f.maxm > 0 ? f.maxseg * f.n : 0;
+    int o = al(sizeof(StreamHdr));
+    f.o_rows = o; o += al((long long)f.maxm * f.rowlen * w + 16);
+    f.o_reach = o; o += al((long long)f.maxm * 2 * P * w + 16);
+    f.o_sig = o; o += al((long long)maxpairs * w + 16);
+    f.o_reg = o; o += al((long long)maxpairs * w + 16);
+    f.o_snum = o; o += al((long long)maxpairs * w + 16);
+    f.o_sden = o; o += al((long long)f.maxseg * w + 16);
+    f.o_own = o; o += al((long long)f.maxseg + 16);
+    f.o_hs = o; o += al((long long)(f.maxseg + 1) * 4 + 16);
+    f.stages = stages;
+    f.stage_bytes = o;
+    int x = stages * o;
+    f.o_sv = x; x += al((long long)f.maxm * Pc * w);
+    f.o_cm = x; x += al((long long)f.maxm * 2);
+    f.o_rt = x; x += al((long long)maxpairs * w);
+    f.o_pos = x; x += al((long long)maxpairs * w);
+    f.o_pib = x; x += al((long long)f.maxseg * w);
+    f.o_zs = x; x += al((long long)f.maxseg * w);
+    f.o_ccnt = x; x += al((long long)f.maxseg * 4);
+    f.o_bar = x; x += al(2 * stages * 8);
+    f.bytes = x;
+}
+
+// Levels served by k_bwd_stream: every slot a player node inside a fused segment,
+// consecutive internal infosets with one |A(h)|, <= kStreamConsumers members per
+// infoset, 16-byte rows.  Tiles pack whole infosets (<= kStreamConsumers members).
+// Appends the tile records (int4 {k0, k1, m0, m1}) and member starts to `pool`.
+template <class R>
+static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<int64_t>& cb_u, std::vector<int>* pool,
+                                              int min_tiles, int stages) {
+    const int w = (int)sizeof(R), P = g.P, Pc = g.Pc;
+    std::vector<StreamLevel> out(g.D, StreamLevel{});
+    for (int L = 0; L < g.D; ++L) {
+        StreamLevel f{};
+        const int64_t s0 = g.slot_ptr[L], s1 = g.slot_ptr[L + 1];
+        if (s1 <= s0) { out[L] = f; continue; }
+        bool ok = ((2 * P * w) % 16 == 0) && s1 < INT32_MAX;
+        std::vector<int> hs;
+        int64_t h_prev = -1, next = s0;
+        int n = -1;
+        for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1] && ok; ++t)
+            for (int k = g.tiles[t].seg0; k < g.tiles[t].seg1 && ok; ++k) {
+                const SegH& sg = g.segs[k];
+                const int nn = (int)(g.qbase_int[sg.h + 1] - g.qbase_int[sg.h]);
+                if (!sg.fused || sg.sb != next || (h_prev >= 0 && sg.h != h_prev + 1) || (n >= 0 && nn != n) ||
+                    sg.se - sg.sb > kStreamConsumers)
+                    ok = false;
+                n = nn;
+                hs.push_back((int)(sg.sb - s0));
+                h_prev = sg.h;
+                next = sg.se;
+            }
+        if (!ok || next != s1 || n <= 0) { out[L] = f; continue; }
+        const int64_t row0 = cb_u[s0];
+        if ((row0 * Pc * w) % 16 != 0 || ((int64_t)n * Pc * w) % 16 != 0) { out[L] = f; continue; }
+        for (int64_t s = s0; s < s1 && ok; ++s) ok = (cb_u[s] == row0 + (s - s0) * n);
+        if (!ok) { out[L] = f; continue; }
+        const int nh = (int)hs.size();
+        hs.push_back((int)(s1 - s0));
+        // tiles: greedy runs of whole infosets, <= kStreamConsumers members, <= 32 infosets
+        std::vector<int> tk = {0};
+        for (int k = 0; k < nh; ++k) {
+            const int k0 = tk.back();
+            if (k > k0 && (hs[k + 1] - hs[k0] > kStreamConsumers || k + 1 - k0 > 32)) tk.push_back(k);
+        }
+        tk.push_back(nh);
+        f.ntiles = (long long)tk.size() - 1;
+        if (f.ntiles < min_tiles) { out[L] = StreamLevel{}; continue; }
+        f.s0 = s0;
+        f.h0 = g.segs[g.tiles[g.tile_ptr[L]].seg0].h;
+        f.q0 = g.qbase_int[f.h0];
+        f.row0 = row0;
+        f.n = n;
+        f.rowlen = n * Pc;
+        for (long long t = 0; t < f.ntiles; ++t) {
+            f.maxm = std::max(f.maxm, hs[tk[t + 1]] - hs[tk[t]]);
+            f.maxseg = std::max(f.maxseg, tk[t + 1] - tk[t]);
+        }
+        if (pool) {
+            while (pool->size() % 4) pool->push_back(0);
+            f.rec = (long long)(pool->size() / 4);
+            for (long long t = 0; t < f.ntiles; ++t) {
+                pool->push_back(tk[t]);
+                pool->push_back(tk[t + 1]);
+                pool->push_back(hs[tk[t]]);
+                pool->push_back(hs[tk[t + 1]]);
+            }
+            f.hs = (long long)pool->size();
+            pool->insert(pool->end(), hs.begin(), hs.end());
+        }
+        stream_plan(f, P, Pc, w, stages);
+        out[L] = f;
+    }
+    if (pool) pool->resize(pool->size() + 8, 0);   // bulk-copy window slack
+    return out;
+}
+
+// ints of the stream tables: per level <= 4 (ntiles <= infosets) + 1 per infoset,
+// + per-level alignment / terminators and the window slack
+static size_t stream_pool_bound(const Game& g) { return (size_t)(5 * g.H + 10 * (int64_t)g.D + 64); }
+
 template <class R, class I>
 static size_t fast_pool_bytes(const Game& g, const ShardInfo* sh) {
     const std::vector<int64_t> uoff = u_layout(g, sizeof(R));
@@ -1304,7 +1763,7 @@ struct Plan {
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, ctrl, out;
-    size_t cutbuf, cutrow, cutown, report, pool;
+    size_t cutbuf, cutrow, cutown, report, pool, spool;
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
         Layout L;
@@ -1343,6 +1802,7 @@ struct Plan {
         cutown = L.take<unsigned char>(ncut + 1);
         report = L.take<unsigned char>(H + 1);
         pool = L.take<unsigned char>(fast_pool_bytes<R, I>(g, sh) + 16);
+        spool = L.take<int>(stream_pool_bound(g));
         total = L.off + 256;
     }
 };
@@ -1370,6 +1830,7 @@ struct Solver final : SolverBase {
     int64_t launches_per_iter = 0;
     bool use_graph = true;
     bool use_fast_ = true;
+    bool use_stream_ = true;
     bool pdl_ = true;
     int num_sms_ = 148;
     int world = 1, rank = 0;
@@ -1407,7 +1868,9 @@ struct Solver final : SolverBase {
     int contrib_of_tile(size_t t) const { return tile_contrib_.empty() ? 1 : (int)tile_contrib_[t]; }
     std::vector<SmemLayout> lay_;   // per parent level
     int max_smem_ = 0;
+    int max_smem_stream_ = 0;
     std::vector<FastLevel> fast_;   // per parent level: recsize > 0 -> pipelined kernel
+    std::vector<StreamLevel> stream_;   // per parent level: ntiles > 0 -> streaming (TMA) kernel
 
     SmemLayout make_layout(int maxch, int maxslot, int maxpairs, int maxseg) const {
         const int Pc = gp->Pc;
@@ -1490,6 +1953,7 @@ struct Solver final : SolverBase {
         }
         use_graph = !(cfg.flags & CFR_FLAG_NO_GRAPH);
         use_fast_ = !(cfg.flags & CFR_FLAG_NO_PIPELINE);
+        use_stream_ = !(cfg.flags & CFR_FLAG_NO_STREAM);
         pdl_ = !(cfg.flags & CFR_FLAG_NO_PDL);
         {
             int dev = 0;
@@ -1618,6 +2082,19 @@ struct Solver final : SolverBase {
             }
             if ((st = up(plan.pool, rec))) return st;
         }
+        {
+            // tables of the streaming levels
+            std::vector<int> sp;
+            int stages = 2;
+            if (const char* e = std::getenv("CFR_STREAM_STAGES")) stages = std::max(2, std::min(4, std::atoi(e)));
+            stream_ = stream_levels<R>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages);
+            if (sp.size() > stream_pool_bound(g)) {
+                cfrb_set_error("internal: stream table bound");
+                return CFR_ERR_INVALID_ARG;
+            }
+            if ((st = up(plan.spool, sp))) return st;
+            for (const StreamLevel& f : stream_) max_smem_stream_ = std::max(max_smem_stream_, f.bytes);
+        }
         std::vector<SegD> segs(g.segs.size());
         for (size_t k = 0; k < g.segs.size(); ++k) {
             const SegH& sh = g.segs[k];
@@ -1711,6 +2188,10 @@ struct Solver final : SolverBase {
             int dev = 0, optin = 0;
             CU(cudaGetDevice(&dev));
             CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            if (max_smem_stream_ > optin) {
+                for (StreamLevel& f : stream_) f.ntiles = 0;   // fall back to the tile kernels
+                max_smem_stream_ = 0;
+            }
             if (max_smem_ > optin) {
                 cfrb_set_error("tile shared-memory layout exceeds the device limit");
                 return CFR_ERR_UNSUPPORTED;
@@ -1741,6 +2222,8 @@ struct Solver final : SolverBase {
     e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_CFR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
     if (e) return e;                                                                                    \
     e = cudaFuncSetAttribute(k_bwd_fast<R, I, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);     \
+    if (e) return e;                                                                                    \
+    e = cudaFuncSetAttribute(k_bwd_stream<R, I, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);   \
     if (e) return e;                                                                                    \
     e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_VALUES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
     if (e) return e;                                                                                    \
@@ -1786,6 +2269,27 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         const long long t0 = g.tile_ptr[L], t1 = g.tile_ptr[L + 1];
         if (t1 <= t0) return;
+        if (MODE == MODE_CFR && sig == dg.sig && use_stream_ && stream_[L].ntiles > 0) {
+            StreamLevel f = stream_[L];
+            f.last = last;
+            int per_sm = 1;
+            switch (g.Pc) {
+                case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_stream<R, I, 1>, kStreamThreads, f.bytes); break;
+                case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_stream<R, I, 2>, kStreamThreads, f.bytes); break;
+                case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_stream<R, I, 3>, kStreamThreads, f.bytes); break;
+                default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_stream<R, I, 4>, kStreamThreads, f.bytes); break;
+            }
+            per_sm = std::max(1, per_sm);
+            const unsigned nb = (unsigned)std::min<long long>(f.ntiles, (long long)num_sms_ * per_sm);
+            const int* sp = at<int>(plan.spool);
+            switch (g.Pc) {
+                case 1: launch(pdl_, k_bwd_stream<R, I, 1>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
+                case 2: launch(pdl_, k_bwd_stream<R, I, 2>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
+                case 3: launch(pdl_, k_bwd_stream<R, I, 3>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
+                default: launch(pdl_, k_bwd_stream<R, I, 4>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
+            }
+            return;
+        }
         // pipelined kernel: measured faster for f64 only (f32 tiles move half the bytes)
         if (MODE == MODE_CFR && sizeof(R) == 8 && sig == dg.sig && use_fast_ && fast_[L].recsize > 0) {
             FastLevel f = fast_[L];
@@ -2215,6 +2719,20 @@ struct Solver final : SolverBase {
         return CFR_OK;
     }
 
+    int level_kernel(int L) const {
+        const Game& g = *gp;
+        if (g.tile_ptr[L + 1] <= g.tile_ptr[L]) return 0;
+        if (use_stream_ && stream_[L].ntiles > 0) return 3;
+        if (sizeof(R) == 8 && use_fast_ && fast_[L].recsize > 0) return 2;
+        return 1;
+    }
+    cfr_status level_kernels(int32_t* out, int32_t max_levels, int32_t* num_levels) override {
+        const Game& g = *gp;
+        *num_levels = g.D;
+        for (int L = 0; L < g.D && L < max_levels; ++L) out[L] = level_kernel(L);
+        return CFR_OK;
+    }
+
     // Algorithmic DRAM bytes per iteration (DESIGN.md §6 byte model).
     int dom_level = -1;   // set by profile(): the backward level with the largest time
     double level_bwd_bytes(int L) const {
@@ -2441,6 +2959,11 @@ cfr_status cfr_solver_model_bytes(cfr_solver* s, double* out) {
     CHK_S(s);
     if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
     return s->impl->model_bytes(out);
+}
+cfr_status cfr_solver_level_kernels(cfr_solver* s, int32_t* out, int32_t max_levels, int32_t* num_levels) {
+    CHK_S(s);
+    if (!num_levels || (max_levels > 0 && !out)) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->level_kernels(out, max_levels, num_levels);
 }
 cfr_status cfr_nccl_unique_id(void* out) {
     if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
