@@ -998,6 +998,7 @@ struct StreamLevel {
     int o_sv, o_cm, o_rt, o_pos, o_pib, o_zs, o_ccnt, o_bar;          // work arrays / barriers
     int bytes;              // dynamic shared memory
     int last;
+    int debug;              // timing experiments only: 1 consumers skip compute, 2 producer skips loads
 };
 constexpr int kStreamConsumers = 256;   // 8 consumer warps
 constexpr int kStreamThreads = kStreamConsumers + 32;   // + 1 producer warp
@@ -1070,7 +1071,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
     }
     {
         int* ccnt = reinterpret_cast<int*>(B + L.o_ccnt);
-        for (int k = tid; k < L.maxseg; k += blockDim.x) ccnt[k] = 0;
+        for (int k = tid; k < 2 * L.maxseg; k += blockDim.x) ccnt[k] = 0;
     }
     __syncthreads();
     pdl_wait();
@@ -1115,6 +1116,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
             hd->hso = hso;
             (void)o_rows; (void)o_reach; (void)po2; (void)po3;   // rows / reach windows are aligned (host check)
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            if (L.debug == 2) {   // timing experiment: no loads (consumers compute on stale data)
+                mbar_expect_tx(&full[st], 0);
+                continue;
+            }
             mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs);
             bulk_g2s(S + L.o_rows, w_rows, b_rows, &full[st]);
             bulk_g2s(S + L.o_reach, w_reach, b_reach, &full[st]);
@@ -1135,7 +1140,6 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
     R* const rt = reinterpret_cast<R*>(B + L.o_rt);
     R* const pos = reinterpret_cast<R*>(B + L.o_pos);
     R* const pib = reinterpret_cast<R*>(B + L.o_pib);
-    R* const zs = reinterpret_cast<R*>(B + L.o_zs);
     int* const ccnt = reinterpret_cast<int*>(B + L.o_ccnt);
     const long long t_iter = g.ctrl[0] + 1;
     const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
@@ -1158,14 +1162,20 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
         const int* hs = reinterpret_cast<const int*>(S + L.o_hs) + hd.hso;   // level-relative member starts
         const int nseg = hd.nseg, M = hd.M, m0 = hd.m0;
         const int npairs = nseg * n;
+        if (L.debug == 1) {   // timing experiment: data movement only
+            consumers_sync();
+            if (tid == 0) mbar_arrive(&empty[st]);
+            continue;
+        }
 
         // ---- phase A: node values (Eq 1, ascending actions from +0); compaction of
         // the members with nonzero pi_check (their regret terms are exact zeros)
+        // and of those with nonzero pi_hat (their pi_bar terms are exact zeros)
         for (int base = 0; base < M; base += kStreamConsumers) {
             const int m = base + tid;
             const bool active = m < M;
             int k = 0;
-            R pc = (R)0;
+            R pc = (R)0, ph = (R)0;
             if (active) {
                 const long long node = (long long)g.s_node[L.s0 + m0 + m];
                 int lo = 0, hi = nseg - 1;
@@ -1179,28 +1189,48 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
                 for (int j = 0; j < PC; ++j) v[j] = (R)0;
                 const R* row = rows + (long long)m * L.rowlen;
                 const R* sg = ssig + k * n;
-                for (int a = 0; a < n; ++a) {
-                    const R x = sg[a];
+                if (PC == 1) {
+                    // 16-byte row reads (rows are 16-byte multiples: host check)
+                    using V = typename std::conditional<sizeof(R) == 8, double2, float4>::type;
+                    constexpr int E = 16 / (int)sizeof(R);
+                    const V* row4 = reinterpret_cast<const V*>(row);
+                    for (int a = 0; a < n; a += E) {
+                        const V u = row4[a / E];
+                        const R* ue = reinterpret_cast<const R*>(&u);
 #pragma unroll
-                    for (int j = 0; j < PC; ++j) v[j] = v[j] + x * row[a * PC + j];
+                        for (int e = 0; e < E; ++e) v[0] = v[0] + sg[a + e] * ue[e];
+                    }
+                } else {
+                    for (int a = 0; a < n; ++a) {
+                        const R x = sg[a];
+#pragma unroll
+                        for (int j = 0; j < PC; ++j) v[j] = v[j] + x * row[a * PC + j];
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < PC; ++j) {
                     g.U[node * PC + j] = v[j];
                     sv[m * PC + j] = v[j];
                 }
-                pc = reach[(long long)m * 2 * P + (own[k] - 1)];
+                const int i = own[k];
+                pc = reach[(long long)m * 2 * P + (i - 1)];
+                ph = reach[(long long)m * 2 * P + P + (i - 1)];
             }
             const int key = active ? k : -1;
             const unsigned grp = __match_any_sync(0xffffffffu, key);
-            const unsigned nz = __ballot_sync(0xffffffffu, active && pc != (R)0);
-            const unsigned mine = grp & nz;
             const int leader = __ffs(grp) - 1;
-            int cbase = 0;
-            if (lane == leader && key >= 0 && mine) cbase = atomicAdd(&ccnt[k], __popc(mine));
-            cbase = __shfl_sync(0xffffffffu, cbase, leader);
-            if (active && pc != (R)0)
-                cm[(hs[k] - m0) + cbase + __popc(mine & ((1u << lane) - 1u))] = (short)m;
+            const unsigned lt = (1u << lane) - 1u;
+            const unsigned nzc = grp & __ballot_sync(0xffffffffu, active && pc != (R)0);
+            const unsigned nzh = grp & __ballot_sync(0xffffffffu, active && ph != (R)0);
+            int bc = 0, bh = 0;
+            if (lane == leader && key >= 0) {
+                if (nzc) bc = atomicAdd(&ccnt[k], __popc(nzc));
+                if (nzh) bh = atomicAdd(&ccnt[L.maxseg + k], __popc(nzh));
+            }
+            bc = __shfl_sync(0xffffffffu, bc, leader);
+            bh = __shfl_sync(0xffffffffu, bh, leader);
+            if (active && pc != (R)0) cm[(hs[k] - m0) + bc + __popc(nzc & lt)] = (short)m;
+            if (active && ph != (R)0) cm[L.maxm + (hs[k] - m0) + bh + __popc(nzh & lt)] = (short)m;
         }
         consumers_sync();
 
@@ -1253,9 +1283,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
                         c2 += e2;
                         if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
                     } else {
-                        const int se = hs[k + 1] - m0;
-                        for (int m = sb + part; m < se; m += ns)
-                            xadd(c0, c1, c2, (double)reach[(long long)m * 2 * P + P + (i - 1)], g.scp0);
+                        const short* mem = cm + L.maxm + sb;
+                        const int cnt = ccnt[L.maxseg + k];
+                        for (int j = part; j < cnt; j += ns)
+                            xadd(c0, c1, c2, (double)reach[(long long)mem[j] * 2 * P + P + (i - 1)], g.scp0);
                     }
                 }
                 for (int o = 1; o < ns; o <<= 1) {
@@ -1275,37 +1306,51 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
         // S_den and z, then regret matching (Eq 9)
         const long long qt = L.q0 + (long long)hd.k0 * n;
         const long long ht = L.h0 + hd.k0;
-        for (int p = tid; p < npairs; p += kStreamConsumers) {
-            const int k = p / n;
-            const R r_t = rt[p];
-            R r;
-            if (g.variant == 0) {
-                r = sreg[p] + r_t;
-            } else {
-                const R x = sreg[p] + r_t;
-                r = (x > (R)0) ? x : (R)0;
-                if (!finite_(x)) r = x;
+        {
+            // warp per infoset: lanes over its actions (chunks of 32); z summed in
+            // ascending action order by a shuffle chain (every lane holds it)
+            const int warp = tid >> 5;
+            for (int k = warp; k < nseg; k += kStreamConsumers / 32) {
+                const R wp = w * pib[k];
+                R z = (R)0;
+                for (int c = 0; c < n; c += 32) {
+                    const int a = c + lane;
+                    R pv = (R)0;
+                    if (a < n) {
+                        const int p = k * n + a;
+                        const R r_t = rt[p];
+                        R r;
+                        if (g.variant == 0) {
+                            r = sreg[p] + r_t;                   // Eq 8/15, cumulative (Q4)
+                        } else {
+                            const R x = sreg[p] + r_t;           // CFR+ (Q6)
+                            r = (x > (R)0) ? x : (R)0;
+                            if (!finite_(x)) r = x;
+                        }
+                        g.regret[qt + p] = r;
+                        g.snum[qt + p] = ssn[p] + wp * ssig[p];  // Eq 10 numerator
+                        pv = (r > (R)0) ? r : (R)0;
+                        pos[p] = pv;
+                    }
+                    (void)pv;
+                }
+                __syncwarp();
+                for (int b = 0; b < n; ++b) z = z + pos[k * n + b];   // broadcast reads, ascending
+                if (lane == 0) {
+                    g.sden[ht + k] = sden[k] + wp;               // Eq 10 denominator
+                    ccnt[k] = 0;                                 // compaction counters of the next tile
+                    ccnt[L.maxseg + k] = 0;
+                }
+                for (int c = 0; c < n; c += 32) {
+                    const int a = c + lane;
+                    if (a < n) {
+                        const int p = k * n + a;
+                        const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)n;   // Eq 9
+                        g.sig[qt + p] = nsig;
+                        if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
+                    }
+                }
             }
-            g.regret[qt + p] = r;
-            const R wp = w * pib[k];
-            g.snum[qt + p] = ssn[p] + wp * ssig[p];
-            pos[p] = (r > (R)0) ? r : (R)0;
-        }
-        consumers_sync();
-        for (int k = tid; k < nseg; k += kStreamConsumers) {
-            g.sden[ht + k] = sden[k] + w * pib[k];
-            R z = (R)0;
-            for (int p = k * n; p < (k + 1) * n; ++p) z = z + pos[p];
-            zs[k] = z;
-            ccnt[k] = 0;   // compaction counters of the next tile
-        }
-        consumers_sync();
-        for (int p = tid; p < npairs; p += kStreamConsumers) {
-            const int k = p / n;
-            const R z = zs[k];
-            const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)n;
-            g.sig[qt + p] = nsig;
-            if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
         }
         consumers_sync();   // every read of this stage is done
         if (tid == 0) mbar_arrive(&empty[st]);
@@ -1655,12 +1700,12 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int stages) {
     f.stage_bytes = o;
     int x = stages * o;
     f.o_sv = x; x += al((long long)f.maxm * Pc * w);
-    f.o_cm = x; x += al((long long)f.maxm * 2);
+    f.o_cm = x; x += al((long long)f.maxm * 4);          // two compaction lists (pi_check, pi_hat)
     f.o_rt = x; x += al((long long)maxpairs * w);
     f.o_pos = x; x += al((long long)maxpairs * w);
     f.o_pib = x; x += al((long long)f.maxseg * w);
     f.o_zs = x; x += al((long long)f.maxseg * w);
-    f.o_ccnt = x; x += al((long long)f.maxseg * 4);
+    f.o_ccnt = x; x += al((long long)f.maxseg * 8);
     f.o_bar = x; x += al(2 * stages * 8);
     f.bytes = x;
 }
@@ -1671,7 +1716,7 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int stages) {
 // Appends the tile records (int4 {k0, k1, m0, m1}) and member starts to `pool`.
 template <class R>
 static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<int64_t>& cb_u, std::vector<int>* pool,
-                                              int min_tiles, int stages) {
+                                              int min_tiles, int stages, int tile_target) {
     const int w = (int)sizeof(R), P = g.P, Pc = g.Pc;
     std::vector<StreamLevel> out(g.D, StreamLevel{});
     for (int L = 0; L < g.D; ++L) {
@@ -1687,7 +1732,7 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
                 const SegH& sg = g.segs[k];
                 const int nn = (int)(g.qbase_int[sg.h + 1] - g.qbase_int[sg.h]);
                 if (!sg.fused || sg.sb != next || (h_prev >= 0 && sg.h != h_prev + 1) || (n >= 0 && nn != n) ||
-                    sg.se - sg.sb > kStreamConsumers)
+                    sg.se - sg.sb > tile_target)
                     ok = false;
                 n = nn;
                 hs.push_back((int)(sg.sb - s0));
@@ -1705,7 +1750,7 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         std::vector<int> tk = {0};
         for (int k = 0; k < nh; ++k) {
             const int k0 = tk.back();
-            if (k > k0 && (hs[k + 1] - hs[k0] > kStreamConsumers || k + 1 - k0 > 32)) tk.push_back(k);
+            if (k > k0 && (hs[k + 1] - hs[k0] > tile_target || k + 1 - k0 > 32)) tk.push_back(k);
         }
         tk.push_back(nh);
         f.ntiles = (long long)tk.size() - 1;
@@ -1831,6 +1876,7 @@ struct Solver final : SolverBase {
     bool use_graph = true;
     bool use_fast_ = true;
     bool use_stream_ = true;
+    int stream_debug_ = 0;   // CFR_STREAM_DEBUG (timing experiments; results are garbage when set)
     bool pdl_ = true;
     int num_sms_ = 148;
     int world = 1, rank = 0;
@@ -2086,8 +2132,11 @@ struct Solver final : SolverBase {
             // tables of the streaming levels
             std::vector<int> sp;
             int stages = 2;
-            if (const char* e = std::getenv("CFR_STREAM_STAGES")) stages = std::max(2, std::min(4, std::atoi(e)));
-            stream_ = stream_levels<R>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages);
+            if (const char* e = std::getenv("CFR_STREAM_STAGES")) stages = std::max(2, std::min(8, std::atoi(e)));
+            if (const char* e = std::getenv("CFR_STREAM_DEBUG")) stream_debug_ = std::atoi(e);
+            int tile = kStreamConsumers;
+            if (const char* e = std::getenv("CFR_STREAM_TILE")) tile = std::max(32, std::min(1024, std::atoi(e)));
+            stream_ = stream_levels<R>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages, tile);
             if (sp.size() > stream_pool_bound(g)) {
                 cfrb_set_error("internal: stream table bound");
                 return CFR_ERR_INVALID_ARG;
@@ -2272,6 +2321,7 @@ struct Solver final : SolverBase {
         if (MODE == MODE_CFR && sig == dg.sig && use_stream_ && stream_[L].ntiles > 0) {
             StreamLevel f = stream_[L];
             f.last = last;
+            f.debug = stream_debug_;
             int per_sm = 1;
             switch (g.Pc) {
                 case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_stream<R, I, 1>, kStreamThreads, f.bytes); break;
