@@ -199,6 +199,12 @@ cfr_status cfr_solver_model_bytes(cfr_solver* s, double* out /* [5] */);
  * cp.async), 3 k_bwd_stream (TMA bulk-copy ring).  `max_levels` bounds out[];
  * *num_levels receives D. */
 cfr_status cfr_solver_level_kernels(cfr_solver* s, int32_t* out, int32_t max_levels, int32_t* num_levels);
+/* Cumulative work counters of the streaming backward levels since creation:
+ * out[0] infosets updated (live: some member with nonzero pi_check or pi_hat),
+ * out[1] their (h, a) pairs, out[2] infosets visited, out[3] pairs visited.  A dead
+ * infoset's update is the identity (every term an exact zero), so its writes are
+ * skipped; bench.py's byte model counts update writes of live infosets only. */
+cfr_status cfr_solver_counters(cfr_solver* s, int64_t* out /* [4] */);
 
 /* Writes a fresh ncclUniqueId (128 bytes) to `out` (rank 0 only). */
 cfr_status cfr_nccl_unique_id(void* out /* 128 bytes */);

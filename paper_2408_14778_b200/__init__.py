@@ -265,6 +265,12 @@ class Solver:
         _native.check(self._L.cfr_solver_level_kernels(self._h, _ptr(out), 64, ctypes.byref(nl)))
         return [self.KERNEL_NAMES[int(x)] for x in out[:min(nl.value, 64)]]
 
+    def counters(self) -> dict:
+        """Cumulative streaming-level work counters (include/cfr_b200.h cfr_solver_counters)."""
+        out = np.zeros(4, dtype=np.int64)
+        _native.check(self._L.cfr_solver_counters(self._h, _ptr(out)))
+        return dict(live_infosets=int(out[0]), live_pairs=int(out[1]), infosets=int(out[2]), pairs=int(out[3]))
+
     def model_bytes(self) -> dict:
         out = np.zeros(5)
         _native.check(self._L.cfr_solver_model_bytes(self._h, _ptr(out)))

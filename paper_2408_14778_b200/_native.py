@@ -53,17 +53,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> libcfr_b200.so (in-tree)."""
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, variant: str | None = None, defines=()) -> str:
+    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> libcfr_b200.so (in-tree).
+    `variant` + `defines` build an experiment copy libcfr_b200.<variant>.so."""
+    out = LIB_PATH if not variant else os.path.join(_HERE, f"libcfr_b200.{variant}.so")
+    if not variant and not force and not needs_build():
         return LIB_PATH
-    tmp = LIB_PATH + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, *SOURCES]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, out)
+    return out
 
 
 class NativeError(RuntimeError):
@@ -125,6 +127,7 @@ SIGNATURES = {
     "cfr_solver_profile": (ctypes.c_int, [_P, _I64, _P]),
     "cfr_solver_model_bytes": (ctypes.c_int, [_P, _P]),
     "cfr_solver_level_kernels": (ctypes.c_int, [_P, _P, _I32, _P]),
+    "cfr_solver_counters": (ctypes.c_int, [_P, _P]),
     "cfr_nccl_unique_id": (ctypes.c_int, [_P]),
     "cfr_solver_phase": (ctypes.c_int, [_P, _I32, _P]),
     "cfr_solver_exchange_size": (ctypes.c_int, [_P, _I32, _P]),
@@ -141,9 +144,13 @@ def load():
     global _lib
     with _lock:
         if _lib is None:
-            if needs_build():
+            path = LIB_PATH
+            alt = os.environ.get("CFR_B200_LIB_VARIANT")   # A/B kernel experiments: libcfr_b200.<variant>.so
+            if alt:
+                path = os.path.join(_HERE, f"libcfr_b200.{alt}.so")
+            elif needs_build():
                 build()
-            L = ctypes.CDLL(LIB_PATH)
+            L = ctypes.CDLL(path)
             for name, (res, args) in SIGNATURES.items():
                 f = getattr(L, name)
                 f.restype = res

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -157,7 +158,10 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
         // two players: 4-value rows (32 B) moved as two 16-byte vectors; FW rows
         // per thread with every load issued before the first use (the parent rows
         // are gathers: memory-level parallelism, not bandwidth, bounds this pass)
-        constexpr int FW = 4;
+#ifndef CFR_FWD_FW
+#define CFR_FWD_FW 4
+#endif
+        constexpr int FW = CFR_FWD_FW;
         using V2 = typename std::conditional<sizeof(R) == 8, double2, float2>::type;
         const long long n = d_end - d_begin;
         const long long chunk = (long long)blockDim.x * FW;
@@ -994,7 +998,9 @@ struct StreamLevel {
     int n, rowlen;          // |A(h)|, n * Pc
     int maxm, maxseg;       // per-tile maxima (members, infosets)
     int stages, stage_bytes;
-    int o_rows, o_reach, o_sig, o_reg, o_snum, o_sden, o_own, o_hs;   // byte offsets inside a stage
+    int o_rows, o_reach, o_sig, o_reg, o_snum, o_sden, o_own, o_hs, o_node;   // byte offsets inside a stage
+    unsigned ndiv_m;        // p / n == (p * ndiv_m) >> ndiv_s (64-bit) for p < 2^16 (host-verified)
+    int ndiv_s;
     int o_sv, o_cm, o_rt, o_pos, o_pib, o_zs, o_ccnt, o_bar;          // work arrays / barriers
     int bytes;              // dynamic shared memory
     int last;
@@ -1046,15 +1052,31 @@ __device__ __forceinline__ const unsigned char* window16(const T* p, long long c
     return reinterpret_cast<const unsigned char*>(lo);
 }
 
+#ifdef CFR_STREAM_PROFILE
+__device__ unsigned long long g_stream_prof[80];   // [warp][8] cycles, [64] tiles
+extern "C" int cfr_debug_stream_profile(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_stream_prof, sizeof(g_stream_prof));
+    if (reset) {
+        unsigned long long z[80] = {0};
+        cudaMemcpyToSymbol(g_stream_prof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 struct StreamHdr {
     int k0, nseg, m0, M;        // first infoset (level-relative), infosets, first member, members
     int po, ho, oo, hso;        // element offsets inside the windows: pairs, S_den, owner, hs
+    int no, pad0, pad1, pad2;   // node-row window offset
 };
 
+#ifndef CFR_STREAM_MINB
+#define CFR_STREAM_MINB 2
+#endif
 template <class R, class I, int PC>
-__global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, const int* __restrict__ pool,
+__global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(DG<R, I> g, const int* __restrict__ pool,
                                                                    StreamLevel L) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned char* const B = smem_raw;
     unsigned long long* const full = reinterpret_cast<unsigned long long*>(B + L.o_bar);
     unsigned long long* const empty = full + L.stages;
@@ -1084,19 +1106,20 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
         const int* hs = pool + L.hs;
         long long t = blockIdx.x;
         int4 rec = (t < L.ntiles) ? recs[t] : make_int4(0, 0, 0, 0);
+        int st = 0;
+        unsigned ph = 0;   // ring pass (parity of the empty barrier's phase to wait for)
         for (int it = 0; t < L.ntiles; ++it, t += G) {
             const int4 cur = rec;
             if (t + G < L.ntiles) rec = recs[t + G];    // next record in flight during the wait
-            const int st = it % L.stages;
-            if (it >= L.stages) mbar_wait(&empty[st], ((unsigned)(it / L.stages) - 1u) & 1u);
+            if (it >= L.stages) mbar_wait(&empty[st], (ph - 1u) & 1u);
             unsigned char* S = B + (size_t)st * L.stage_bytes;
             const int k0 = cur.x, k1 = cur.y, m0 = cur.z, m1 = cur.w;
             const int nseg = k1 - k0, M = m1 - m0;
             const long long slot = L.s0 + m0;
             const long long q = L.q0 + (long long)k0 * n;
             const long long h = L.h0 + k0;
-            unsigned b_rows, b_reach, b_sig, b_reg, b_snum, b_sden, b_own, b_hs;
-            int o_rows, o_reach, po, po2, po3, ho, oo, hso;
+            unsigned b_rows, b_reach, b_sig, b_reg, b_snum, b_sden, b_own, b_hs, b_node;
+            int o_rows, o_reach, po, po2, po3, ho, oo, hso, no;
             const unsigned char* w_rows = window16(g.U + (L.row0 + (long long)m0 * n) * PC, (long long)M * L.rowlen, &b_rows, &o_rows);
             const unsigned char* w_reach = window16(g.reach + slot * 2 * P, (long long)M * 2 * P, &b_reach, &o_reach);
             const unsigned char* w_sig = window16(g.sig + q, (long long)nseg * n, &b_sig, &po);
@@ -1105,6 +1128,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
             const unsigned char* w_sden = window16(g.sden + h, nseg, &b_sden, &ho);
             const unsigned char* w_own = window16(g.owner + h, nseg, &b_own, &oo);
             const unsigned char* w_hs = window16(hs + k0, nseg + 1, &b_hs, &hso);
+            const unsigned char* w_node = window16(g.s_node + slot, M, &b_node, &no);
             StreamHdr* hd = reinterpret_cast<StreamHdr*>(S);
             hd->k0 = k0;
             hd->nseg = nseg;
@@ -1114,13 +1138,16 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
             hd->ho = ho;
             hd->oo = oo;
             hd->hso = hso;
+            hd->no = no;
             (void)o_rows; (void)o_reach; (void)po2; (void)po3;   // rows / reach windows are aligned (host check)
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             if (L.debug == 2) {   // timing experiment: no loads (consumers compute on stale data)
                 mbar_expect_tx(&full[st], 0);
+                if (++st == L.stages) { st = 0; ++ph; }
                 continue;
             }
-            mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs);
+            mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs + b_node);
+            bulk_g2s(S + L.o_node, w_node, b_node, &full[st]);
             bulk_g2s(S + L.o_rows, w_rows, b_rows, &full[st]);
             bulk_g2s(S + L.o_reach, w_reach, b_reach, &full[st]);
             bulk_g2s(S + L.o_sig, w_sig, b_sig, &full[st]);
@@ -1129,12 +1156,31 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
             bulk_g2s(S + L.o_sden, w_sden, b_sden, &full[st]);
             bulk_g2s(S + L.o_own, w_own, b_own, &full[st]);
             bulk_g2s(S + L.o_hs, w_hs, b_hs, &full[st]);
+            if (++st == L.stages) { st = 0; ++ph; }
         }
         return;
     }
 
     // -------------------------------------------------------------- consumers
     const int lane = tid & 31;
+#ifdef CFR_STREAM_PROFILE
+    // timing experiment: per consumer warp, cycles between the marks below
+    unsigned long long sp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    auto sp_clock = []() {
+        long long c;
+        asm volatile("mov.u64 %0, %%clock64;\n" : "=l"(c)::"memory");
+        return c;
+    };
+    long long sp_last = sp_clock();
+#define SPROF(k)                                      \
+    do {                                              \
+        const long long now_ = sp_clock();            \
+        sp_acc[k] += (unsigned long long)(now_ - sp_last); \
+        sp_last = now_;                               \
+    } while (0)
+#else
+#define SPROF(k) do { } while (0)
+#endif
     R* const sv = reinterpret_cast<R*>(B + L.o_sv);
     short* const cm = reinterpret_cast<short*>(B + L.o_cm);
     R* const rt = reinterpret_cast<R*>(B + L.o_rt);
@@ -1144,13 +1190,15 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
     const long long t_iter = g.ctrl[0] + 1;
     const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
     bool bad = false;
+    const R inv_n = (R)1 / (R)n;   // uniform strategy of the level's infosets (Eq 9, z = 0)
+    unsigned long long live_h = 0, all_h = 0;   // updated / visited infosets (thread 0)
     long long t = blockIdx.x;
-    for (int it = 0; t < L.ntiles; ++it, t += G) {
-        const int st = it % L.stages;
+    int st = 0;
+    unsigned ph = 0;
+    for (; t < L.ntiles; t += G) {
         unsigned char* S = B + (size_t)st * L.stage_bytes;
-        // node rows of this tile's members (constant metadata): in flight during the wait
         const StreamHdr* hdp = reinterpret_cast<const StreamHdr*>(S);
-        mbar_wait(&full[st], (unsigned)(it / L.stages) & 1u);
+        SPROF(0); mbar_wait(&full[st], ph & 1u); SPROF(1);
         const StreamHdr hd = *hdp;
         const R* rows = reinterpret_cast<const R*>(S + L.o_rows);
         const R* reach = reinterpret_cast<const R*>(S + L.o_reach);
@@ -1160,11 +1208,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
         const R* sden = reinterpret_cast<const R*>(S + L.o_sden) + hd.ho;
         const unsigned char* own = reinterpret_cast<const unsigned char*>(S + L.o_own) + hd.oo;
         const int* hs = reinterpret_cast<const int*>(S + L.o_hs) + hd.hso;   // level-relative member starts
+        const I* snode = reinterpret_cast<const I*>(S + L.o_node) + hd.no;   // U rows of the members
         const int nseg = hd.nseg, M = hd.M, m0 = hd.m0;
         const int npairs = nseg * n;
         if (L.debug == 1) {   // timing experiment: data movement only
             consumers_sync();
             if (tid == 0) mbar_arrive(&empty[st]);
+            if (++st == L.stages) { st = 0; ++ph; }
             continue;
         }
 
@@ -1177,7 +1227,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
             int k = 0;
             R pc = (R)0, ph = (R)0;
             if (active) {
-                const long long node = (long long)g.s_node[L.s0 + m0 + m];
+                const long long node = (long long)snode[m];
                 int lo = 0, hi = nseg - 1;
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
@@ -1209,7 +1259,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
                 }
 #pragma unroll
                 for (int j = 0; j < PC; ++j) {
-                    g.U[node * PC + j] = v[j];
+                    if (!(L.debug & 4)) g.U[node * PC + j] = v[j];   // (debug bit 4: timing experiment)
                     sv[m * PC + j] = v[j];
                 }
                 const int i = own[k];
@@ -1232,7 +1282,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
             if (active && pc != (R)0) cm[(hs[k] - m0) + bc + __popc(nzc & lt)] = (short)m;
             if (active && ph != (R)0) cm[L.maxm + (hs[k] - m0) + bh + __popc(nzh & lt)] = (short)m;
         }
-        consumers_sync();
+        SPROF(2); consumers_sync(); SPROF(3);
 
         // ---- phase B: exact sums.  Items: every (h, a) pair (r~) then one pi_bar
         // item per infoset, each split over ns adjacent lanes; partial slice sums
@@ -1249,7 +1299,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
                 const bool is_pair = itm < npairs;
                 int k = 0, a = 0;
                 if (is_pair) {
-                    k = itm / n;
+                    k = (int)(((unsigned long long)(unsigned)itm * L.ndiv_m) >> L.ndiv_s);   // itm / n
                     a = itm - k * n;
                 } else if (itm < nitems) {
                     k = itm - npairs;
@@ -1300,22 +1350,32 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
                 }
             }
         }
-        consumers_sync();
+        SPROF(4); consumers_sync(); SPROF(5);
 
         // ---- phase C: fused update (Eq 8/15 or CFR+, Eq 10 numerator), then
         // S_den and z, then regret matching (Eq 9)
         const long long qt = L.q0 + (long long)hd.k0 * n;
         const long long ht = L.h0 + hd.k0;
         {
-            // warp per infoset: lanes over its actions (chunks of 32); z summed in
-            // ascending action order by a shuffle chain (every lane holds it)
+            // Live infosets: some member has a nonzero pi_check (r~ may be nonzero)
+            // or pi_hat (pi_bar may be nonzero).  For a dead infoset every term is an
+            // exact zero: r~ = +0 and pi_bar = +0, so R, S_num, S_den and sigma keep
+            // their bits and its update (and its writes) are skipped.  Live ones: a
+            // warp each, lanes over the actions (chunks of 32).
             const int warp = tid >> 5;
-            for (int k = warp; k < nseg; k += kStreamConsumers / 32) {
+            const unsigned live =
+                __ballot_sync(0xffffffffu, lane < nseg && (ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0));
+            if (tid == 0) {
+                live_h += __popc(live);
+                all_h += nseg;
+            }
+            int j = 0;
+            for (unsigned lm = live; lm; lm &= lm - 1u, ++j) {
+                if ((j & (kStreamConsumers / 32 - 1)) != warp) continue;
+                const int k = __ffs(lm) - 1;
                 const R wp = w * pib[k];
-                R z = (R)0;
                 for (int c = 0; c < n; c += 32) {
                     const int a = c + lane;
-                    R pv = (R)0;
                     if (a < n) {
                         const int p = k * n + a;
                         const R r_t = rt[p];
@@ -1327,17 +1387,20 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
                             r = (x > (R)0) ? x : (R)0;
                             if (!finite_(x)) r = x;
                         }
-                        g.regret[qt + p] = r;
-                        g.snum[qt + p] = ssn[p] + wp * ssig[p];  // Eq 10 numerator
-                        pv = (r > (R)0) ? r : (R)0;
-                        pos[p] = pv;
+                        if (!(L.debug & 8)) {   // (debug bit 8: timing experiment)
+                            g.regret[qt + p] = r;
+                            g.snum[qt + p] = ssn[p] + wp * ssig[p];  // Eq 10 numerator
+                        }
+                        pos[p] = (r > (R)0) ? r : (R)0;
                     }
-                    (void)pv;
                 }
                 __syncwarp();
-                for (int b = 0; b < n; ++b) z = z + pos[k * n + b];   // broadcast reads, ascending
+                R z = (R)0;
+                const R* pk = pos + k * n;
+#pragma unroll 4
+                for (int b = 0; b < n; ++b) z = z + pk[b];   // broadcast reads, ascending
                 if (lane == 0) {
-                    g.sden[ht + k] = sden[k] + wp;               // Eq 10 denominator
+                    if (!(L.debug & 8)) g.sden[ht + k] = sden[k] + wp;   // Eq 10 denominator
                     ccnt[k] = 0;                                 // compaction counters of the next tile
                     ccnt[L.maxseg + k] = 0;
                 }
@@ -1345,17 +1408,33 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_bwd_stream(DG<R, I> g, co
                     const int a = c + lane;
                     if (a < n) {
                         const int p = k * n + a;
-                        const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)n;   // Eq 9
-                        g.sig[qt + p] = nsig;
+                        const R nsig = (z > (R)0) ? pos[p] / z : inv_n;   // Eq 9
+                        if (!(L.debug & 8)) g.sig[qt + p] = nsig;
                         if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
                     }
                 }
             }
         }
-        consumers_sync();   // every read of this stage is done
+        SPROF(6); consumers_sync();   // every read of this stage is done
+        SPROF(7);
         if (tid == 0) mbar_arrive(&empty[st]);
+        if (++st == L.stages) { st = 0; ++ph; }
     }
+#ifdef CFR_STREAM_PROFILE
+    if (lane == 0)
+        for (int k = 0; k < 8; ++k) atomicAdd(&g_stream_prof[(tid >> 5) * 8 + k], sp_acc[k]);
+    if (tid == 0) atomicAdd(&g_stream_prof[64], (unsigned long long)((L.ntiles - blockIdx.x + G - 1) / G));
+#endif
+#undef SPROF
     if (bad) atomicMin(&g.ctrl[1], t_iter);
+    if (tid == 0) {
+        // cumulative: infosets updated / visited by the streaming levels (bench.py's
+        // byte model counts update writes of live infosets only)
+        atomicAdd((unsigned long long*)&g.ctrl[4], live_h);
+        atomicAdd((unsigned long long*)&g.ctrl[5], live_h * (unsigned long long)n);
+        atomicAdd((unsigned long long*)&g.ctrl[6], all_h);
+        atomicAdd((unsigned long long*)&g.ctrl[7], all_h * (unsigned long long)n);
+    }
     if (L.last) {
         consumers_sync();
         if (tid == 0) {
@@ -1525,6 +1604,7 @@ struct SolverBase {
     virtual cfr_status profile(int64_t iters, double* out) = 0;
     virtual cfr_status model_bytes(double* out) = 0;
     virtual cfr_status level_kernels(int32_t* out, int32_t max_levels, int32_t* num_levels) = 0;
+    virtual cfr_status counters(int64_t* out) = 0;
     virtual cfr_status phase(int ph, double* out) = 0;
     virtual cfr_status exchange_size(int which, size_t* bytes) = 0;
     virtual cfr_status exchange(int which, int put, void* host, size_t bytes) = 0;
@@ -1684,7 +1764,7 @@ static std::vector<FastLevel> fast_levels(const Game& g, const std::vector<TileD
 
 // Shared-memory plan of k_bwd_stream for one level (stage ring + work arrays +
 // barriers).  Every block is 16-byte aligned; windows get 16 bytes of slack.
-static void stream_plan(StreamLevel& f, int P, int Pc, int w, int stages) {
+static void stream_plan(StreamLevel& f, int P, int Pc, int w, int ix, int stages) {
     auto al = [](long long x) { return (int)((x + 15) & ~15ll); };
     const int maxpairs = f.maxm > 0 ? f.maxseg * f.n : 0;
     int o = al(sizeof(StreamHdr));
@@ -1696,6 +1776,7 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int stages) {
     f.o_sden = o; o += al((long long)f.maxseg * w + 16);
     f.o_own = o; o += al((long long)f.maxseg + 16);
     f.o_hs = o; o += al((long long)(f.maxseg + 1) * 4 + 16);
+    f.o_node = o; o += al((long long)f.maxm * ix + 16);
     f.stages = stages;
     f.stage_bytes = o;
     int x = stages * o;
@@ -1714,10 +1795,10 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int stages) {
 // consecutive internal infosets with one |A(h)|, <= kStreamConsumers members per
 // infoset, 16-byte rows.  Tiles pack whole infosets (<= kStreamConsumers members).
 // Appends the tile records (int4 {k0, k1, m0, m1}) and member starts to `pool`.
-template <class R>
+template <class R, class I>
 static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<int64_t>& cb_u, std::vector<int>* pool,
                                               int min_tiles, int stages, int tile_target) {
-    const int w = (int)sizeof(R), P = g.P, Pc = g.Pc;
+    const int w = (int)sizeof(R), P = g.P, Pc = g.Pc, ix = (int)sizeof(I);
     std::vector<StreamLevel> out(g.D, StreamLevel{});
     for (int L = 0; L < g.D; ++L) {
         StreamLevel f{};
@@ -1761,6 +1842,16 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         f.row0 = row0;
         f.n = n;
         f.rowlen = n * Pc;
+        {
+            // p / n by a 64-bit multiply and shift (round-up reciprocal), verified for p < 2^16
+            int l = 0;
+            while ((1 << l) < n) ++l;
+            f.ndiv_s = 16 + l;
+            f.ndiv_m = (unsigned)((((unsigned long long)1 << (16 + l)) + (unsigned long long)n - 1) / (unsigned long long)n);
+            for (unsigned x = 0; x < 65536u && ok; ++x)
+                ok = (unsigned)(((unsigned long long)x * f.ndiv_m) >> f.ndiv_s) == x / (unsigned)n;
+            if (!ok) { out[L] = StreamLevel{}; continue; }
+        }
         for (long long t = 0; t < f.ntiles; ++t) {
             f.maxm = std::max(f.maxm, hs[tk[t + 1]] - hs[tk[t]]);
             f.maxseg = std::max(f.maxseg, tk[t + 1] - tk[t]);
@@ -1777,7 +1868,8 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
             f.hs = (long long)pool->size();
             pool->insert(pool->end(), hs.begin(), hs.end());
         }
-        stream_plan(f, P, Pc, w, stages);
+        if ((int64_t)f.maxseg * n + f.maxseg >= 65536) { out[L] = StreamLevel{}; continue; }   // item ids < 2^16
+        stream_plan(f, P, Pc, w, ix, stages);
         out[L] = f;
     }
     if (pool) pool->resize(pool->size() + 8, 0);   // bulk-copy window slack
@@ -2136,7 +2228,7 @@ struct Solver final : SolverBase {
             if (const char* e = std::getenv("CFR_STREAM_DEBUG")) stream_debug_ = std::atoi(e);
             int tile = kStreamConsumers;
             if (const char* e = std::getenv("CFR_STREAM_TILE")) tile = std::max(32, std::min(1024, std::atoi(e)));
-            stream_ = stream_levels<R>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages, tile);
+            stream_ = stream_levels<R, I>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages, tile);
             if (sp.size() > stream_pool_bound(g)) {
                 cfrb_set_error("internal: stream table bound");
                 return CFR_ERR_INVALID_ARG;
@@ -2274,6 +2366,8 @@ struct Solver final : SolverBase {
     if (e) return e;                                                                                    \
     e = cudaFuncSetAttribute(k_bwd_stream<R, I, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);   \
     if (e) return e;                                                                                    \
+    e = cudaFuncSetAttribute(k_bwd_stream<R, I, PC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100); \
+    if (e) return e;                                                                                    \
     e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_VALUES>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
     if (e) return e;                                                                                    \
     e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
@@ -2305,7 +2399,7 @@ struct Solver final : SolverBase {
         if (s1 <= s0) return;
         const long long n = s1 - s0;
         const int threads = 256;
-        const long long per_block = (g.P == 2) ? threads * 4 : threads;
+        const long long per_block = (g.P == 2) ? threads * CFR_FWD_FW : threads;
         const long long blocks = std::min<long long>((n + per_block - 1) / per_block, 148LL * 16);
         if (g.P == 2)
             launch(pdl_, k_fwd<R, I, 2>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1);
@@ -2331,6 +2425,9 @@ struct Solver final : SolverBase {
             }
             per_sm = std::max(1, per_sm);
             const unsigned nb = (unsigned)std::min<long long>(f.ntiles, (long long)num_sms_ * per_sm);
+            if (std::getenv("CFR_STREAM_VERBOSE"))
+                std::fprintf(stderr, "[stream] level %d: %lld tiles, maxm %d, maxseg %d, smem %d B, %d CTA/SM, grid %u\n", L,
+                             f.ntiles, f.maxm, f.maxseg, f.bytes, per_sm, nb);
             const int* sp = at<int>(plan.spool);
             switch (g.Pc) {
                 case 1: launch(pdl_, k_bwd_stream<R, I, 1>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
@@ -2776,6 +2873,13 @@ struct Solver final : SolverBase {
         if (sizeof(R) == 8 && use_fast_ && fast_[L].recsize > 0) return 2;
         return 1;
     }
+    cfr_status counters(int64_t* out) override {
+        CU(cudaStreamSynchronize(stream));
+        long long c[4];
+        CU(cudaMemcpy(c, dg.ctrl + 4, sizeof(c), cudaMemcpyDeviceToHost));
+        for (int k = 0; k < 4; ++k) out[k] = c[k];
+        return CFR_OK;
+    }
     cfr_status level_kernels(int32_t* out, int32_t max_levels, int32_t* num_levels) override {
         const Game& g = *gp;
         *num_levels = g.D;
@@ -3014,6 +3118,11 @@ cfr_status cfr_solver_level_kernels(cfr_solver* s, int32_t* out, int32_t max_lev
     CHK_S(s);
     if (!num_levels || (max_levels > 0 && !out)) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
     return s->impl->level_kernels(out, max_levels, num_levels);
+}
+cfr_status cfr_solver_counters(cfr_solver* s, int64_t* out) {
+    CHK_S(s);
+    if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->counters(out);
 }
 cfr_status cfr_nccl_unique_id(void* out) {
     if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }

@@ -1,0 +1,36 @@
+"""Per-phase cycle split of k_bwd_stream (built with -DCFR_STREAM_PROFILE as the
+'sprof' library variant): cycles per consumer warp per tile, summed over the
+iteration's streaming levels."""
+import ctypes
+import os
+import sys
+
+os.environ["CFR_B200_LIB_VARIANT"] = "sprof"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+import gamegen
+import paper_2408_14778_b200 as pb
+from paper_2408_14778_b200 import _native
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+d = gamegen.synthetic(n_types=n)
+g = pb.Game(d)
+del d
+s = pb.Solver(g, variant="cfr+", precision=64)
+s.run(4)
+L = _native.load()
+f = L.cfr_debug_stream_profile
+f.argtypes = [ctypes.c_void_p, ctypes.c_int]
+buf = np.zeros(80, dtype=np.uint64)
+f(buf.ctypes.data, 1)
+s.run(1)
+f(buf.ctypes.data, 1)
+tiles = int(buf[64])
+names = ["loop", "wait_full", "A_work", "A_barrier", "B_work", "B_barrier", "C_work", "C_end_barrier"]
+per = buf[:64].reshape(8, 8).astype(np.float64) / tiles
+print(f"tiles {tiles}; cycles per tile, per consumer warp (rows) and mark (columns):")
+print("warp " + " ".join(f"{n:>13s}" for n in names))
+for w in range(8):
+    print(f"{w:4d} " + " ".join(f"{x:13.1f}" for x in per[w]))
+print("mean " + " ".join(f"{x:13.1f}" for x in per.mean(0)))

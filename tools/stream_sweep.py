@@ -37,7 +37,12 @@ for tile, stages, dbg in configs:
         prof = s.profile(3)
     except pb.NativeError:
         prof = {"dominant_level": -1, "dominant_ms": 0, "bwd_ms": 0, "fwd_ms": 0}
-    print(f"tile={tile:4d} stages={stages} debug={dbg}: {ms:.3f} ms/it ({1e3 / ms:.1f} it/s)  dominant L{prof['dominant_level']} "
+    try:
+        cnt = s.counters()
+        live = f"live {cnt['live_infosets'] / max(1, cnt['infosets']):.3f}"
+    except Exception:
+        live = ""
+    print(f"{live} tile={tile:4d} stages={stages} debug={dbg}: {ms:.3f} ms/it ({1e3 / ms:.1f} it/s)  dominant L{prof['dominant_level']} "
           f"{prof['dominant_ms']:.3f} ms  bwd {prof['bwd_ms']:.3f} fwd {prof['fwd_ms']:.3f}  kernels {s.level_kernels()}",
           flush=True)
     del s
