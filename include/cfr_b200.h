@@ -119,7 +119,9 @@ typedef struct {
                          /* programmatic dependent launch; bit 4: disable the     */
                          /* streaming (TMA) backward kernel (A/B comparisons);    */
                          /* bit 5: use the streaming kernel on every eligible     */
-                         /* level, however small (tests)                          */
+                         /* level, however small (tests); bit 6: fuse the         */
+                         /* deepest level's forward pass into its streaming       */
+                         /* backward kernel (experimental)                        */
     int32_t reserved;
 } cfr_solver_config;
 
@@ -129,6 +131,7 @@ typedef struct {
 #define CFR_FLAG_NO_PDL 8
 #define CFR_FLAG_NO_STREAM 16
 #define CFR_FLAG_FORCE_STREAM 32
+#define CFR_FLAG_FUSED_FORWARD 64
 
 /* Multi-GPU level sharding.  NULL or world_size == 1 means a
  * single GPU.  nccl_unique_id points to the 128-byte ncclUniqueId that rank 0

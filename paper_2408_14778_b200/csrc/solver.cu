@@ -70,7 +70,7 @@ struct DG {
     unsigned long long* acc_r;  // [ndef pairs][3] exact slices of the deferred infosets (compact)
     unsigned long long* acc_p;  // [ndef][3]; acc_r and acc_p are one contiguous exchange block
     const long long* dqbase;    // [ndef + 1] compact pair base of each deferred infoset
-    const I* f_parent;            // [ND] forward pass (canonical decision order)
+    const I* f_parent;            // [NS] slot order: parent slot, incoming sigma_ext edge, parent actor
     const I* f_e;
     const unsigned char* f_pact;
     const I* s_node;              // [NS] backward pass (slot order)
@@ -999,6 +999,8 @@ struct StreamLevel {
     int maxm, maxseg;       // per-tile maxima (members, infosets)
     int stages, stage_bytes;
     int o_rows, o_reach, o_sig, o_reg, o_snum, o_sden, o_own, o_hs, o_node;   // byte offsets inside a stage
+    int fused;              // 1: deepest decision level -- its forward pass (Eq 2 / Eq 4) is fused here
+    int o_pact, o_gsig;     // fused: parent actors, gathered incoming-edge sigma (reach area = parent rows)
     unsigned ndiv_m;        // p / n == (p * ndiv_m) >> ndiv_s (64-bit) for p < 2^16 (host-verified)
     int ndiv_s;
     int o_sv, o_cm, o_rt, o_pos, o_pib, o_zs, o_ccnt, o_bar;          // work arrays / barriers
@@ -1067,7 +1069,7 @@ extern "C" int cfr_debug_stream_profile(unsigned long long* out, int reset) {
 struct StreamHdr {
     int k0, nseg, m0, M;        // first infoset (level-relative), infosets, first member, members
     int po, ho, oo, hso;        // element offsets inside the windows: pairs, S_den, owner, hs
-    int no, pad0, pad1, pad2;   // node-row window offset
+    int no, pao, pad1, pad2;    // node-row / parent-actor window offsets
 };
 
 #ifndef CFR_STREAM_MINB
@@ -1086,7 +1088,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
     pdl_trigger();
     if (tid == 0) {
         for (int s = 0; s < L.stages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], L.fused ? 33 : 1);   // fused: + the producer lanes' cp.async arrivals
             mbar_init(&empty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1101,11 +1103,28 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
 
     if (tid >= kStreamConsumers) {
         // ------------------------------------------------------------ producer
-        if (tid != kStreamConsumers) return;
+        // Lane 0 arms the stage and issues the TMA bulk copies.  On the fused level
+        // all 32 lanes also gather each member's parent reach row and incoming-edge
+        // sigma (cp.async, completion counted on the same barrier); the parent /
+        // edge indices of the next tile are prefetched into registers meanwhile.
+        const int plane = tid - kStreamConsumers;
+        if (!L.fused && plane != 0) return;
         const int4* recs = reinterpret_cast<const int4*>(pool) + L.rec;
         const int* hs = pool + L.hs;
+        constexpr int GMAX = kStreamConsumers / 32;   // members per lane (maxm <= kStreamConsumers)
         long long t = blockIdx.x;
         int4 rec = (t < L.ntiles) ? recs[t] : make_int4(0, 0, 0, 0);
+        long long fp[GMAX], fe[GMAX];
+        auto prefetch = [&](const int4& r) {
+#pragma unroll
+            for (int q = 0; q < GMAX; ++q) {
+                const int m = q * 32 + plane;
+                const long long s = L.s0 + r.z + m;
+                fp[q] = (m < r.w - r.z) ? (long long)g.f_parent[s] : 0;
+                fe[q] = (m < r.w - r.z) ? (long long)g.f_e[s] : 0;
+            }
+        };
+        if (L.fused && t < L.ntiles) prefetch(rec);
         int st = 0;
         unsigned ph = 0;   // ring pass (parity of the empty barrier's phase to wait for)
         for (int it = 0; t < L.ntiles; ++it, t += G) {
@@ -1116,46 +1135,74 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
             const int k0 = cur.x, k1 = cur.y, m0 = cur.z, m1 = cur.w;
             const int nseg = k1 - k0, M = m1 - m0;
             const long long slot = L.s0 + m0;
-            const long long q = L.q0 + (long long)k0 * n;
-            const long long h = L.h0 + k0;
-            unsigned b_rows, b_reach, b_sig, b_reg, b_snum, b_sden, b_own, b_hs, b_node;
-            int o_rows, o_reach, po, po2, po3, ho, oo, hso, no;
-            const unsigned char* w_rows = window16(g.U + (L.row0 + (long long)m0 * n) * PC, (long long)M * L.rowlen, &b_rows, &o_rows);
-            const unsigned char* w_reach = window16(g.reach + slot * 2 * P, (long long)M * 2 * P, &b_reach, &o_reach);
-            const unsigned char* w_sig = window16(g.sig + q, (long long)nseg * n, &b_sig, &po);
-            const unsigned char* w_reg = window16(g.regret + q, (long long)nseg * n, &b_reg, &po2);
-            const unsigned char* w_snum = window16(g.snum + q, (long long)nseg * n, &b_snum, &po3);
-            const unsigned char* w_sden = window16(g.sden + h, nseg, &b_sden, &ho);
-            const unsigned char* w_own = window16(g.owner + h, nseg, &b_own, &oo);
-            const unsigned char* w_hs = window16(hs + k0, nseg + 1, &b_hs, &hso);
-            const unsigned char* w_node = window16(g.s_node + slot, M, &b_node, &no);
-            StreamHdr* hd = reinterpret_cast<StreamHdr*>(S);
-            hd->k0 = k0;
-            hd->nseg = nseg;
-            hd->m0 = m0;
-            hd->M = M;
-            hd->po = po;
-            hd->ho = ho;
-            hd->oo = oo;
-            hd->hso = hso;
-            hd->no = no;
-            (void)o_rows; (void)o_reach; (void)po2; (void)po3;   // rows / reach windows are aligned (host check)
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            if (L.debug == 2) {   // timing experiment: no loads (consumers compute on stale data)
-                mbar_expect_tx(&full[st], 0);
-                if (++st == L.stages) { st = 0; ++ph; }
-                continue;
+            if (plane == 0) {
+                const long long q = L.q0 + (long long)k0 * n;
+                const long long h = L.h0 + k0;
+                unsigned b_rows, b_reach = 0, b_sig, b_reg, b_snum, b_sden, b_own, b_hs, b_node, b_pact = 0;
+                int o_rows, o_reach = 0, po, po2, po3, ho, oo, hso, no, pao = 0;
+                const unsigned char* w_rows = window16(g.U + (L.row0 + (long long)m0 * n) * PC, (long long)M * L.rowlen, &b_rows, &o_rows);
+                const unsigned char* w_reach = nullptr;
+                const unsigned char* w_pact = nullptr;
+                if (L.fused) w_pact = window16(g.f_pact + slot, M, &b_pact, &pao);
+                else w_reach = window16(g.reach + slot * 2 * P, (long long)M * 2 * P, &b_reach, &o_reach);
+                const unsigned char* w_sig = window16(g.sig + q, (long long)nseg * n, &b_sig, &po);
+                const unsigned char* w_reg = window16(g.regret + q, (long long)nseg * n, &b_reg, &po2);
+                const unsigned char* w_snum = window16(g.snum + q, (long long)nseg * n, &b_snum, &po3);
+                const unsigned char* w_sden = window16(g.sden + h, nseg, &b_sden, &ho);
+                const unsigned char* w_own = window16(g.owner + h, nseg, &b_own, &oo);
+                const unsigned char* w_hs = window16(hs + k0, nseg + 1, &b_hs, &hso);
+                const unsigned char* w_node = window16(g.s_node + slot, M, &b_node, &no);
+                StreamHdr* hd = reinterpret_cast<StreamHdr*>(S);
+                hd->k0 = k0;
+                hd->nseg = nseg;
+                hd->m0 = m0;
+                hd->M = M;
+                hd->po = po;
+                hd->ho = ho;
+                hd->oo = oo;
+                hd->hso = hso;
+                hd->no = no;
+                hd->pao = pao;
+                (void)o_rows; (void)o_reach; (void)po2; (void)po3;   // rows / reach windows are aligned (host check)
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                if (L.debug == 2) {   // timing experiment: no loads (consumers compute on stale data)
+                    mbar_expect_tx(&full[st], 0);
+                } else {
+                    mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs + b_node + b_pact);
+                    bulk_g2s(S + L.o_node, w_node, b_node, &full[st]);
+                    bulk_g2s(S + L.o_rows, w_rows, b_rows, &full[st]);
+                    if (L.fused) bulk_g2s(S + L.o_pact, w_pact, b_pact, &full[st]);
+                    else bulk_g2s(S + L.o_reach, w_reach, b_reach, &full[st]);
+                    bulk_g2s(S + L.o_sig, w_sig, b_sig, &full[st]);
+                    bulk_g2s(S + L.o_reg, w_reg, b_reg, &full[st]);
+                    bulk_g2s(S + L.o_snum, w_snum, b_snum, &full[st]);
+                    bulk_g2s(S + L.o_sden, w_sden, b_sden, &full[st]);
+                    bulk_g2s(S + L.o_own, w_own, b_own, &full[st]);
+                    bulk_g2s(S + L.o_hs, w_hs, b_hs, &full[st]);
+                }
             }
-            mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs + b_node);
-            bulk_g2s(S + L.o_node, w_node, b_node, &full[st]);
-            bulk_g2s(S + L.o_rows, w_rows, b_rows, &full[st]);
-            bulk_g2s(S + L.o_reach, w_reach, b_reach, &full[st]);
-            bulk_g2s(S + L.o_sig, w_sig, b_sig, &full[st]);
-            bulk_g2s(S + L.o_reg, w_reg, b_reg, &full[st]);
-            bulk_g2s(S + L.o_snum, w_snum, b_snum, &full[st]);
-            bulk_g2s(S + L.o_sden, w_sden, b_sden, &full[st]);
-            bulk_g2s(S + L.o_own, w_own, b_own, &full[st]);
-            bulk_g2s(S + L.o_hs, w_hs, b_hs, &full[st]);
+            if (L.fused) {
+                // gathers: parent reach row (2P values, 16-byte pieces) and sigma of
+                // the incoming edge, per member, into the stage
+                constexpr int RB = 2 * 2 * (int)sizeof(R);   // P = 2 fast path is the common case
+                R* prow = reinterpret_cast<R*>(S + L.o_reach);
+                R* gsig = reinterpret_cast<R*>(S + L.o_gsig);
+                const int rowb = 2 * P * (int)sizeof(R);
+                (void)RB;
+#pragma unroll
+                for (int q = 0; q < GMAX; ++q) {
+                    const int m = q * 32 + plane;
+                    if (m < M) {
+                        const unsigned char* src = reinterpret_cast<const unsigned char*>(g.reach + fp[q] * 2 * P);
+                        unsigned char* dst = reinterpret_cast<unsigned char*>(prow + (long long)m * 2 * P);
+                        for (int c = 0; c < rowb; c += 16) cp_async<16>(dst + c, src + c);
+                        cp_async<(int)sizeof(R)>(gsig + m, g.sig + fe[q]);
+                    }
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[st]))
+                             : "memory");
+                if (t + G < L.ntiles) prefetch(rec);
+            }
             if (++st == L.stages) { st = 0; ++ph; }
         }
         return;
@@ -1209,8 +1256,10 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         const unsigned char* own = reinterpret_cast<const unsigned char*>(S + L.o_own) + hd.oo;
         const int* hs = reinterpret_cast<const int*>(S + L.o_hs) + hd.hso;   // level-relative member starts
         const I* snode = reinterpret_cast<const I*>(S + L.o_node) + hd.no;   // U rows of the members
+        const unsigned char* pact = reinterpret_cast<const unsigned char*>(S + L.o_pact) + hd.pao;   // fused only
+        const R* gsig = reinterpret_cast<const R*>(S + L.o_gsig);                                  // fused only
         const int nseg = hd.nseg, M = hd.M, m0 = hd.m0;
-        const int npairs = nseg * n;
+
         if (L.debug == 1) {   // timing experiment: data movement only
             consumers_sync();
             if (tid == 0) mbar_arrive(&empty[st]);
@@ -1239,7 +1288,8 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 for (int j = 0; j < PC; ++j) v[j] = (R)0;
                 const R* row = rows + (long long)m * L.rowlen;
                 const R* sg = ssig + k * n;
-                if (PC == 1) {
+                if (L.debug & 16) {   // timing experiment: no value loop
+                } else if (PC == 1) {
                     // 16-byte row reads (rows are 16-byte multiples: host check)
                     using V = typename std::conditional<sizeof(R) == 8, double2, float4>::type;
                     constexpr int E = 16 / (int)sizeof(R);
@@ -1263,9 +1313,24 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                     sv[m * PC + j] = v[j];
                 }
                 const int i = own[k];
-                pc = reach[(long long)m * 2 * P + (i - 1)];
-                ph = reach[(long long)m * 2 * P + P + (i - 1)];
+                if (L.fused) {
+                    // forward pass of this member (Eq 2 pi_check and Eq 4 pi_hat, reading
+                    // Q1; the k_fwd arithmetic) from its gathered parent row and edge
+                    // sigma; the actor's two factors replace the parent row in place
+                    R* prow = const_cast<R*>(reach) + (long long)m * 2 * P;
+                    const R x = gsig[m];
+                    const int act = pact[m];
+                    const R pcp = prow[i - 1], php = prow[P + i - 1];
+                    pc = (act != i) ? pcp * x : pcp;
+                    ph = (act == i) ? php * x : php;
+                    prow[0] = pc;
+                    prow[1] = ph;
+                } else {
+                    pc = reach[(long long)m * 2 * P + (i - 1)];
+                    ph = reach[(long long)m * 2 * P + P + (i - 1)];
+                }
             }
+            if (L.debug & 32) continue;   // timing experiment: no compaction
             const int key = active ? k : -1;
             const unsigned grp = __match_any_sync(0xffffffffu, key);
             const int leader = __ffs(grp) - 1;
@@ -1284,84 +1349,14 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         }
         SPROF(2); consumers_sync(); SPROF(3);
 
-        // ---- phase B: exact sums.  Items: every (h, a) pair (r~) then one pi_bar
-        // item per infoset, each split over ns adjacent lanes; partial slice sums
-        // are integer-valued doubles, combined exactly with shuffles.
-        {
-            const int nitems = npairs + nseg;
-            int ns = 1, lns = 0;
-            while (ns < 8 && nitems * ns * 2 <= kStreamConsumers) { ns <<= 1; ++lns; }
-            const int rounds = (nitems * ns + kStreamConsumers - 1) / kStreamConsumers;
-            for (int rd = 0; rd < rounds; ++rd) {
-                const int wi = rd * kStreamConsumers + tid;
-                const int itm = wi >> lns, part = wi & (ns - 1);
-                double c0 = 0, c1 = 0, c2 = 0;
-                const bool is_pair = itm < npairs;
-                int k = 0, a = 0;
-                if (is_pair) {
-                    k = (int)(((unsigned long long)(unsigned)itm * L.ndiv_m) >> L.ndiv_s);   // itm / n
-                    a = itm - k * n;
-                } else if (itm < nitems) {
-                    k = itm - npairs;
-                }
-                if (itm < nitems) {
-                    const int i = own[k];
-                    const int sb = hs[k] - m0;
-                    if (is_pair) {
-                        const int col = (PC == 1) ? 0 : i - 1;
-                        double e0 = 0, e1 = 0, e2 = 0;   // second independent slice chain (ILP)
-                        const short* mem = cm + sb;
-                        const int cnt = ccnt[k];
-                        int j = part;
-                        for (; j + ns < cnt; j += 2 * ns) {
-                            const int la = mem[j], lb = mem[j + ns];
-                            const R ua = rows[(long long)la * L.rowlen + a * PC + col];
-                            const R ub = rows[(long long)lb * L.rowlen + a * PC + col];
-                            const R ta = reach[(long long)la * 2 * P + (i - 1)] * (ua - sv[la * PC + col]);
-                            const R tb = reach[(long long)lb * 2 * P + (i - 1)] * (ub - sv[lb * PC + col]);
-                            xadd(c0, c1, c2, (double)ta, g.sc0);
-                            xadd(e0, e1, e2, (double)tb, g.sc0);
-                        }
-                        if (j < cnt) {
-                            const int la = mem[j];
-                            const R ua = rows[(long long)la * L.rowlen + a * PC + col];
-                            const R ta = reach[(long long)la * 2 * P + (i - 1)] * (ua - sv[la * PC + col]);
-                            xadd(c0, c1, c2, (double)ta, g.sc0);
-                        }
-                        c0 += e0;
-                        c1 += e1;
-                        c2 += e2;
-                        if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
-                    } else {
-                        const short* mem = cm + L.maxm + sb;
-                        const int cnt = ccnt[L.maxseg + k];
-                        for (int j = part; j < cnt; j += ns)
-                            xadd(c0, c1, c2, (double)reach[(long long)mem[j] * 2 * P + P + (i - 1)], g.scp0);
-                    }
-                }
-                for (int o = 1; o < ns; o <<= 1) {
-                    c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-                    c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-                    c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-                }
-                if (itm < nitems && part == 0) {
-                    if (is_pair) rt[itm] = (R)xdec(c0, c1, c2, g.rc);
-                    else pib[k] = (R)xdec(c0, c1, c2, g.rcp);
-                }
-            }
-        }
-        SPROF(4); consumers_sync(); SPROF(5);
-
-        // ---- phase C: fused update (Eq 8/15 or CFR+, Eq 10 numerator), then
-        // S_den and z, then regret matching (Eq 9)
+        // ---- phases B + C, a warp per LIVE infoset (no CTA barrier in between).
+        // Live: some member has a nonzero pi_check (r~ may be nonzero) or pi_hat
+        // (pi_bar may be nonzero).  For a dead infoset every term is an exact zero:
+        // r~ = +0 and pi_bar = +0, so R, S_num, S_den and sigma keep their bits and
+        // its update (and its writes) are skipped.
         const long long qt = L.q0 + (long long)hd.k0 * n;
         const long long ht = L.h0 + hd.k0;
         {
-            // Live infosets: some member has a nonzero pi_check (r~ may be nonzero)
-            // or pi_hat (pi_bar may be nonzero).  For a dead infoset every term is an
-            // exact zero: r~ = +0 and pi_bar = +0, so R, S_num, S_den and sigma keep
-            // their bits and its update (and its writes) are skipped.  Live ones: a
-            // warp each, lanes over the actions (chunks of 32).
             const int warp = tid >> 5;
             const unsigned live =
                 __ballot_sync(0xffffffffu, lane < nseg && (ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0));
@@ -1369,10 +1364,65 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 live_h += __popc(live);
                 all_h += nseg;
             }
+            // phase B items of one infoset: n pairs (r~) + 1 pi_bar, ns lanes each
+            int ns = 1, lns = 0;
+            while (ns < 32 && (n + 1) * ns * 2 <= 32) { ns <<= 1; ++lns; }
+            const int ipr = 32 >> lns;   // items per round
             int j = 0;
             for (unsigned lm = live; lm; lm &= lm - 1u, ++j) {
                 if ((j & (kStreamConsumers / 32 - 1)) != warp) continue;
                 const int k = __ffs(lm) - 1;
+                const int i = own[k];
+                const int col = (PC == 1) ? 0 : i - 1;
+                const int sb = hs[k] - m0;
+                const int cntc = ccnt[k], cnth = ccnt[L.maxseg + k];
+                const int oc = L.fused ? 0 : i - 1, oh = L.fused ? 1 : P + i - 1;   // pi_check / pi_hat in a reach row
+                const short* memc = cm + sb;
+                const short* memh = cm + L.maxm + sb;
+                // ---- phase B: exact sums (slices of integer-valued doubles combine
+                // exactly in any order)
+                for (int base = 0; base <= n; base += ipr) {
+                    const int itm = base + (lane >> lns), part = lane & (ns - 1);
+                    double c0 = 0, c1 = 0, c2 = 0;
+                    if (itm < n) {
+                        const int a = itm;
+                        double e0 = 0, e1 = 0, e2 = 0;   // second independent slice chain (ILP)
+                        int jj = part;
+                        for (; jj + ns < cntc; jj += 2 * ns) {
+                            const int la = memc[jj], lb = memc[jj + ns];
+                            const R ua = rows[(long long)la * L.rowlen + a * PC + col];
+                            const R ub = rows[(long long)lb * L.rowlen + a * PC + col];
+                            const R ta = reach[(long long)la * 2 * P + oc] * (ua - sv[la * PC + col]);
+                            const R tb = reach[(long long)lb * 2 * P + oc] * (ub - sv[lb * PC + col]);
+                            xadd(c0, c1, c2, (double)ta, g.sc0);
+                            xadd(e0, e1, e2, (double)tb, g.sc0);
+                        }
+                        if (jj < cntc) {
+                            const int la = memc[jj];
+                            const R ua = rows[(long long)la * L.rowlen + a * PC + col];
+                            const R ta = reach[(long long)la * 2 * P + oc] * (ua - sv[la * PC + col]);
+                            xadd(c0, c1, c2, (double)ta, g.sc0);
+                        }
+                        c0 += e0;
+                        c1 += e1;
+                        c2 += e2;
+                        if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
+                    } else if (itm == n) {
+                        for (int jj = part; jj < cnth; jj += ns)
+                            xadd(c0, c1, c2, (double)reach[(long long)memh[jj] * 2 * P + oh], g.scp0);
+                    }
+                    for (int o = 1; o < ns; o <<= 1) {
+                        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+                        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+                        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+                    }
+                    if (part == 0) {
+                        if (itm < n) rt[k * n + itm] = (R)xdec(c0, c1, c2, g.rc);
+                        else if (itm == n) pib[k] = (R)xdec(c0, c1, c2, g.rcp);
+                    }
+                }
+                __syncwarp();
+                // ---- phase C: Eq 8/15 or CFR+, Eq 10, then Eq 9 (z ascending)
                 const R wp = w * pib[k];
                 for (int c = 0; c < n; c += 32) {
                     const int a = c + lane;
@@ -1777,6 +1827,8 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int ix, int stages
     f.o_own = o; o += al((long long)f.maxseg + 16);
     f.o_hs = o; o += al((long long)(f.maxseg + 1) * 4 + 16);
     f.o_node = o; o += al((long long)f.maxm * ix + 16);
+    f.o_pact = o; o += f.fused ? al((long long)f.maxm + 16) : 0;
+    f.o_gsig = o; o += f.fused ? al((long long)f.maxm * w) : 0;
     f.stages = stages;
     f.stage_bytes = o;
     int x = stages * o;
@@ -1797,7 +1849,7 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int ix, int stages
 // Appends the tile records (int4 {k0, k1, m0, m1}) and member starts to `pool`.
 template <class R, class I>
 static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<int64_t>& cb_u, std::vector<int>* pool,
-                                              int min_tiles, int stages, int tile_target) {
+                                              int min_tiles, int stages, int tile_target, bool fuse_forward) {
     const int w = (int)sizeof(R), P = g.P, Pc = g.Pc, ix = (int)sizeof(I);
     std::vector<StreamLevel> out(g.D, StreamLevel{});
     for (int L = 0; L < g.D; ++L) {
@@ -1869,6 +1921,9 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
             pool->insert(pool->end(), hs.begin(), hs.end());
         }
         if ((int64_t)f.maxseg * n + f.maxseg >= 65536) { out[L] = StreamLevel{}; continue; }   // item ids < 2^16
+        // the deepest decision level: no decision children, so no other forward
+        // level reads its reach rows -- its forward pass runs inside this kernel
+        f.fused = (fuse_forward && L == g.D - 1) ? 1 : 0;
         stream_plan(f, P, Pc, w, ix, stages);
         out[L] = f;
     }
@@ -2228,7 +2283,8 @@ struct Solver final : SolverBase {
             if (const char* e = std::getenv("CFR_STREAM_DEBUG")) stream_debug_ = std::atoi(e);
             int tile = kStreamConsumers;
             if (const char* e = std::getenv("CFR_STREAM_TILE")) tile = std::max(32, std::min(1024, std::atoi(e)));
-            stream_ = stream_levels<R, I>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages, tile);
+            stream_ = stream_levels<R, I>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages, tile,
+                                          (cfg.flags & CFR_FLAG_FUSED_FORWARD) != 0);
             if (sp.size() > stream_pool_bound(g)) {
                 cfrb_set_error("internal: stream table bound");
                 return CFR_ERR_INVALID_ARG;
@@ -2386,7 +2442,7 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         int64_t n = 0;
         for (int l = 1; l < g.D; ++l)
-            if (g.slot_ptr[l + 1] > g.slot_ptr[l]) ++n;
+            if (g.slot_ptr[l + 1] > g.slot_ptr[l] && !fwd_fused(l)) ++n;
         for (int L = g.D - 1; L >= 0; --L)
             if (g.tile_ptr[L + 1] > g.tile_ptr[L]) ++n;
         if (!g.deferred_list.empty()) ++n;
@@ -2495,10 +2551,14 @@ struct Solver final : SolverBase {
     }
     bool has_def() const { return !gp->deferred_list.empty(); }
 
+    // forward level l runs inside the streaming backward kernel of level l
+    bool fwd_fused(int l) const { return use_stream_ && l < (int)stream_.size() && stream_[l].ntiles > 0 && stream_[l].fused; }
+
     void launch_lower(cudaStream_t st, int mode, const R* sig, std::vector<Mark>* ev) {
         const Game& g = *gp;
         if (mode == MODE_CFR)
             for (int l = 1; l < g.D; ++l) {
+                if (sig == dg.sig && fwd_fused(l)) continue;
                 fwd_level(st, sig, l);
                 mark(st, ev, 0, l);
             }

@@ -46,3 +46,21 @@ def test_stream_vs_tile_kernels_same_bits(cuda):
     for k in ("regret", "snum", "sden"):
         assert np.array_equal(sa[k], sb[k]), k
     assert np.array_equal(a.current_strategy(), b.current_strategy())
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_fused_forward_same_bits_as_separate_forward(cuda, precision):
+    """The deepest level's forward pass fused into its streaming backward kernel
+    gives the same state as the separate k_fwd launch (and the oracle)."""
+    import numpy as np
+    desc = gamegen.synthetic(n_types=4, seed=9)
+    g = pb.Game(desc)
+    a = pb.Solver(g, variant="cfr+", precision=precision, flags=pb.FLAG_FORCE_STREAM | pb.FLAG_FUSED_FORWARD)
+    b = pb.Solver(g, variant="cfr+", precision=precision, flags=pb.FLAG_FORCE_STREAM)
+    assert a.launches_per_iteration() == b.launches_per_iteration() - 1
+    a.run(5)
+    b.run(5)
+    sa, sb = a.state(), b.state()
+    for k in ("regret", "snum", "sden"):
+        assert np.array_equal(sa[k], sb[k]), k
+    run_pair(desc, 1, precision, 5, flags=pb.FLAG_FORCE_STREAM | pb.FLAG_FUSED_FORWARD, checks=("state",))
