@@ -413,6 +413,7 @@ bool build_game(const cfr_game_desc* d, Game& g, std::string& err) {
     std::vector<int64_t> ebase_dec(g.ND, -1);  // sigma_ext base of each decision node's children
     std::vector<int64_t> slot_h(NS, -1);     // internal infoset of each player slot
     std::vector<int64_t> dec_of_canon_lvl, prev_dec_of_canon;   // level-local canonical -> dec
+    std::vector<int64_t> row_x;              // the level's decision nodes (dec_k indices) in row order
     g.chance_vals.clear();
     int64_t slot = 0, dec = 0, cnext = 0;
     const int64_t Qtot = g.Q;
@@ -443,11 +444,30 @@ bool build_game(const cfr_game_desc* d, Game& g, std::string& err) {
                 g.f_pact[dec + x] = (uint8_t)d->player[order[pk]];
             }
         }
+        // visiting order of the level's decision nodes: the device row order, i.e.
+        // the previous level's slots in slot order, each slot's children in action
+        // order.  Infosets are numbered, and their members ordered, by first
+        // occurrence in this order, so the children of one parent and the users of
+        // one parent-infoset edge (same sigma) sit close together in slot order --
+        // the forward pass's parent-row and sigma gathers then hit in cache.
+        row_x.clear();
+        if (L == 0) {
+            for (int64_t x = 0; x < nd; ++x) row_x.push_back(x);
+        } else {
+            const int64_t plo = g.slot_ptr[L - 1];
+            for (int64_t ps = plo; ps < slot; ++ps) {
+                const int64_t pk = g.s_node[ps];
+                for (int64_t c = canon_cb[pk]; c < canon_cb[pk] + ncanon[pk]; ++c)
+                    if (ncanon[c] > 0) row_x.push_back(dec_of_canon_lvl[c - lo] - dec);
+            }
+        }
+        if ((int64_t)row_x.size() != nd) return fail(err, "internal: row order size mismatch");
         // groups: infosets in order of first occurrence, chance nodes alone
         grp_count.clear();
         grp_h.clear();
         node_grp.assign(nd, -1);
-        for (int64_t x = 0; x < nd; ++x) {
+        for (int64_t xi = 0; xi < nd; ++xi) {
+            const int64_t x = row_x[xi];
             const int64_t k = dec_k[x];
             const int64_t v = order[k];
             const int32_t pl = d->player[v];
@@ -493,7 +513,8 @@ bool build_game(const cfr_game_desc* d, Game& g, std::string& err) {
                 acc += grp_count[gi];
             }
         }
-        for (int64_t x = 0; x < nd; ++x) {
+        for (int64_t xi = 0; xi < nd; ++xi) {
+            const int64_t x = row_x[xi];
             const int64_t k = dec_k[x];
             const int64_t s = slot + gfill[node_grp[x]]++;
             const int64_t v = order[k];

@@ -138,6 +138,64 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
+// L2 eviction-priority policies (createpolicy) for loads / stores with a cache hint:
+// streams read or written once go first, small reused gather tables stay
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_normal() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+template <class T>
+__device__ __forceinline__ T ld_hint(const T* p, unsigned long long pol);
+template <>
+__device__ __forceinline__ double ld_hint<double>(const double* p, unsigned long long pol) {
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <>
+__device__ __forceinline__ float ld_hint<float>(const float* p, unsigned long long pol) {
+    float v;
+    asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <>
+__device__ __forceinline__ int ld_hint<int>(const int* p, unsigned long long pol) {
+    int v;
+    asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;\n" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <>
+__device__ __forceinline__ long long ld_hint<long long>(const long long* p, unsigned long long pol) {
+    long long v;
+    asm volatile("ld.global.L2::cache_hint.s64 %0, [%1], %2;\n" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <>
+__device__ __forceinline__ unsigned char ld_hint<unsigned char>(const unsigned char* p, unsigned long long pol) {
+    unsigned short v;
+    asm volatile("ld.global.L2::cache_hint.u8 %0, [%1], %2;\n" : "=h"(v) : "l"(p), "l"(pol));
+    return (unsigned char)v;
+}
+__device__ __forceinline__ void st_hint_v2(double2* p, double2 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st_hint_v2(float2* p, float2 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;\n" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol)
+                 : "memory");
+}
+
 template <class R>
 __device__ __forceinline__ bool finite_(R x) {
     return isfinite(x);
@@ -165,6 +223,11 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
         using V2 = typename std::conditional<sizeof(R) == 8, double2, float2>::type;
         const long long n = d_end - d_begin;
         const long long chunk = (long long)blockDim.x * FW;
+#ifndef CFR_FWD_HINTS
+#define CFR_FWD_HINTS 1
+#endif
+        const unsigned long long pf = CFR_FWD_HINTS ? policy_evict_first() : policy_evict_normal();
+        const unsigned long long pl = CFR_FWD_HINTS ? policy_evict_last() : policy_evict_normal();
         pdl_wait();
         for (long long base = (long long)blockIdx.x * chunk; base < n; base += (long long)gridDim.x * chunk) {
             long long p[FW];
@@ -174,9 +237,9 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
             for (int k = 0; k < FW; ++k) {
                 const long long i = base + k * blockDim.x + threadIdx.x;
                 const long long d = d_begin + (i < n ? i : 0);
-                p[k] = (long long)g.f_parent[d];
-                e[k] = (long long)g.f_e[d];
-                act[k] = g.f_pact[d];
+                p[k] = (long long)ld_hint(g.f_parent + d, pf);
+                e[k] = (long long)ld_hint(g.f_e + d, pf);
+                act[k] = ld_hint(g.f_pact + d, pf);
             }
             V2 a[FW], b[FW];
             R x[FW];
@@ -185,7 +248,7 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
                 const V2* src = reinterpret_cast<const V2*>(g.reach + p[k] * 4);
                 a[k] = src[0];   // pi_check(1), pi_check(2)
                 b[k] = src[1];   // pi_hat(1), pi_hat(2)
-                x[k] = sig[e[k]];
+                x[k] = ld_hint(sig + e[k], pl);   // the edge's sigma: reused by every member of the parent's infoset
             }
 #pragma unroll
             for (int k = 0; k < FW; ++k) {
@@ -197,8 +260,8 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
                 cb.x = (act[k] == 1) ? b[k].x * x[k] : b[k].x;
                 cb.y = (act[k] == 2) ? b[k].y * x[k] : b[k].y;
                 V2* dst = reinterpret_cast<V2*>(g.reach + (d_begin + i) * 4);
-                dst[0] = ca;
-                dst[1] = cb;
+                st_hint_v2(dst, ca, pf);
+                st_hint_v2(dst + 1, cb, pf);
             }
         }
         return;
