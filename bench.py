@@ -290,8 +290,15 @@ def main():
     peak, peak_src = peaks()
     dom_ms = prof["dominant_ms"]
     achieved = mb["dominant"] / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else None
+    kernels = solver.level_kernels()
+    dom = prof["dominant_level"]
+    cnt = solver.counters()["per_level"]
+    live = None
+    if 0 <= dom < len(cnt) and cnt[dom][2] > 0:
+        live = round(cnt[dom][0] / cnt[dom][2], 4)
     roofline = {
-        "bound": "hbm", "kernel": f"k_bwd (parent level {prof['dominant_level']})",
+        "bound": "hbm", "kernel": f"{kernels[dom]} (parent level {dom})",
+        "live_infoset_fraction": live,
         "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": ncu_traffic(args.n_types, args.precision),

@@ -202,12 +202,15 @@ cfr_status cfr_solver_model_bytes(cfr_solver* s, double* out /* [5] */);
  * cp.async), 3 k_bwd_stream (TMA bulk-copy ring).  `max_levels` bounds out[];
  * *num_levels receives D. */
 cfr_status cfr_solver_level_kernels(cfr_solver* s, int32_t* out, int32_t max_levels, int32_t* num_levels);
-/* Cumulative work counters of the streaming backward levels since creation:
- * out[0] infosets updated (live: some member with nonzero pi_check or pi_hat),
- * out[1] their (h, a) pairs, out[2] infosets visited, out[3] pairs visited.  A dead
- * infoset's update is the identity (every term an exact zero), so its writes are
- * skipped; bench.py's byte model counts update writes of live infosets only. */
-cfr_status cfr_solver_counters(cfr_solver* s, int64_t* out /* [4] */);
+/* Cumulative work counters of the streaming backward kernel per parent level L
+ * (0..D-1) since creation: out[4L+0] infosets updated (live: some member with a
+ * nonzero pi_check or pi_hat), out[4L+1] their (h, a) pairs, out[4L+2] infosets
+ * visited, out[4L+3] pairs visited (zeros for levels served by other kernels).  A
+ * dead infoset's update is the identity (every term an exact zero), so its writes
+ * are skipped; cfr_solver_model_bytes counts update writes of live infosets only
+ * (live fractions of the last cfr_solver_profile window). */
+cfr_status cfr_solver_counters(cfr_solver* s, int64_t* out /* [4 * max_levels] */, int32_t max_levels,
+                               int32_t* num_levels);
 
 /* Writes a fresh ncclUniqueId (128 bytes) to `out` (rank 0 only). */
 cfr_status cfr_nccl_unique_id(void* out /* 128 bytes */);

@@ -267,10 +267,15 @@ class Solver:
         return [self.KERNEL_NAMES[int(x)] for x in out[:min(nl.value, 64)]]
 
     def counters(self) -> dict:
-        """Cumulative streaming-level work counters (include/cfr_b200.h cfr_solver_counters)."""
-        out = np.zeros(4, dtype=np.int64)
-        _native.check(self._L.cfr_solver_counters(self._h, _ptr(out)))
-        return dict(live_infosets=int(out[0]), live_pairs=int(out[1]), infosets=int(out[2]), pairs=int(out[3]))
+        """Cumulative streaming-level work counters (include/cfr_b200.h cfr_solver_counters),
+        summed over levels, plus the per-level table."""
+        out = np.zeros(4 * 64, dtype=np.int64)
+        nl = ctypes.c_int32()
+        _native.check(self._L.cfr_solver_counters(self._h, _ptr(out), 64, ctypes.byref(nl)))
+        per = out[:4 * min(nl.value, 64)].reshape(-1, 4)
+        tot = per.sum(0)
+        return dict(live_infosets=int(tot[0]), live_pairs=int(tot[1]), infosets=int(tot[2]), pairs=int(tot[3]),
+                    per_level=per.tolist())
 
     def model_bytes(self) -> dict:
         out = np.zeros(5)

@@ -86,6 +86,7 @@ struct DG {
     const SegD* segs;
     const I* deferred;            // [ndef]
     long long* ctrl;              // [0] iterations done, [1] first bad iteration, [2] done counter
+    unsigned long long* lcnt;     // [D][4] streaming-level work counters (updated / visited infosets, pairs)
     long long ndef;
     int P;
     int variant;
@@ -1070,6 +1071,7 @@ struct StreamLevel {
     int bytes;              // dynamic shared memory
     int last;
     int debug;              // timing experiments only: 1 consumers skip compute, 2 producer skips loads
+    int level;              // parent level (work counters)
 };
 constexpr int kStreamConsumers = 256;   // 8 consumer warps
 constexpr int kStreamThreads = kStreamConsumers + 32;   // + 1 producer warp
@@ -1543,10 +1545,11 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
     if (tid == 0) {
         // cumulative: infosets updated / visited by the streaming levels (bench.py's
         // byte model counts update writes of live infosets only)
-        atomicAdd((unsigned long long*)&g.ctrl[4], live_h);
-        atomicAdd((unsigned long long*)&g.ctrl[5], live_h * (unsigned long long)n);
-        atomicAdd((unsigned long long*)&g.ctrl[6], all_h);
-        atomicAdd((unsigned long long*)&g.ctrl[7], all_h * (unsigned long long)n);
+        unsigned long long* c = g.lcnt + 4 * L.level;
+        atomicAdd(c + 0, live_h);
+        atomicAdd(c + 1, live_h * (unsigned long long)n);
+        atomicAdd(c + 2, all_h);
+        atomicAdd(c + 3, all_h * (unsigned long long)n);
     }
     if (L.last) {
         consumers_sync();
@@ -1717,7 +1720,7 @@ struct SolverBase {
     virtual cfr_status profile(int64_t iters, double* out) = 0;
     virtual cfr_status model_bytes(double* out) = 0;
     virtual cfr_status level_kernels(int32_t* out, int32_t max_levels, int32_t* num_levels) = 0;
-    virtual cfr_status counters(int64_t* out) = 0;
+    virtual cfr_status counters(int64_t* out, int32_t max_levels, int32_t* num_levels) = 0;
     virtual cfr_status phase(int ph, double* out) = 0;
     virtual cfr_status exchange_size(int which, size_t* bytes) = 0;
     virtual cfr_status exchange(int which, int put, void* host, size_t bytes) = 0;
@@ -1987,6 +1990,7 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         // the deepest decision level: no decision children, so no other forward
         // level reads its reach rows -- its forward pass runs inside this kernel
         f.fused = (fuse_forward && L == g.D - 1) ? 1 : 0;
+        f.level = L;
         stream_plan(f, P, Pc, w, ix, stages);
         out[L] = f;
     }
@@ -2017,7 +2021,7 @@ struct Plan {
     size_t U, reach, sig, sig_eval, regret, snum, sden, acc_r, acc_p, dqbase;
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
-    size_t qbase, owner, tiles, segs, deferred, ctrl, out;
+    size_t qbase, owner, tiles, segs, deferred, ctrl, lcnt, out;
     size_t cutbuf, cutrow, cutown, report, pool, spool;
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
@@ -2050,6 +2054,7 @@ struct Plan {
         segs = L.take<SegD>(g.segs.size());
         deferred = L.take<I>(g.deferred_list.size());
         ctrl = L.take<long long>(8);
+        lcnt = L.take<unsigned long long>(4 * (size_t)g.D + 4);
         out = L.take<R>(std::max<size_t>(Q + C, (size_t)g.P * 2 + 8));
         const size_t ncut = sh ? sh->cut_row.size() : 0;
         cutbuf = L.take<R>(ncut * g.Pc + 1);
@@ -2246,6 +2251,7 @@ struct Solver final : SolverBase {
         dg.segs = at<SegD>(plan.segs);
         dg.deferred = at<I>(plan.deferred);
         dg.ctrl = at<long long>(plan.ctrl);
+        dg.lcnt = at<unsigned long long>(plan.lcnt);
         dg.ndef = (long long)g.deferred_list.size();
         dg.P = g.P;
         dg.variant = cfg.variant;
@@ -2430,6 +2436,7 @@ struct Solver final : SolverBase {
         CU(cudaMemsetAsync(ws + plan.snum, 0, g.Q * sizeof(R), stream));
         CU(cudaMemsetAsync(ws + plan.sden, 0, g.H * sizeof(R), stream));
         CU(cudaMemsetAsync(ws + plan.acc_r, 0, acc_bytes(), stream));
+        CU(cudaMemsetAsync(ws + plan.lcnt, 0, (4 * (size_t)g.D + 4) * sizeof(unsigned long long), stream));
         CU(cudaMemsetAsync(ws + plan.reach, 0, 2 * (size_t)g.P * g.ND * sizeof(R), stream));
         {
             // root reach factors = 1 (Eq 2 / Eq 4 base case); the root is decision 0
@@ -2893,6 +2900,9 @@ struct Solver final : SolverBase {
             return CFR_ERR_UNSUPPORTED;
         }
         std::vector<double> per_bwd(g.D, 0.0);
+        std::vector<unsigned long long> c0, c1;
+        cfr_status cs = read_lcnt(c0);
+        if (cs) return cs;
         for (int64_t it = 0; it < iters; ++it) {
             std::vector<Mark> ev;
             cfr_status s = launch_iteration(stream, &ev);
@@ -2910,6 +2920,14 @@ struct Solver final : SolverBase {
             }
             for (auto& m : ev) cudaEventDestroy(m.e);
         }
+        if ((cs = read_lcnt(c1))) return cs;
+        // live (updated) infosets / pairs per iteration of the streaming levels
+        prof_live_.assign(2 * (size_t)g.D, -1.0);
+        for (int L = 0; L < g.D; ++L)
+            if (c1[4 * L + 2] > c0[4 * L + 2]) {
+                prof_live_[2 * L] = (double)(c1[4 * L + 0] - c0[4 * L + 0]) / (double)iters;
+                prof_live_[2 * L + 1] = (double)(c1[4 * L + 1] - c0[4 * L + 1]) / (double)iters;
+            }
         int dom = 0;
         for (int L = 0; L < g.D; ++L)
             if (per_bwd[L] > per_bwd[dom]) dom = L;
@@ -2996,11 +3014,19 @@ struct Solver final : SolverBase {
         if (sizeof(R) == 8 && use_fast_ && fast_[L].recsize > 0) return 2;
         return 1;
     }
-    cfr_status counters(int64_t* out) override {
+    cfr_status read_lcnt(std::vector<unsigned long long>& c) {
+        c.assign(4 * (size_t)gp->D, 0);
         CU(cudaStreamSynchronize(stream));
-        long long c[4];
-        CU(cudaMemcpy(c, dg.ctrl + 4, sizeof(c), cudaMemcpyDeviceToHost));
-        for (int k = 0; k < 4; ++k) out[k] = c[k];
+        if (!c.empty()) CU(cudaMemcpy(c.data(), dg.lcnt, c.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        return CFR_OK;
+    }
+    cfr_status counters(int64_t* out, int32_t max_levels, int32_t* num_levels) override {
+        std::vector<unsigned long long> c;
+        cfr_status st = read_lcnt(c);
+        if (st) return st;
+        *num_levels = gp->D;
+        for (int L = 0; L < gp->D && L < max_levels; ++L)
+            for (int k = 0; k < 4; ++k) out[4 * L + k] = (int64_t)c[4 * L + k];
         return CFR_OK;
     }
     cfr_status level_kernels(int32_t* out, int32_t max_levels, int32_t* num_levels) override {
@@ -3012,12 +3038,34 @@ struct Solver final : SolverBase {
 
     // Algorithmic DRAM bytes per iteration (DESIGN.md §6 byte model).
     int dom_level = -1;   // set by profile(): the backward level with the largest time
+    std::vector<double> prof_live_;   // per level: live infosets, live pairs per iteration (last profile), -1 unknown
     double level_bwd_bytes(int L) const {
         const Game& g = *gp;
         const double w = sizeof(R), ix = sizeof(I);
         const int Pc = g.Pc;
         const double parents = (double)(g.slot_ptr[L + 1] - g.slot_ptr[L]);
         const double children = (double)(g.level_ptr[L + 2] - g.level_ptr[L + 1]);
+        if (use_stream_ && L < (int)stream_.size() && stream_[L].ntiles > 0) {
+            // k_bwd_stream: children's values read once; per member its U row index,
+            // value write, the actor's pi_check and pi_hat; per infoset its member
+            // start, owner and S_den read; per pair sigma, R, S_num read.  Writes of
+            // the update (R, S_num, sigma per pair, S_den per infoset) for LIVE
+            // infosets only (the measured count of the last profile window; all
+            // infosets if unknown).  The fused forward variant is not modelled.
+            double nh = 0, npairs = 0;
+            for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1]; ++t)
+                for (int k = g.tiles[t].seg0; k < g.tiles[t].seg1; ++k) {
+                    nh += 1;
+                    npairs += (double)(g.qbase_int[g.segs[k].h + 1] - g.qbase_int[g.segs[k].h]);
+                }
+            double live_h = nh, live_p = npairs;
+            if ((int)prof_live_.size() == 2 * g.D && prof_live_[2 * L] >= 0) {
+                live_h = prof_live_[2 * L];
+                live_p = prof_live_[2 * L + 1];
+            }
+            return children * Pc * w + parents * (ix + Pc * w + 2 * w) + npairs * 3 * w + nh * (4 + 1 + w) +
+                   live_p * 3 * w + live_h * w;
+        }
         // children values read once; parent: node, cb, ebase, dec (ix each), n, coff
         // (4 each), actor (1); value write; the owner's pi_check and pi_hat
         double b = children * Pc * w + parents * (4 * ix + 8 + 1 + Pc * w + 2 * w);
@@ -3242,10 +3290,10 @@ cfr_status cfr_solver_level_kernels(cfr_solver* s, int32_t* out, int32_t max_lev
     if (!num_levels || (max_levels > 0 && !out)) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
     return s->impl->level_kernels(out, max_levels, num_levels);
 }
-cfr_status cfr_solver_counters(cfr_solver* s, int64_t* out) {
+cfr_status cfr_solver_counters(cfr_solver* s, int64_t* out, int32_t max_levels, int32_t* num_levels) {
     CHK_S(s);
-    if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
-    return s->impl->counters(out);
+    if (!num_levels || (max_levels > 0 && !out)) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->counters(out, max_levels, num_levels);
 }
 cfr_status cfr_nccl_unique_id(void* out) {
     if (!out) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
