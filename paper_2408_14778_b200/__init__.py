@@ -193,12 +193,12 @@ class Solver:
 
     # -- readbacks (caller (h, a) order)
     def average_strategy(self) -> np.ndarray:
-        out = np.zeros(self.Q)
+        out = np.empty(self.Q)
         _native.check(self._L.cfr_solver_average_strategy(self._h, _ptr(out)))
         return out
 
     def current_strategy(self) -> np.ndarray:
-        out = np.zeros(self.Q)
+        out = np.empty(self.Q)
         _native.check(self._L.cfr_solver_current_strategy(self._h, _ptr(out)))
         return out
 

@@ -207,9 +207,13 @@ __device__ __forceinline__ bool finite_(R x) {
 // parents' rows, streaming writes).  Eq 2: pi_check(v,i) =
 // pi_check(parent,i) * (sigma if the parent's actor != i else 1); Eq 4 (P:97,
 // reading Q1): pi_hat(v,i) = pi_hat(parent,i) * (sigma if actor == i else 1).
+// compact != 0 (two players, the deepest decision level when its backward pass
+// is the streaming kernel): no forward level reads these rows, and the backward
+// pass needs only the acting player's pi_check and pi_hat -- 2 values per slot
+// are written at reach + d_begin*2P + (d - d_begin)*2 instead of the 2P-value row.
 template <class R, class I, int PT>
 __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ sig, long long d_begin,
-                                             long long d_end) {
+                                             long long d_end, int compact) {
     const int P = (PT > 0) ? PT : g.P;
     const long long stride = (long long)gridDim.x * blockDim.x;
     pdl_trigger();
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
         for (long long base = (long long)blockIdx.x * chunk; base < n; base += (long long)gridDim.x * chunk) {
             long long p[FW];
             long long e[FW];
-            int act[FW];
+            int act[FW], own[FW];
 #pragma unroll
             for (int k = 0; k < FW; ++k) {
                 const long long i = base + k * blockDim.x + threadIdx.x;
@@ -241,6 +245,7 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
                 p[k] = (long long)ld_hint(g.f_parent + d, pf);
                 e[k] = (long long)ld_hint(g.f_e + d, pf);
                 act[k] = ld_hint(g.f_pact + d, pf);
+                own[k] = compact ? (int)ld_hint(g.s_actor + d, pf) : 0;
             }
             V2 a[FW], b[FW];
             R x[FW];
@@ -260,6 +265,14 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
                 ca.y = (act[k] != 2) ? a[k].y * x[k] : a[k].y;
                 cb.x = (act[k] == 1) ? b[k].x * x[k] : b[k].x;
                 cb.y = (act[k] == 2) ? b[k].y * x[k] : b[k].y;
+                if (compact) {
+                    // the slot's actor: (pi_check, pi_hat) of that player only
+                    V2 c2;
+                    c2.x = (own[k] == 2) ? ca.y : ca.x;
+                    c2.y = (own[k] == 2) ? cb.y : cb.x;
+                    st_hint_v2(reinterpret_cast<V2*>(g.reach + d_begin * 4 + i * 2), c2, pf);
+                    continue;
+                }
                 V2* dst = reinterpret_cast<V2*>(g.reach + (d_begin + i) * 4);
                 st_hint_v2(dst, ca, pf);
                 st_hint_v2(dst + 1, cb, pf);
@@ -1072,6 +1085,7 @@ struct StreamLevel {
     int last;
     int debug;              // timing experiments only: 1 consumers skip compute, 2 producer skips loads
     int level;              // parent level (work counters)
+    int compact;            // 1: reach rows of this level are compact (pi_check, pi_hat of the actor; k_fwd compact)
 };
 constexpr int kStreamConsumers = 256;   // 8 consumer warps
 constexpr int kStreamThreads = kStreamConsumers + 32;   // + 1 producer warp
@@ -1209,6 +1223,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 const unsigned char* w_reach = nullptr;
                 const unsigned char* w_pact = nullptr;
                 if (L.fused) w_pact = window16(g.f_pact + slot, M, &b_pact, &pao);
+                else if (L.compact) w_reach = window16(g.reach + L.s0 * 2 * P + (long long)m0 * 2, (long long)M * 2, &b_reach, &o_reach);
                 else w_reach = window16(g.reach + slot * 2 * P, (long long)M * 2 * P, &b_reach, &o_reach);
                 const unsigned char* w_sig = window16(g.sig + q, (long long)nseg * n, &b_sig, &po);
                 const unsigned char* w_reg = window16(g.regret + q, (long long)nseg * n, &b_reg, &po2);
@@ -1303,6 +1318,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
     const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
     bool bad = false;
     const R inv_n = (R)1 / (R)n;   // uniform strategy of the level's infosets (Eq 9, z = 0)
+    const int rs = L.compact ? 2 : 2 * P;   // reach row stride in the stage (elements)
     unsigned long long live_h = 0, all_h = 0;   // updated / visited infosets (thread 0)
     long long t = blockIdx.x;
     int st = 0;
@@ -1391,8 +1407,8 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                     prow[0] = pc;
                     prow[1] = ph;
                 } else {
-                    pc = reach[(long long)m * 2 * P + (i - 1)];
-                    ph = reach[(long long)m * 2 * P + P + (i - 1)];
+                    pc = reach[(long long)m * rs + (L.compact ? 0 : i - 1)];
+                    ph = reach[(long long)m * rs + (L.compact ? 1 : P + i - 1)];
                 }
             }
             if (L.debug & 32) continue;   // timing experiment: no compaction
@@ -1441,7 +1457,8 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 const int col = (PC == 1) ? 0 : i - 1;
                 const int sb = hs[k] - m0;
                 const int cntc = ccnt[k], cnth = ccnt[L.maxseg + k];
-                const int oc = L.fused ? 0 : i - 1, oh = L.fused ? 1 : P + i - 1;   // pi_check / pi_hat in a reach row
+                const bool two = L.fused || L.compact;
+                const int oc = two ? 0 : i - 1, oh = two ? 1 : P + i - 1;   // pi_check / pi_hat in a reach row
                 const short* memc = cm + sb;
                 const short* memh = cm + L.maxm + sb;
                 // ---- phase B: exact sums (slices of integer-valued doubles combine
@@ -1457,15 +1474,15 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                             const int la = memc[jj], lb = memc[jj + ns];
                             const R ua = rows[(long long)la * L.rowlen + a * PC + col];
                             const R ub = rows[(long long)lb * L.rowlen + a * PC + col];
-                            const R ta = reach[(long long)la * 2 * P + oc] * (ua - sv[la * PC + col]);
-                            const R tb = reach[(long long)lb * 2 * P + oc] * (ub - sv[lb * PC + col]);
+                            const R ta = reach[(long long)la * rs + oc] * (ua - sv[la * PC + col]);
+                            const R tb = reach[(long long)lb * rs + oc] * (ub - sv[lb * PC + col]);
                             xadd(c0, c1, c2, (double)ta, g.sc0);
                             xadd(e0, e1, e2, (double)tb, g.sc0);
                         }
                         if (jj < cntc) {
                             const int la = memc[jj];
                             const R ua = rows[(long long)la * L.rowlen + a * PC + col];
-                            const R ta = reach[(long long)la * 2 * P + oc] * (ua - sv[la * PC + col]);
+                            const R ta = reach[(long long)la * rs + oc] * (ua - sv[la * PC + col]);
                             xadd(c0, c1, c2, (double)ta, g.sc0);
                         }
                         c0 += e0;
@@ -1474,7 +1491,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                         if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
                     } else if (itm == n) {
                         for (int jj = part; jj < cnth; jj += ns)
-                            xadd(c0, c1, c2, (double)reach[(long long)memh[jj] * 2 * P + oh], g.scp0);
+                            xadd(c0, c1, c2, (double)reach[(long long)memh[jj] * rs + oh], g.scp0);
                     }
                     for (int o = 1; o < ns; o <<= 1) {
                         c0 += __shfl_xor_sync(0xffffffffu, c0, o);
@@ -1915,7 +1932,8 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int ix, int stages
 // Appends the tile records (int4 {k0, k1, m0, m1}) and member starts to `pool`.
 template <class R, class I>
 static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<int64_t>& cb_u, std::vector<int>* pool,
-                                              int min_tiles, int stages, int tile_target, bool fuse_forward) {
+                                              int min_tiles, int stages, int tile_target, bool fuse_forward,
+                                              bool compact_reach) {
     const int w = (int)sizeof(R), P = g.P, Pc = g.Pc, ix = (int)sizeof(I);
     std::vector<StreamLevel> out(g.D, StreamLevel{});
     for (int L = 0; L < g.D; ++L) {
@@ -1991,6 +2009,7 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         // level reads its reach rows -- its forward pass runs inside this kernel
         f.fused = (fuse_forward && L == g.D - 1) ? 1 : 0;
         f.level = L;
+        f.compact = (!f.fused && P == 2 && L == g.D - 1 && compact_reach) ? 1 : 0;
         stream_plan(f, P, Pc, w, ix, stages);
         out[L] = f;
     }
@@ -2105,6 +2124,7 @@ struct Solver final : SolverBase {
     }
 
     ~Solver() override {
+        if (pinned_) cudaFreeHost(pinned_);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (cap_stream) cudaStreamDestroy(cap_stream);
         if (comm) ncclCommDestroy(comm);
@@ -2353,7 +2373,7 @@ struct Solver final : SolverBase {
             int tile = kStreamConsumers;
             if (const char* e = std::getenv("CFR_STREAM_TILE")) tile = std::max(32, std::min(1024, std::atoi(e)));
             stream_ = stream_levels<R, I>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages, tile,
-                                          (cfg.flags & CFR_FLAG_FUSED_FORWARD) != 0);
+                                          (cfg.flags & CFR_FLAG_FUSED_FORWARD) != 0, std::getenv("CFR_NO_COMPACT") == nullptr);
             if (sp.size() > stream_pool_bound(g)) {
                 cfrb_set_error("internal: stream table bound");
                 return CFR_ERR_INVALID_ARG;
@@ -2519,7 +2539,13 @@ struct Solver final : SolverBase {
         return n;
     }
 
-    void fwd_level(cudaStream_t st, const R* sig, int l) {
+    // the deepest level's reach rows in compact (actor-only) form: CFR iterations
+    // whose backward pass there is the (unfused) streaming kernel, two players
+    bool fwd_compact(int l) const {
+        return gp->P == 2 && l == gp->D - 1 && use_stream_ && l < (int)stream_.size() && stream_[l].ntiles > 0 &&
+               !stream_[l].fused && stream_[l].compact;
+    }
+    void fwd_level(cudaStream_t st, const R* sig, int l, int compact = 0) {
         const Game& g = *gp;
         const long long s0 = g.slot_ptr[l], s1 = g.slot_ptr[l + 1];   // reach rows = slots
         if (s1 <= s0) return;
@@ -2528,9 +2554,11 @@ struct Solver final : SolverBase {
         const long long per_block = (g.P == 2) ? threads * CFR_FWD_FW : threads;
         const long long blocks = std::min<long long>((n + per_block - 1) / per_block, 148LL * 16);
         if (g.P == 2)
-            launch(pdl_, k_fwd<R, I, 2>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1);
+            launch(pdl_, k_fwd<R, I, 2>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1,
+                   compact);
         else
-            launch(pdl_, k_fwd<R, I, 0>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1);
+            launch(pdl_, k_fwd<R, I, 0>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1,
+                   0);
     }
 
     template <int MODE>
@@ -2629,7 +2657,7 @@ struct Solver final : SolverBase {
         if (mode == MODE_CFR)
             for (int l = 1; l < g.D; ++l) {
                 if (sig == dg.sig && fwd_fused(l)) continue;
-                fwd_level(st, sig, l);
+                fwd_level(st, sig, l, (sig == dg.sig && fwd_compact(l)) ? 1 : 0);
                 mark(st, ev, 0, l);
             }
         const int stop = sharded() ? sh->cut : 0;
@@ -2753,15 +2781,36 @@ struct Solver final : SolverBase {
     }
 
     // device buffer (internal q order) -> combined -> host doubles in caller order
+    // pinned host staging for readbacks (allocated on first use)
+    R* pinned_ = nullptr;
+    size_t pinned_n_ = 0;
+    cfr_status staging(size_t n, R** out) {
+        if (pinned_n_ < n) {
+            if (pinned_) cudaFreeHost(pinned_);
+            pinned_ = nullptr;
+            pinned_n_ = 0;
+            CU(cudaMallocHost(&pinned_, std::max<size_t>(n, 1) * sizeof(R)));
+            pinned_n_ = n;
+        }
+        *out = pinned_;
+        return CFR_OK;
+    }
     cfr_status read_q(const R* dptr, double* out) {
         const Game& g = *gp;
-        R* tmpd = at<R>(plan.out);
-        if (g.Q) CU(cudaMemcpyAsync(tmpd, dptr, g.Q * sizeof(R), cudaMemcpyDeviceToDevice, stream));
-        cfr_status s = combine_q(tmpd);
+        const R* src = dptr;
+        if (world > 1) {
+            R* tmpd = at<R>(plan.out);
+            if (g.Q) CU(cudaMemcpyAsync(tmpd, dptr, g.Q * sizeof(R), cudaMemcpyDeviceToDevice, stream));
+            cfr_status s = combine_q(tmpd);
+            if (s) return s;
+            src = tmpd;
+        }
+        R* tmp = nullptr;
+        cfr_status s = staging((size_t)g.Q, &tmp);
         if (s) return s;
-        std::vector<R> tmp(g.Q);
-        if (g.Q) CU(cudaMemcpyAsync(tmp.data(), tmpd, g.Q * sizeof(R), cudaMemcpyDeviceToHost, stream));
+        if (g.Q) CU(cudaMemcpyAsync(tmp, src, g.Q * sizeof(R), cudaMemcpyDeviceToHost, stream));
         CU(cudaStreamSynchronize(stream));
+#pragma omp parallel for schedule(static)
         for (int64_t hc = 0; hc < g.H; ++hc) {
             const int64_t hi = g.h_int_of_caller[hc];
             const int64_t n = g.qbase_caller[hc + 1] - g.qbase_caller[hc];
@@ -3087,11 +3136,15 @@ struct Solver final : SolverBase {
         const int P = g.P;
         double fwd = 0, bwd = 0, upd = 0;
         for (int l = 1; l < g.D; ++l) {
-            const double n = (double)(g.dec_ptr[l + 1] - g.dec_ptr[l]);
-            // per decision node: parent dec + edge index + parent actor, its 2P factors
-            // written; every parent's 2P factors read once (streaming, canonical order)
-            fwd += n * (2 * ix + 1 + 2 * P * w);
-            fwd += (double)(g.dec_ptr[l] - g.dec_ptr[l - 1]) * 2 * P * w;
+            if (fwd_fused(l)) continue;   // inside the streaming backward kernel (not modelled)
+            const double n = (double)(g.slot_ptr[l + 1] - g.slot_ptr[l]);
+            // per decision node: parent slot + edge index + parent actor, its 2P factors
+            // written (compact: the actor and its 2 factors); every parent's 2P
+            // factors and the edge's sigma read once (parent rows and sigma are gathers
+            // made cache-local by the row-order slot numbering)
+            if (fwd_compact(l)) fwd += n * (2 * ix + 1 + 1 + 2 * w);
+            else fwd += n * (2 * ix + 1 + 2 * P * w);
+            fwd += (double)(g.slot_ptr[l] - g.slot_ptr[l - 1]) * 2 * P * w;
         }
         int big = 0;
         for (int L = g.D - 1; L >= 0; --L) {
