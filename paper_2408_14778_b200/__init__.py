@@ -32,6 +32,7 @@ def nccl_unique_id() -> bytes:
 CFR, CFR_PLUS = 0, 1
 # cfr_solver_config.flags (include/cfr_b200.h)
 FLAG_NO_GRAPH = 1
+FLAG_PERSISTENT = 2
 FLAG_NO_PIPELINE = 4
 FLAG_NO_PDL = 8
 FLAG_NO_STREAM = 16

@@ -212,8 +212,8 @@ __device__ __forceinline__ bool finite_(R x) {
 // pass needs only the acting player's pi_check and pi_hat -- 2 values per slot
 // are written at reach + d_begin*2P + (d - d_begin)*2 instead of the 2P-value row.
 template <class R, class I, int PT>
-__global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ sig, long long d_begin,
-                                             long long d_end, int compact) {
+__device__ __forceinline__ void fwd_body(const DG<R, I>& g, const R* __restrict__ sig, long long d_begin,
+                                         long long d_end, int compact) {
     const int P = (PT > 0) ? PT : g.P;
     const long long stride = (long long)gridDim.x * blockDim.x;
     pdl_trigger();
@@ -298,6 +298,12 @@ __global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ s
     }
 }
 
+template <class R, class I, int PT>
+__global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ sig, long long d_begin,
+                                             long long d_end, int compact) {
+    fwd_body<R, I, PT>(g, sig, d_begin, d_end, compact);
+}
+
 // ----------------------------------------------------------- backward pass
 // One CTA (kTileSlots threads) per tile of whole infosets.  Global memory is
 // touched in three dependency steps only (metadata; reach + sigma + children +
@@ -367,11 +373,10 @@ __device__ __forceinline__ int seg_of_pair(const int* soff, int nseg, int p) {
 }
 
 template <class R, class I, int PC, int MODE>
-__global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restrict__ sig, long long tile0,
-                                                    int br_player, int last, SmemLayout lay) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict__ sig, long long tile, int br_player,
+                                         int last, const SmemLayout& lay, unsigned char* smem_raw) {
     const TileView<R> sm = make_view<R>(smem_raw, lay);
-    const TileD T = g.tiles[tile0 + blockIdx.x];
+    const TileD T = g.tiles[tile];
     const int nslot = (int)(T.s1 - T.s0);
     const int nseg = T.seg1 - T.seg0;
     const int tid = threadIdx.x, nth = blockDim.x;
@@ -704,6 +709,13 @@ __global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restr
         __syncthreads();
         if (tid == 0) g.ctrl[0] = t_iter;
     }
+}
+
+template <class R, class I, int PC, int MODE>
+__global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restrict__ sig, long long tile0,
+                                                    int br_player, int last, SmemLayout lay) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    bwd_tile<R, I, PC, MODE>(g, sig, tile0 + blockIdx.x, br_player, last, lay, smem_raw);
 }
 
 // ------------------------------------------------- pipelined backward pass
@@ -1584,7 +1596,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
 // Update of deferred infosets (span several depths / tiles): decode the global
 // exact sums, then the same Eq 8/15, Eq 10, Eq 9 steps; zero the accumulators.
 template <class R, class I>
-__global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
+__device__ __forceinline__ void deferred_body(const DG<R, I>& g, int last) {
     pdl_trigger();
     pdl_wait();
     const long long t_iter = g.ctrl[0] + 1;
@@ -1648,6 +1660,75 @@ __global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
                 g.ctrl[2] = 0;
             }
         }
+    }
+}
+
+template <class R, class I>
+__global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
+    deferred_body<R, I>(g, last);
+}
+
+// --------------------------------------------------- persistent iteration
+// Small games are launch-latency bound (2D kernels per iteration).  k_persist runs
+// T whole iterations in ONE cooperative launch: every CTA is resident; the levels
+// of an iteration are separated by grid-wide barriers (the same forward, tile and
+// deferred bodies as the per-level kernels, so the arithmetic is identical).
+struct PLevel {
+    long long s0, s1;   // slots of depth l (forward pass of level l)
+    long long t0, t1;   // tiles of parent depth L (backward pass)
+    SmemLayout lay;     // tile shared-memory layout of depth L
+};
+
+// Sense-free grid barrier: bar[0] arrivals, bar[1] generation.  Thread 0 arrives
+// after a gpu-scope fence (the block's writes are visible) and leaves after one
+// (other blocks' writes are visible to the block, L1 included).
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <class R, class I, int PC, int PT>
+__global__ void __launch_bounds__(kTileSlots) k_persist(DG<R, I> g, const PLevel* __restrict__ lv, int D, int has_def,
+                                                         long long T, unsigned* bar) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    long long t_done = g.ctrl[0];
+    for (long long it = 0; it < T; ++it) {
+        for (int l = 1; l < D; ++l) {   // forward pass, depth 1 .. D-1
+            const long long s0 = lv[l].s0, s1 = lv[l].s1;
+            if (s1 <= s0) continue;
+            fwd_body<R, I, PT>(g, g.sig, s0, s1, 0);
+            grid_sync(bar);
+        }
+        for (int L = D - 1; L >= 0; --L) {   // backward pass, parent depth D-1 .. 0
+            const long long t0 = lv[L].t0, t1 = lv[L].t1;
+            if (t1 <= t0) continue;
+            const SmemLayout lay = lv[L].lay;
+            for (long long t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
+                __syncthreads();   // the previous tile's shared-memory reads are done
+                bwd_tile<R, I, PC, MODE_CFR>(g, g.sig, t, 0, 0, lay, smem_raw);
+            }
+            grid_sync(bar);
+        }
+        if (has_def) {
+            deferred_body<R, I>(g, 0);
+            grid_sync(bar);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) g.ctrl[0] = ++t_done;   // the iteration is complete
+        else ++t_done;
+        grid_sync(bar);
     }
 }
 
@@ -2041,7 +2122,7 @@ struct Plan {
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, ctrl, lcnt, out;
-    size_t cutbuf, cutrow, cutown, report, pool, spool;
+    size_t cutbuf, cutrow, cutown, report, pool, spool, plev, gbar;
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
         Layout L;
@@ -2082,6 +2163,8 @@ struct Plan {
         report = L.take<unsigned char>(H + 1);
         pool = L.take<unsigned char>(fast_pool_bytes<R, I>(g, sh) + 16);
         spool = L.take<int>(stream_pool_bound(g));
+        plev = L.take<PLevel>((size_t)g.D + 1);
+        gbar = L.take<unsigned>(4);
         total = L.off + 256;
     }
 };
@@ -2108,6 +2191,8 @@ struct Solver final : SolverBase {
     int E = 1;
     int64_t launches_per_iter = 0;
     bool use_graph = true;
+    bool persist_ = false;        // small game: whole iterations in one cooperative launch (k_persist)
+    int persist_grid_ = 0, persist_smem_ = 0;
     bool use_fast_ = true;
     bool use_stream_ = true;
     int stream_debug_ = 0;   // CFR_STREAM_DEBUG (timing experiments; results are garbage when set)
@@ -2486,6 +2571,10 @@ struct Solver final : SolverBase {
             CU(set_smem_attr(optin));
         }
         launches_per_iter = count_launches();
+        {
+            cfr_status ps = setup_persistent();
+            if (ps) return ps;
+        }
         if (use_graph && g.NS > 0 && !external) {
             CU(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
             cudaGraph_t graph;
@@ -2527,6 +2616,69 @@ struct Solver final : SolverBase {
 #undef SETA
         return e;
     }
+
+    // Persistent mode for small games (opt-in, CFR_FLAG_PERSISTENT): one cooperative
+    // launch runs T iterations (k_persist).  Measured slower than the PDL graph on
+    // B200 (Kuhn 36.6 vs 24.6 us/it, Leduc 134 vs 108): each level's dependent
+    // global-memory chain, not the launch, dominates.  Off for sharded solvers.
+    static constexpr int64_t kPersistMaxNodes = int64_t(1) << 22;
+    cfr_status setup_persistent() {
+        const Game& g = *gp;
+        persist_ = false;
+        if (world > 1 || external || !(cfg.flags & CFR_FLAG_PERSISTENT) || g.NS == 0 || g.V > kPersistMaxNodes)
+            return CFR_OK;
+        int dev = 0, coop = 0;
+        CU(cudaGetDevice(&dev));
+        CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        if (!coop) return CFR_OK;
+        std::vector<PLevel> lv(g.D + 1);
+        long long max_units = 1;
+        for (int l = 0; l < g.D; ++l) {
+            lv[l].s0 = g.slot_ptr[l];
+            lv[l].s1 = g.slot_ptr[l + 1];
+            lv[l].t0 = g.tile_ptr[l];
+            lv[l].t1 = g.tile_ptr[l + 1];
+            lv[l].lay = lay_[l];
+            max_units = std::max<long long>(max_units, lv[l].t1 - lv[l].t0);
+            max_units = std::max<long long>(max_units, (lv[l].s1 - lv[l].s0 + 1023) / 1024);
+        }
+        persist_smem_ = std::max(16, max_smem_);
+        void* fn = persist_fn();
+        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, persist_smem_));
+        int per_sm = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTileSlots, persist_smem_));
+        if (per_sm < 1) return CFR_OK;
+        persist_grid_ = (int)std::min<long long>((long long)num_sms_ * per_sm, max_units);
+        cfr_status st = up(plan.plev, lv);
+        if (st) return st;
+        CU(cudaMemsetAsync(ws + plan.gbar, 0, 4 * sizeof(unsigned), stream));
+        CU(cudaStreamSynchronize(stream));
+        persist_ = true;
+        return CFR_OK;
+    }
+    void* persist_fn() const {
+        const int Pc = gp->Pc;
+        const bool p2 = gp->P == 2;
+        switch (Pc) {
+            case 1: return p2 ? (void*)k_persist<R, I, 1, 2> : (void*)k_persist<R, I, 1, 0>;
+            case 2: return p2 ? (void*)k_persist<R, I, 2, 2> : (void*)k_persist<R, I, 2, 0>;
+            case 3: return p2 ? (void*)k_persist<R, I, 3, 2> : (void*)k_persist<R, I, 3, 0>;
+            default: return p2 ? (void*)k_persist<R, I, 4, 2> : (void*)k_persist<R, I, 4, 0>;
+        }
+    }
+    cfr_status launch_persistent(int64_t iters) {
+        const Game& g = *gp;
+        const PLevel* lv = at<PLevel>(plan.plev);
+        int D = g.D;
+        int has_def = has_def_() ? 1 : 0;
+        long long T = (long long)iters;
+        unsigned* bar = at<unsigned>(plan.gbar);
+        void* args[] = {(void*)&dg, (void*)&lv, (void*)&D, (void*)&has_def, (void*)&T, (void*)&bar};
+        CU(cudaLaunchCooperativeKernel(persist_fn(), dim3(persist_grid_), dim3(kTileSlots), args, (size_t)persist_smem_,
+                                       stream));
+        return CFR_OK;
+    }
+    bool has_def_() const { return !gp->deferred_list.empty(); }
 
     int64_t count_launches() const {
         const Game& g = *gp;
@@ -2729,6 +2881,7 @@ struct Solver final : SolverBase {
             cfrb_set_error("world_size > 1 without an NCCL id: drive the iteration with cfr_solver_phase");
             return CFR_ERR_UNSUPPORTED;
         }
+        if (persist_ && iters > 0) return launch_persistent(iters);
         for (int64_t k = 0; k < iters; ++k) {
             if (gexec) CU(cudaGraphLaunch(gexec, stream));
             else {
@@ -2936,7 +3089,7 @@ struct Solver final : SolverBase {
     }
 
     cfr_status launches(int64_t* n) override {
-        *n = launches_per_iter;
+        *n = persist_ ? 1 : launches_per_iter;   // persistent: one launch per enqueue of T iterations
         return CFR_OK;
     }
 

@@ -74,3 +74,23 @@ def test_synthetic_small(cuda):
     run_pair(desc, 1, 64, 2, checks=("state",))
     desc = gamegen.synthetic(n_types=2, seed=5)
     run_pair(desc, 0, 32, 2, checks=("state",))
+
+
+@pytest.mark.parametrize("name", ["kuhn", "leduc", "goofspiel", "liars_dice"])
+def test_persistent_matches_per_level_launches(cuda, name):
+    """The persistent single-launch iteration (k_persist, grid barriers between
+    levels) and the per-level kernel launches give the same bits."""
+    import paper_2408_14778_b200 as pb
+    desc = gamegen.by_name(name)
+    g = pb.Game(desc)
+    T = 7 if name == "liars_dice" else 40
+    a = pb.Solver(g, variant="cfr+", precision=64, flags=pb.FLAG_PERSISTENT)
+    b = pb.Solver(g, variant="cfr+", precision=64)
+    assert a.launches_per_iteration() == 1 and b.launches_per_iteration() > 1
+    a.run(T)
+    b.run(T)
+    assert a.iteration == b.iteration == T
+    sa, sb = a.state(), b.state()
+    for k in ("regret", "snum", "sden"):
+        assert np.array_equal(sa[k], sb[k]), k
+    assert np.array_equal(a.average_strategy(), b.average_strategy())
