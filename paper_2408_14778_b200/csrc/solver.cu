@@ -1092,6 +1092,9 @@ struct StreamLevel {
     int o_pact, o_gsig;     // fused: parent actors, gathered incoming-edge sigma (reach area = parent rows)
     unsigned ndiv_m;        // p / n == (p * ndiv_m) >> ndiv_s (64-bit) for p < 2^16 (host-verified)
     int ndiv_s;
+    int umem;               // > 0: every infoset of the level has umem members (m / umem by udiv)
+    unsigned udiv_m;
+    int udiv_s;
     int o_sv, o_cm, o_rt, o_pos, o_pib, o_zs, o_ccnt, o_bar;          // work arrays / barriers
     int bytes;              // dynamic shared memory
     int last;
@@ -1199,7 +1202,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         // sigma (cp.async, completion counted on the same barrier); the parent /
         // edge indices of the next tile are prefetched into registers meanwhile.
         const int plane = tid - kStreamConsumers;
-        if (!L.fused && plane != 0) return;
+        if (!L.fused && plane != 0) return;   // lane 0 alone issues
         const int4* recs = reinterpret_cast<const int4*>(pool) + L.rec;
         const int* hs = pool + L.hs;
         constexpr int GMAX = kStreamConsumers / 32;   // members per lane (maxm <= kStreamConsumers)
@@ -1370,12 +1373,17 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
             R pc = (R)0, ph = (R)0;
             if (active) {
                 const long long node = (long long)snode[m];
-                int lo = 0, hi = nseg - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (hs[mid] - m0 <= m) lo = mid; else hi = mid - 1;
+                if (L.umem > 0) {
+                    // every infoset of the level has umem members: k = m / umem
+                    k = (int)(((unsigned long long)(unsigned)m * L.udiv_m) >> L.udiv_s);
+                } else {
+                    int lo = 0, hi = nseg - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (hs[mid] - m0 <= m) lo = mid; else hi = mid - 1;
+                    }
+                    k = lo;
                 }
-                k = lo;
                 R v[PC];
 #pragma unroll
                 for (int j = 0; j < PC; ++j) v[j] = (R)0;
@@ -1387,11 +1395,45 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                     using V = typename std::conditional<sizeof(R) == 8, double2, float4>::type;
                     constexpr int E = 16 / (int)sizeof(R);
                     const V* row4 = reinterpret_cast<const V*>(row);
-                    for (int a = 0; a < n; a += E) {
-                        const V u = row4[a / E];
-                        const R* ue = reinterpret_cast<const R*>(&u);
+                    if ((reinterpret_cast<unsigned long long>(sg) & 15ull) == 0) {
+                        // sigma row 16-byte aligned: vector loads of it too.  Row chunks
+                        // are read in pairs, each lane starting with chunk 2j + d, d =
+                        // bit 2 of the member: rows of 8 consecutive members then fall
+                        // in 8 distinct 16-byte bank groups (a row of an even number of
+                        // chunks would otherwise give 2-way conflicts); the additions
+                        // stay in ascending action order
+                        const V* sg4 = reinterpret_cast<const V*>(sg);
+                        const int d = (m >> 2) & 1;
+                        const int nc = n / E;
+                        int c = 0;
+                        for (; c + 1 < nc; c += 2) {
+                            const V p0 = row4[c + d];
+                            const V p1 = row4[c + 1 - d];
+                            const V x0 = sg4[c], x1 = sg4[c + 1];
+                            const R* ua = reinterpret_cast<const R*>(d ? &p1 : &p0);
+                            const R* ub = reinterpret_cast<const R*>(d ? &p0 : &p1);
+                            const R* xa = reinterpret_cast<const R*>(&x0);
+                            const R* xb = reinterpret_cast<const R*>(&x1);
 #pragma unroll
-                        for (int e = 0; e < E; ++e) v[0] = v[0] + sg[a + e] * ue[e];
+                            for (int e = 0; e < E; ++e) v[0] = v[0] + xa[e] * ua[e];
+#pragma unroll
+                            for (int e = 0; e < E; ++e) v[0] = v[0] + xb[e] * ub[e];
+                        }
+                        if (c < nc) {
+                            const V u = row4[c];
+                            const V x = sg4[c];
+                            const R* ue = reinterpret_cast<const R*>(&u);
+                            const R* xe = reinterpret_cast<const R*>(&x);
+#pragma unroll
+                            for (int e = 0; e < E; ++e) v[0] = v[0] + xe[e] * ue[e];
+                        }
+                    } else {
+                        for (int a = 0; a < n; a += E) {
+                            const V u = row4[a / E];
+                            const R* ue = reinterpret_cast<const R*>(&u);
+#pragma unroll
+                            for (int e = 0; e < E; ++e) v[0] = v[0] + sg[a + e] * ue[e];
+                        }
                     }
                 } else {
                     for (int a = 0; a < n; ++a) {
@@ -1400,6 +1442,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                         for (int j = 0; j < PC; ++j) v[j] = v[j] + x * row[a * PC + j];
                     }
                 }
+                SPROF(2);
 #pragma unroll
                 for (int j = 0; j < PC; ++j) {
                     if (!(L.debug & 4)) g.U[node * PC + j] = v[j];   // (debug bit 4: timing experiment)
@@ -1423,7 +1466,10 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                     ph = reach[(long long)m * rs + (L.compact ? 1 : P + i - 1)];
                 }
             }
+            SPROF(3);
             if (L.debug & 32) continue;   // timing experiment: no compaction
+            // a warp whose members all have zero reach has nothing to compact
+            if (__ballot_sync(0xffffffffu, active && (pc != (R)0 || ph != (R)0)) == 0u) continue;
             const int key = active ? k : -1;
             const unsigned grp = __match_any_sync(0xffffffffu, key);
             const int leader = __ffs(grp) - 1;
@@ -1440,13 +1486,15 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
             if (active && pc != (R)0) cm[(hs[k] - m0) + bc + __popc(nzc & lt)] = (short)m;
             if (active && ph != (R)0) cm[L.maxm + (hs[k] - m0) + bh + __popc(nzh & lt)] = (short)m;
         }
-        SPROF(2); consumers_sync(); SPROF(3);
+        SPROF(4); consumers_sync(); SPROF(5);
 
         // ---- phases B + C, a warp per LIVE infoset (no CTA barrier in between).
         // Live: some member has a nonzero pi_check (r~ may be nonzero) or pi_hat
         // (pi_bar may be nonzero).  For a dead infoset every term is an exact zero:
         // r~ = +0 and pi_bar = +0, so R, S_num, S_den and sigma keep their bits and
-        // its update (and its writes) are skipped.
+        // its update (and its writes) are skipped.  (Splitting a live infoset's
+        // members over several warps, combined after a CTA barrier, was measured
+        // slower: live infosets mostly have few live members.)
         const long long qt = L.q0 + (long long)hd.k0 * n;
         const long long ht = L.h0 + hd.k0;
         {
@@ -1469,10 +1517,10 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 const int col = (PC == 1) ? 0 : i - 1;
                 const int sb = hs[k] - m0;
                 const int cntc = ccnt[k], cnth = ccnt[L.maxseg + k];
-                const bool two = L.fused || L.compact;
-                const int oc = two ? 0 : i - 1, oh = two ? 1 : P + i - 1;   // pi_check / pi_hat in a reach row
                 const short* memc = cm + sb;
                 const short* memh = cm + L.maxm + sb;
+                const bool two = L.fused || L.compact;
+                const int oc = two ? 0 : i - 1, oh = two ? 1 : P + i - 1;   // pi_check / pi_hat in a reach row
                 // ---- phase B: exact sums (slices of integer-valued doubles combine
                 // exactly in any order)
                 for (int base = 0; base <= n; base += ipr) {
@@ -2086,6 +2134,22 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
             pool->insert(pool->end(), hs.begin(), hs.end());
         }
         if ((int64_t)f.maxseg * n + f.maxseg >= 65536) { out[L] = StreamLevel{}; continue; }   // item ids < 2^16
+        {
+            // uniform member count: member -> infoset by multiply-shift (verified)
+            int um = hs[1] - hs[0];
+            for (int k = 1; k < nh && um > 0; ++k)
+                if (hs[k + 1] - hs[k] != um) um = 0;
+            if (um > 0) {
+                int l = 0;
+                while ((1 << l) < um) ++l;
+                f.udiv_s = 16 + l;
+                f.udiv_m = (unsigned)((((unsigned long long)1 << (16 + l)) + (unsigned long long)um - 1) / (unsigned long long)um);
+                bool uok = true;
+                for (unsigned x = 0; x < 65536u && uok; ++x)
+                    uok = (unsigned)(((unsigned long long)x * f.udiv_m) >> f.udiv_s) == x / (unsigned)um;
+                f.umem = uok ? um : 0;
+            }
+        }
         // the deepest decision level: no decision children, so no other forward
         // level reads its reach rows -- its forward pass runs inside this kernel
         f.fused = (fuse_forward && L == g.D - 1) ? 1 : 0;

@@ -27,7 +27,7 @@ f(buf.ctypes.data, 1)
 s.run(1)
 f(buf.ctypes.data, 1)
 tiles = int(buf[64])
-names = ["loop", "wait_full", "A_work", "A_barrier", "B_work", "B_barrier", "C_work", "C_end_barrier"]
+names = ["loop", "wait_full", "A_values", "A_store_reach", "A_compact", "A_barrier", "B+C", "end_barrier"]
 per = buf[:64].reshape(8, 8).astype(np.float64) / tiles
 print(f"tiles {tiles}; cycles per tile, per consumer warp (rows) and mark (columns):")
 print("warp " + " ".join(f"{n:>13s}" for n in names))
