@@ -18,12 +18,13 @@ tests.  Rules follow SURVEY.md Appendix C (they reproduce PAPER.md Table 7,
 P:659-673).
 """
 from .desc import GameDesc, Builder
-from .games import kuhn, leduc, liars_dice, goofspiel, random_game, chance_pm1, single_decision, signal_game
+from .games import (kuhn, leduc, liars_dice, goofspiel, random_game, chance_pm1, single_decision, signal_game,
+                    matrix_game)
 from .synthetic_tree import synthetic, synthetic_numpy, synthetic_counts, DEFAULT_C
 
 __all__ = [
     "GameDesc", "Builder", "kuhn", "leduc", "liars_dice", "goofspiel", "random_game",
-    "chance_pm1", "single_decision", "signal_game", "synthetic", "synthetic_numpy", "synthetic_counts", "DEFAULT_C",
+    "chance_pm1", "single_decision", "signal_game", "matrix_game", "synthetic", "synthetic_numpy", "synthetic_counts", "DEFAULT_C",
     "by_name",
 ]
 

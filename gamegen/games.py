@@ -307,3 +307,21 @@ def random_game(seed: int, max_depth: int = 6, max_branching: int = 4, num_playe
     r = b.node(-1, -1)
     gen(r, 0, {p: () for p in range(1, P + 1)})
     return b.build(zero_sum=bool(zero_sum))
+
+
+def matrix_game(A, name: str = "matrix") -> GameDesc:
+    """Two-player zero-sum normal-form game as a tree: player 1 picks a row at the
+    root, player 2 (one infoset: it does not see the row) picks a column; payoff
+    (A[r][c], -A[r][c]).  Strategies stay mixed, so CFR variants differ."""
+    A = [list(map(float, row)) for row in A]
+    m, k = len(A), len(A[0])
+    b = Builder(name, 2)
+    r = b.node(-1, -1)
+    b.set_player(r, 1, "rows", m)
+    for i in range(m):
+        c = b.node(r, i)
+        b.set_player(c, 2, "cols", k)
+        for j in range(k):
+            t = b.node(c, j)
+            b.set_terminal(t, [A[i][j], -A[i][j]])
+    return b.build(zero_sum=True)

@@ -6,7 +6,8 @@
 // helper with the CUDA product (paper_2408_14778_b200/); it reads the same
 // C-ABI input arrays (gamegen/) and nothing else.
 //
-// What it computes: plain recursive, simultaneous-update CFR and CFR+ following
+// What it computes: plain recursive, simultaneous-update CFR and CFR+ (and the
+// discounted variants LCFR / DCFR of reading Q18) following
 // the paper's DEFINITIONS step by step (SURVEY.md §8(c) "Oracle per iteration"):
 //   * Eq 1   u_check(v,i): recursive expected payoff, children summed
 //                        in ascending action order starting from +0.
@@ -162,24 +163,48 @@ struct Solver {
     }
 
     // Per-infoset update: Eq 10 running sums, Eq 8/15 cumulative regret (CFR or
-    // CFR+), Eq 9 regret matching.
+    // CFR+), Eq 9 regret matching.  Variants 2 (linear CFR) and 3 (DCFR with
+    // alpha = 3/2, beta = 0, gamma = 2) apply Brown & Sandholm's discounting to
+    // Eq 14 / Eq 15 as P:399 suggests (reading Q18): after iteration t's terms are
+    // added, positive regrets are multiplied by t^a/(t^a+1), the others by
+    // t^b/(t^b+1), and both average-strategy sums by (t/(t+1))^g.
     void update_infoset(int64_t h) {
         const int64_t qb = g.qbase[h], n = g.nact[h];
         const R pibar = (R)slice_decode(&acc_p[h * kSlices], 1);
-        const R w = (variant == 0) ? (R)1 : (R)t;
+        const R w = (variant == 1) ? (R)t : (R)1;
         const R wp = w * pibar;
+        // discount factors of iteration t (only correctly rounded operations)
+        const R tt = (R)t;
+        R dpos = (R)1, dneg = (R)1, dsum = (R)1;
+        if (variant == 2) {            // LCFR: alpha = beta = gamma = 1
+            const R f = tt / (tt + (R)1);
+            dpos = f;
+            dneg = f;
+            dsum = f;
+        } else if (variant == 3) {     // DCFR(3/2, 0, 2): t^(3/2) = t * sqrt(t), t^0 = 1
+            const R a = tt * std::sqrt(tt);
+            dpos = a / (a + (R)1);
+            dneg = (R)1 / ((R)1 + (R)1);
+            const R f = tt / (tt + (R)1);
+            dsum = f * f;
+        }
         for (int64_t a = 0; a < n; ++a) {
             const int64_t q = qb + a;
             const R rt = (R)slice_decode(&acc_r[q * kSlices], g.E);
             if (variant == 0) {
                 regret[q] = regret[q] + rt;
-            } else {
+            } else if (variant == 1) {
                 const R x = regret[q] + rt;
                 regret[q] = (x > (R)0) ? x : (R)0;
+            } else {
+                const R x = regret[q] + rt;
+                regret[q] = (x > (R)0) ? x * dpos : x * dneg;
             }
-            snum[q] = snum[q] + wp * sigma[q];
+            if (variant >= 2) snum[q] = (snum[q] + wp * sigma[q]) * dsum;
+            else snum[q] = snum[q] + wp * sigma[q];
         }
-        sden[h] = sden[h] + wp;
+        if (variant >= 2) sden[h] = (sden[h] + wp) * dsum;
+        else sden[h] = sden[h] + wp;
         R z = (R)0;
         for (int64_t a = 0; a < n; ++a) {
             const R r = regret[qb + a];
@@ -493,7 +518,7 @@ void oracle_qbase(void* hp, int64_t* qbase) {
 
 int oracle_run(void* hp, int32_t variant, int64_t T) {
     Handle* h = (Handle*)hp;
-    if (variant != 0 && variant != 1) { g_err = "bad variant"; return 1; }
+    if (variant < 0 || variant > 3) { g_err = "bad variant"; return 1; }
     if (h->precision == 32) run_impl((Solver<float>*)h->solver, variant, T);
     else run_impl((Solver<double>*)h->solver, variant, T);
     return 0;

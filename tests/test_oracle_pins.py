@@ -328,3 +328,64 @@ def test_goofspiel_symmetric_value_bound():
     o = oracle.Oracle(gamegen.goofspiel()).run(100, 1)
     ex = o.exploitability()
     assert abs(ex["ev"][0]) <= ex["nash_conv"]
+
+
+# ---- discounted variants (reading Q18: Brown & Sandholm's discounting of
+# Eq 14 / Eq 15).  LCFR = DCFR(1, 1, 1), DCFR = DCFR(3/2, 0, 2).
+BIASED_RPS = [[0.0, -1.0, 2.0], [1.0, 0.0, -1.0], [-1.0, 1.0, 0.0]]
+
+
+@pytest.mark.parametrize("variant,power", [(2, 1), (3, 2)])
+def test_discounted_average_is_polynomially_weighted(variant, power):
+    """Unrolling the discount (S + x_t) * (t/(t+1))^g gives S_T = sum_t x_t t^g / (T+1)^g:
+    the average strategy is the t^g-weighted average of the iterates (pi_bar is
+    constant in a matrix game, so it cancels).  The recursion in the oracle must
+    reproduce that closed form from its own recorded iterates."""
+    d = gamegen.matrix_game(BIASED_RPS)
+    o = oracle.Oracle(d, precision=64)
+    T = 60
+    sig = []
+    for _ in range(T):
+        sig.append(o.state()["sigma"].copy())
+        o.run(1, variant)
+    w = np.array([(t + 1) ** power for t in range(T)], dtype=np.float64)
+    want = (w[:, None] * np.array(sig)).sum(0) / w.sum()
+    got = o.average_strategy()
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-14), (got, want)
+    # the iterates genuinely change and mix (the weighting is exercised)
+    S = np.array(sig)
+    assert ((S > 0.05) & (S < 0.95)).any() and np.abs(S[T // 2] - S[-1]).max() > 1e-3
+
+
+def test_lcfr_regret_is_linearly_weighted():
+    """LCFR: R_T = sum_t t r~_t / (T+1).  With the opponent fixed to its recorded
+    strategies, player 1's instantaneous regrets in a matrix game are
+    r~_t(i) = (A sigma2_t)_i - sigma1_t . A sigma2_t (Eq 7 at the root, pi_check = 1)."""
+    A = np.array(BIASED_RPS)
+    d = gamegen.matrix_game(BIASED_RPS)
+    o = oracle.Oracle(d, precision=64)
+    qb = o.qbase
+    T = 40
+    acc = np.zeros(3)
+    for t in range(1, T + 1):
+        s = o.state()["sigma"]
+        # infoset ids follow the builder's order: 0 = rows (player 1), 1 = cols (player 2)
+        s1, s2 = s[qb[0]:qb[1]], s[qb[1]:qb[2]]
+        ua = A @ s2
+        acc += t * (ua - s1 @ ua)
+        o.run(1, 2)
+    R1 = o.state()["regret"][qb[0]:qb[1]]
+    assert np.allclose(R1, acc / (T + 1), rtol=1e-11, atol=1e-13), (R1, acc / (T + 1))
+
+
+@pytest.mark.parametrize("variant", [2, 3])
+def test_discounted_variants_converge_on_kuhn(variant):
+    d = gamegen.kuhn(2)
+    o = oracle.Oracle(d, precision=64)
+    nc = []
+    for T in (10, 100, 1000):
+        o.run(T - o.state()["t"], variant)
+        nc.append(o.exploitability()["nash_conv"])
+    assert nc[0] > nc[1] > nc[2] and nc[2] < 2.5e-2, nc   # simultaneous updates: ~vanilla rate
+    ev = o.expected_values()[0]
+    assert abs(ev + 1.0 / 18.0) <= nc[2], (ev, nc)
