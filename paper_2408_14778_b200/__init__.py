@@ -29,7 +29,7 @@ def nccl_unique_id() -> bytes:
     _native.check(L.cfr_nccl_unique_id(buf))
     return buf.raw
 
-CFR, CFR_PLUS = 0, 1
+CFR, CFR_PLUS, CFR_LINEAR, CFR_DISCOUNTED = 0, 1, 2, 3
 # cfr_solver_config.flags (include/cfr_b200.h)
 FLAG_NO_GRAPH = 1
 FLAG_PERSISTENT = 2
@@ -134,7 +134,8 @@ class Solver:
         L = load()
         self._L = L
         self.game = game
-        v = {"cfr": CFR, "vanilla": CFR, "cfr+": CFR_PLUS, "cfrplus": CFR_PLUS}.get(variant, variant)
+        v = {"cfr": CFR, "vanilla": CFR, "cfr+": CFR_PLUS, "cfrplus": CFR_PLUS, "lcfr": CFR_LINEAR,
+             "linear": CFR_LINEAR, "dcfr": CFR_DISCOUNTED, "discounted": CFR_DISCOUNTED}.get(variant, variant)
         self.cfg = _native.SolverConfigC(int(v), int(precision), int(flags), 0)
         self.precision = int(precision)
         self.rank, self.world_size = int(rank), int(world_size)
@@ -193,13 +194,21 @@ class Solver:
         return int(t.value)
 
     # -- readbacks (caller (h, a) order)
-    def average_strategy(self) -> np.ndarray:
-        out = np.empty(self.Q)
+    def _out_buf(self, out):
+        if out is None:
+            return np.empty(self.Q)
+        if out.dtype != np.float64 or out.shape != (self.Q,) or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a C-contiguous float64 array of shape ({self.Q},)")
+        return out
+
+    def average_strategy(self, out: np.ndarray | None = None) -> np.ndarray:
+        """sigma_bar in caller (h, a) order; `out` (float64[Q], C-contiguous) is reused if given."""
+        out = self._out_buf(out)
         _native.check(self._L.cfr_solver_average_strategy(self._h, _ptr(out)))
         return out
 
-    def current_strategy(self) -> np.ndarray:
-        out = np.empty(self.Q)
+    def current_strategy(self, out: np.ndarray | None = None) -> np.ndarray:
+        out = self._out_buf(out)
         _native.check(self._L.cfr_solver_current_strategy(self._h, _ptr(out)))
         return out
 

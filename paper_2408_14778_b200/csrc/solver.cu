@@ -202,6 +202,56 @@ __device__ __forceinline__ bool finite_(R x) {
     return isfinite(x);
 }
 
+// Per-iteration update rule (cfr_solver_config.variant): 0 CFR (Eq 8/15
+// cumulative, reading Q4), 1 CFR+ (RM+, w_t = t; reading Q6), 2 linear CFR and 3
+// DCFR(3/2, 0, 2) -- Brown & Sandholm's discounting of Eq 14/15 (reading
+// Q18): after iteration t's terms are added, positive regrets x t^a/(t^a+1),
+// others x t^b/(t^b+1), both average-strategy sums x (t/(t+1))^g.  Only correctly
+// rounded operations (t^(3/2) = t * sqrt(t)), so CPU and GPU agree bit for bit.
+template <class R>
+struct Upd {
+    int variant;
+    R w;                  // weight of pi_bar inside the average sums: t for CFR+, else 1
+    R dpos, dneg, dsum;   // discount factors (variants 2, 3)
+};
+template <class R>
+__device__ __forceinline__ Upd<R> make_upd(int variant, long long t) {
+    Upd<R> u;
+    u.variant = variant;
+    u.w = (variant == 1) ? (R)t : (R)1;
+    u.dpos = u.dneg = u.dsum = (R)1;
+    const R tt = (R)t;
+    if (variant == 2) {
+        const R f = tt / (tt + (R)1);
+        u.dpos = f;
+        u.dneg = f;
+        u.dsum = f;
+    } else if (variant == 3) {
+        const R a = tt * sqrt(tt);
+        u.dpos = a / (a + (R)1);
+        u.dneg = (R)1 / ((R)1 + (R)1);
+        const R f = tt / (tt + (R)1);
+        u.dsum = f * f;
+    }
+    return u;
+}
+template <class R>
+__device__ __forceinline__ R upd_regret(const Upd<R>& u, R reg, R rt) {
+    const R x = reg + rt;
+    if (u.variant == 0) return x;
+    if (u.variant == 1) {
+        R r = (x > (R)0) ? x : (R)0;
+        if (!finite_(x)) r = x;
+        return r;
+    }
+    return (x > (R)0) ? x * u.dpos : x * u.dneg;
+}
+// S_num (add = (w pi_bar) sigma) or S_den (add = w pi_bar)
+template <class R>
+__device__ __forceinline__ R upd_sum(const Upd<R>& u, R s, R add) {
+    return (u.variant >= 2) ? (s + add) * u.dsum : s + add;
+}
+
 // ------------------------------------------------------------ forward pass
 // Decision nodes of one depth in canonical order (streaming reads of the
 // parents' rows, streaming writes).  Eq 2: pi_check(v,i) =
@@ -659,7 +709,8 @@ __device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict_
     }
 
     // ---- phase C: fused update of complete single-depth infosets
-    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
+    const Upd<R> up = make_upd<R>(g.variant, t_iter);
+    const R w = up.w;
     if (!sig_staged) {   // split tile: every segment is deferred
         if (last) {
             __syncthreads();
@@ -672,23 +723,16 @@ __device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict_
         if (!sm.seg[k].fused) continue;
         const long long q = sm.seg[k].qb + (p - sm.soff[k]);
         const R r_t = rt[p];
-        R r;
-        if (g.variant == 0) {
-            r = sm.sreg[p] + r_t;                       // Eq 8/15, cumulative (Q4)
-        } else {
-            const R x = sm.sreg[p] + r_t;               // CFR+ (Q6)
-            r = (x > (R)0) ? x : (R)0;
-            if (!finite_(x)) r = x;
-        }
+        const R r = upd_regret(up, sm.sreg[p], r_t);   // Eq 8/15 (Q4) / CFR+ (Q6) / Q18
         g.regret[q] = r;
         const R wp = w * sm.pib[k];
-        g.snum[q] = sm.ssn[p] + wp * sm.ssig[p];        // Eq 10 numerator
+        g.snum[q] = upd_sum(up, sm.ssn[p], wp * sm.ssig[p]);   // Eq 10 numerator
         pos[p] = (r > (R)0) ? r : (R)0;
     }
     __syncthreads();
     for (int k = tid; k < nseg; k += nth) {
         if (!sm.seg[k].fused) continue;
-        g.sden[sm.seg[k].h] = sm.sden[k] + w * sm.pib[k];   // Eq 10 denominator
+        g.sden[sm.seg[k].h] = upd_sum(up, sm.sden[k], w * sm.pib[k]);   // Eq 10 denominator
         R z = (R)0;
         for (int p = sm.soff[k]; p < sm.soff[k + 1]; ++p) z = z + pos[p];
         sm.zs[k] = z;
@@ -860,7 +904,8 @@ __global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, cons
     asm volatile("cp.async.commit_group;\n" ::);
     pdl_wait();
     const long long t_iter = g.ctrl[0] + 1;
-    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
+    const Upd<R> up = make_upd<R>(g.variant, t_iter);
+    const R w = up.w;
     cp_async_wait_all();
     __syncthreads();
     ISSUE(0, 0);
@@ -1019,22 +1064,15 @@ __global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, cons
             const int k = rpseg[p];
             const long long q = seg[k].qb + (p - seg[k].pair_off);
             const R r_t = rt[p];
-            R r;
-            if (g.variant == 0) {
-                r = sreg[p] + r_t;
-            } else {
-                const R x = sreg[p] + r_t;
-                r = (x > (R)0) ? x : (R)0;
-                if (!finite_(x)) r = x;
-            }
+            const R r = upd_regret(up, sreg[p], r_t);
             g.regret[q] = r;
             const R wp = w * pib_[k];
-            g.snum[q] = ssn[p] + wp * ssig[p];
+            g.snum[q] = upd_sum(up, ssn[p], wp * ssig[p]);
             pos[p] = (r > (R)0) ? r : (R)0;
         }
         __syncthreads();
         for (int k = tid; k < nseg; k += nth) {
-            g.sden[seg[k].h] = sden[k] + w * pib_[k];
+            g.sden[seg[k].h] = upd_sum(up, sden[k], w * pib_[k]);
             R z = (R)0;
             for (int p = seg[k].pair_off; p < seg[k].pair_off + seg[k].n; ++p) z = z + pos[p];
             zs_[k] = z;
@@ -1330,8 +1368,10 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
     R* const pib = reinterpret_cast<R*>(B + L.o_pib);
     int* const ccnt = reinterpret_cast<int*>(B + L.o_ccnt);
     const long long t_iter = g.ctrl[0] + 1;
-    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
+    const Upd<R> up = make_upd<R>(g.variant, t_iter);
+    const R w = up.w;
     bool bad = false;
+    const bool all_live = g.variant >= 2;   // discounting changes every infoset: no identity updates
     const R inv_n = (R)1 / (R)n;   // uniform strategy of the level's infosets (Eq 9, z = 0)
     const int rs = L.compact ? 2 : 2 * P;   // reach row stride in the stage (elements)
     unsigned long long live_h = 0, all_h = 0;   // updated / visited infosets (thread 0)
@@ -1499,8 +1539,8 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         const long long ht = L.h0 + hd.k0;
         {
             const int warp = tid >> 5;
-            const unsigned live =
-                __ballot_sync(0xffffffffu, lane < nseg && (ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0));
+            const unsigned live = __ballot_sync(
+                0xffffffffu, lane < nseg && (all_live || ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0));
             if (tid == 0) {
                 live_h += __popc(live);
                 all_h += nseg;
@@ -1571,17 +1611,10 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                     if (a < n) {
                         const int p = k * n + a;
                         const R r_t = rt[p];
-                        R r;
-                        if (g.variant == 0) {
-                            r = sreg[p] + r_t;                   // Eq 8/15, cumulative (Q4)
-                        } else {
-                            const R x = sreg[p] + r_t;           // CFR+ (Q6)
-                            r = (x > (R)0) ? x : (R)0;
-                            if (!finite_(x)) r = x;
-                        }
+                        const R r = upd_regret(up, sreg[p], r_t);   // Eq 8/15 (Q4) / CFR+ (Q6) / Q18
                         if (!(L.debug & 8)) {   // (debug bit 8: timing experiment)
                             g.regret[qt + p] = r;
-                            g.snum[qt + p] = ssn[p] + wp * ssig[p];  // Eq 10 numerator
+                            g.snum[qt + p] = upd_sum(up, ssn[p], wp * ssig[p]);  // Eq 10 numerator
                         }
                         pos[p] = (r > (R)0) ? r : (R)0;
                     }
@@ -1592,7 +1625,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
 #pragma unroll 4
                 for (int b = 0; b < n; ++b) z = z + pk[b];   // broadcast reads, ascending
                 if (lane == 0) {
-                    if (!(L.debug & 8)) g.sden[ht + k] = sden[k] + wp;   // Eq 10 denominator
+                    if (!(L.debug & 8)) g.sden[ht + k] = upd_sum(up, sden[k], wp);   // Eq 10 denominator
                     ccnt[k] = 0;                                 // compaction counters of the next tile
                     ccnt[L.maxseg + k] = 0;
                 }
@@ -1648,7 +1681,8 @@ __device__ __forceinline__ void deferred_body(const DG<R, I>& g, int last) {
     pdl_trigger();
     pdl_wait();
     const long long t_iter = g.ctrl[0] + 1;
-    const R w = (g.variant == 0) ? (R)1 : (R)t_iter;
+    const Upd<R> up = make_upd<R>(g.variant, t_iter);
+    const R w = up.w;
     bool bad = false;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < g.ndef; idx += stride) {
@@ -1673,18 +1707,10 @@ __device__ __forceinline__ void deferred_body(const DG<R, I>& g, int last) {
             g.acc_r[cq * 3 + 1] = 0;
             g.acc_r[cq * 3 + 2] = 0;
             const R rt = (R)xdec_ll(c0, c1, c2, g.rc);
-            R r;
-            if (g.variant == 0) {
-                r = g.regret[q] + rt;
-            } else {
-                const R x = g.regret[q] + rt;
-                r = (x > (R)0) ? x : (R)0;
-                if (!finite_(x)) r = x;
-            }
-            g.regret[q] = r;
-            g.snum[q] = g.snum[q] + wp * g.sig[q];
+            g.regret[q] = upd_regret(up, g.regret[q], rt);
+            g.snum[q] = upd_sum(up, g.snum[q], wp * g.sig[q]);
         }
-        g.sden[h] = g.sden[h] + wp;
+        g.sden[h] = upd_sum(up, g.sden[h], wp);
         for (int a = 0; a < n; ++a) {
             const R r = g.regret[qb + a];
             z = z + ((r > (R)0) ? r : (R)0);
@@ -3462,7 +3488,7 @@ cfr_status cfr_solver_create(const cfr_game* g, const cfr_solver_config* cfg, vo
                              void* stream, const cfr_dist* dist, cfr_solver** out) {
     if (!g || !cfg || !out || !workspace) { cfrb_set_error("NULL argument"); return CFR_ERR_INVALID_ARG; }
     *out = nullptr;
-    if (cfg->variant != CFR_VANILLA && cfg->variant != CFR_PLUS) { cfrb_set_error("bad variant"); return CFR_ERR_INVALID_ARG; }
+    if (cfg->variant < CFR_VANILLA || cfg->variant > CFR_DISCOUNTED) { cfrb_set_error("bad variant"); return CFR_ERR_INVALID_ARG; }
     if (cfg->precision != 64 && cfg->precision != 32) { cfrb_set_error("precision must be 64 or 32"); return CFR_ERR_INVALID_ARG; }
     const Game* local = nullptr;
     const ShardInfo* info = nullptr;

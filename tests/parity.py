@@ -48,7 +48,7 @@ def run_pair(desc, variant: int, precision: int, T: int, device=None, flags=0, c
     o.run(T, variant)
     if solver is None:
         g = pb.Game(desc)
-        solver = pb.Solver(g, variant="cfr+" if variant else "cfr", precision=precision,
+        solver = pb.Solver(g, variant=int(variant), precision=precision,
                            device=device or "cuda", flags=flags)
     solver.run(T)
     assert solver.iteration == o.state()["t"]

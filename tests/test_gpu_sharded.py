@@ -19,7 +19,7 @@ def run_world(desc, variant, precision, T, world, shard_prefix=None):
     if shard_prefix is not None:      # ranks load their own view from shard files
         g.save_shards(world, shard_prefix)
         games = [pb.Game.load_shard(shard_prefix, r, world) for r in range(world)]
-    ss = [pb.Solver(games[r], variant="cfr+" if variant else "cfr", precision=precision, rank=r, world_size=world)
+    ss = [pb.Solver(games[r], variant=int(variant), precision=precision, rank=r, world_size=world)
           for r in range(world)]
 
     def allreduce(which):
@@ -57,7 +57,8 @@ def run_world(desc, variant, precision, T, world, shard_prefix=None):
 
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("name,variant,precision,T", [("leduc", 1, 64, 30), ("leduc", 0, 32, 30),
-                                                       ("goofspiel", 1, 64, 10), ("kuhn3", 0, 64, 20)])
+                                                       ("goofspiel", 1, 64, 10), ("kuhn3", 0, 64, 20),
+                                                       ("leduc", 3, 64, 20), ("goofspiel", 2, 32, 8)])
 def test_sharded_bit_identical_to_oracle(cuda, name, variant, precision, T, world):
     desc = gamegen.by_name(name)
     o = oracle.Oracle(desc, precision=precision).run(T, variant)
