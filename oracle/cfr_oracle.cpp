@@ -171,7 +171,7 @@ struct Solver {
     void update_infoset(int64_t h) {
         const int64_t qb = g.qbase[h], n = g.nact[h];
         const R pibar = (R)slice_decode(&acc_p[h * kSlices], 1);
-        const R w = (variant == 1) ? (R)t : (R)1;
+        const R w = (variant == 1 || variant == 4) ? (R)t : (R)1;
         const R wp = w * pibar;
         // discount factors of iteration t (only correctly rounded operations)
         const R tt = (R)t;
@@ -193,17 +193,17 @@ struct Solver {
             const R rt = (R)slice_decode(&acc_r[q * kSlices], g.E);
             if (variant == 0) {
                 regret[q] = regret[q] + rt;
-            } else if (variant == 1) {
+            } else if (variant == 1 || variant == 4) {
                 const R x = regret[q] + rt;
                 regret[q] = (x > (R)0) ? x : (R)0;
             } else {
                 const R x = regret[q] + rt;
                 regret[q] = (x > (R)0) ? x * dpos : x * dneg;
             }
-            if (variant >= 2) snum[q] = (snum[q] + wp * sigma[q]) * dsum;
+            if (variant == 2 || variant == 3) snum[q] = (snum[q] + wp * sigma[q]) * dsum;
             else snum[q] = snum[q] + wp * sigma[q];
         }
-        if (variant >= 2) sden[h] = (sden[h] + wp) * dsum;
+        if (variant == 2 || variant == 3) sden[h] = (sden[h] + wp) * dsum;
         else sden[h] = sden[h] + wp;
         R z = (R)0;
         for (int64_t a = 0; a < n; ++a) {
@@ -217,15 +217,24 @@ struct Solver {
         }
     }
 
+    // One iteration.  Simultaneous updates (variants 0-3): one walk, every infoset
+    // updated.  Variant 4 = CFR+ with ALTERNATING updates (Tammelin's published
+    // form, reading Q19): for players i = 1..P in turn, a full walk under the
+    // current profile (already holding the players updated earlier this
+    // iteration), then only player i's infosets are updated (RM+, w_t = t).
     void iterate() {
         t += 1;
-        std::fill(acc_r.begin(), acc_r.end(), 0);
-        std::fill(acc_p.begin(), acc_p.end(), 0);
-        R pc[kMaxP], ph[kMaxP], out[kMaxP];
-        for (int j = 0; j < g.P; ++j) { pc[j] = (R)1; ph[j] = (R)1; }
-        sp = 0;
-        walk(g.root, pc, ph, out);
-        for (int64_t h = 0; h < g.H; ++h) update_infoset(h);
+        const int passes = (variant == 4) ? g.P : 1;
+        for (int pass = 1; pass <= passes; ++pass) {
+            std::fill(acc_r.begin(), acc_r.end(), 0);
+            std::fill(acc_p.begin(), acc_p.end(), 0);
+            R pc[kMaxP], ph[kMaxP], out[kMaxP];
+            for (int j = 0; j < g.P; ++j) { pc[j] = (R)1; ph[j] = (R)1; }
+            sp = 0;
+            walk(g.root, pc, ph, out);
+            for (int64_t h = 0; h < g.H; ++h)
+                if (variant != 4 || g.owner[h] == pass) update_infoset(h);
+        }
     }
 
     void average(std::vector<R>& avg) const {
@@ -518,7 +527,7 @@ void oracle_qbase(void* hp, int64_t* qbase) {
 
 int oracle_run(void* hp, int32_t variant, int64_t T) {
     Handle* h = (Handle*)hp;
-    if (variant < 0 || variant > 3) { g_err = "bad variant"; return 1; }
+    if (variant < 0 || variant > 4) { g_err = "bad variant"; return 1; }
     if (h->precision == 32) run_impl((Solver<float>*)h->solver, variant, T);
     else run_impl((Solver<double>*)h->solver, variant, T);
     return 0;

@@ -389,3 +389,41 @@ def test_discounted_variants_converge_on_kuhn(variant):
     assert nc[0] > nc[1] > nc[2] and nc[2] < 2.5e-2, nc   # simultaneous updates: ~vanilla rate
     ev = o.expected_values()[0]
     assert abs(ev + 1.0 / 18.0) <= nc[2], (ev, nc)
+
+
+# ---- CFR+ with alternating updates (variant 4, reading Q19)
+def test_alternating_equals_simultaneous_for_one_player():
+    """With one player there is nothing to alternate: variant 4 == CFR+ bit for bit."""
+    d = gamegen.single_decision()
+    a = oracle.Oracle(d).run(7, 4).state()
+    b = oracle.Oracle(d).run(7, 1).state()
+    for k in ("sigma", "regret", "snum", "sden"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_alternating_first_iteration_matrix_game():
+    """Iteration 1 on a matrix game by direct enumeration: player 1 updates against
+    the uniform column mix; player 2 then updates against player 1's NEW strategy."""
+    A = np.array(BIASED_RPS)
+    d = gamegen.matrix_game(BIASED_RPS)
+    o = oracle.Oracle(d).run(1, 4)
+    qb = o.qbase
+    st = o.state()
+    s2 = np.full(3, 1 / 3)
+    u1 = A @ s2
+    r1 = np.maximum(u1 - np.full(3, 1 / 3) @ u1, 0.0)
+    s1_new = r1 / r1.sum()
+    u2 = -(s1_new @ A)                     # player 2's payoff per column
+    r2 = np.maximum(u2 - s2 @ u2, 0.0)
+    s2_new = r2 / r2.sum() if r2.sum() > 0 else np.full(3, 1 / 3)
+    assert np.allclose(st["regret"][qb[0]:qb[1]], r1, atol=1e-14)
+    assert np.allclose(st["regret"][qb[1]:qb[2]], r2, atol=1e-14)   # members weighted by pi_check = sigma1_new(row)
+    assert np.allclose(st["sigma"][qb[0]:qb[1]], s1_new, atol=1e-14)
+    assert np.allclose(st["sigma"][qb[1]:qb[2]], s2_new, atol=1e-14)
+
+
+def test_alternating_cfr_plus_converges_faster_on_kuhn():
+    d = gamegen.kuhn(2)
+    alt = oracle.Oracle(d).run(1000, 4).exploitability()["nash_conv"]
+    sim = oracle.Oracle(d).run(1000, 1).exploitability()["nash_conv"]
+    assert alt < sim and alt < 3e-3, (alt, sim)
