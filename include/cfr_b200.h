@@ -112,10 +112,14 @@ cfr_status cfr_game_canonical(const cfr_game* g, int64_t* canon_of_input, int64_
  * apply Brown & Sandholm's discounting to Eq 14/15 (DESIGN.md reading
  * Q18): after iteration t, positive regrets x t^a/(t^a+1), the others x
  * t^b/(t^b+1), the average-strategy sums x (t/(t+1))^g; LCFR is a = b = g = 1. */
-typedef enum { CFR_VANILLA = 0, CFR_PLUS = 1, CFR_LINEAR = 2, CFR_DISCOUNTED = 3 } cfr_variant;
+/* CFR_PLUS_ALT: CFR+ with alternating updates (Tammelin; reading Q19):
+ * per iteration one full pass per player, each updating only that player's
+ * infosets under the profile current at that point. */
+typedef enum { CFR_VANILLA = 0, CFR_PLUS = 1, CFR_LINEAR = 2, CFR_DISCOUNTED = 3, CFR_PLUS_ALT = 4 } cfr_variant;
 
 typedef struct {
-    int32_t variant;     /* cfr_variant: CFR (w_t = 1), CFR+ (RM+, w_t = t), LCFR, DCFR */
+    int32_t variant;     /* cfr_variant: CFR (w_t = 1), CFR+ (RM+, w_t = t), LCFR,   */
+                         /* DCFR, CFR+ with alternating updates                    */
     int32_t precision;   /* 64 (binary64) or 32 (binary32) working precision      */
     int32_t flags;       /* bit 0: disable CUDA-Graph capture (debug);            */
                          /* bit 1: run small games (<= 2^22 nodes) as ONE         */

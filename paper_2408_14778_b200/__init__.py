@@ -29,7 +29,7 @@ def nccl_unique_id() -> bytes:
     _native.check(L.cfr_nccl_unique_id(buf))
     return buf.raw
 
-CFR, CFR_PLUS, CFR_LINEAR, CFR_DISCOUNTED = 0, 1, 2, 3
+CFR, CFR_PLUS, CFR_LINEAR, CFR_DISCOUNTED, CFR_PLUS_ALT = 0, 1, 2, 3, 4
 # cfr_solver_config.flags (include/cfr_b200.h)
 FLAG_NO_GRAPH = 1
 FLAG_PERSISTENT = 2
@@ -135,7 +135,8 @@ class Solver:
         self._L = L
         self.game = game
         v = {"cfr": CFR, "vanilla": CFR, "cfr+": CFR_PLUS, "cfrplus": CFR_PLUS, "lcfr": CFR_LINEAR,
-             "linear": CFR_LINEAR, "dcfr": CFR_DISCOUNTED, "discounted": CFR_DISCOUNTED}.get(variant, variant)
+             "linear": CFR_LINEAR, "dcfr": CFR_DISCOUNTED, "discounted": CFR_DISCOUNTED,
+             "cfr+alt": CFR_PLUS_ALT, "alternating": CFR_PLUS_ALT}.get(variant, variant)
         self.cfg = _native.SolverConfigC(int(v), int(precision), int(flags), 0)
         self.precision = int(precision)
         self.rank, self.world_size = int(rank), int(world_size)

@@ -90,6 +90,7 @@ struct DG {
     long long ndef;
     int P;
     int variant;
+    int upd_player;               // alternating updates (variant 4): the player updated by this pass; 0 = all
     double sc0, rc[3];            // 2^(40-E), 2^(E-40k): regret / BR sums
     double scp0, rcp[3];          // same with E = 1: pi_bar sums
 };
@@ -203,7 +204,8 @@ __device__ __forceinline__ bool finite_(R x) {
 }
 
 // Per-iteration update rule (cfr_solver_config.variant): 0 CFR (Eq 8/15
-// cumulative, reading Q4), 1 CFR+ (RM+, w_t = t; reading Q6), 2 linear CFR and 3
+// cumulative, reading Q4), 1 CFR+ (RM+, w_t = t; reading Q6) and 4 its
+// alternating-update form (reading Q19: same rule, one player per pass), 2 linear CFR and 3
 // DCFR(3/2, 0, 2) -- Brown & Sandholm's discounting of Eq 14/15 (reading
 // Q18): after iteration t's terms are added, positive regrets x t^a/(t^a+1),
 // others x t^b/(t^b+1), both average-strategy sums x (t/(t+1))^g.  Only correctly
@@ -218,7 +220,7 @@ template <class R>
 __device__ __forceinline__ Upd<R> make_upd(int variant, long long t) {
     Upd<R> u;
     u.variant = variant;
-    u.w = (variant == 1) ? (R)t : (R)1;
+    u.w = (variant == 1 || variant == 4) ? (R)t : (R)1;
     u.dpos = u.dneg = u.dsum = (R)1;
     const R tt = (R)t;
     if (variant == 2) {
@@ -239,7 +241,7 @@ template <class R>
 __device__ __forceinline__ R upd_regret(const Upd<R>& u, R reg, R rt) {
     const R x = reg + rt;
     if (u.variant == 0) return x;
-    if (u.variant == 1) {
+    if (u.variant == 1 || u.variant == 4) {
         R r = (x > (R)0) ? x : (R)0;
         if (!finite_(x)) r = x;
         return r;
@@ -249,7 +251,7 @@ __device__ __forceinline__ R upd_regret(const Upd<R>& u, R reg, R rt) {
 // S_num (add = (w pi_bar) sigma) or S_den (add = w pi_bar)
 template <class R>
 __device__ __forceinline__ R upd_sum(const Upd<R>& u, R s, R add) {
-    return (u.variant >= 2) ? (s + add) * u.dsum : s + add;
+    return (u.variant == 2 || u.variant == 3) ? (s + add) * u.dsum : s + add;
 }
 
 // ------------------------------------------------------------ forward pass
@@ -718,9 +720,12 @@ __device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict_
         }
         return;
     }
+    auto upd_seg = [&](int k) {   // fused and (alternating updates) owned by this pass's player
+        return sm.seg[k].fused && (g.upd_player == 0 || sm.seg[k].owner == g.upd_player);
+    };
     for (int p = tid; p < T.npairs; p += nth) {
         const int k = sm.pseg[p];
-        if (!sm.seg[k].fused) continue;
+        if (!upd_seg(k)) continue;
         const long long q = sm.seg[k].qb + (p - sm.soff[k]);
         const R r_t = rt[p];
         const R r = upd_regret(up, sm.sreg[p], r_t);   // Eq 8/15 (Q4) / CFR+ (Q6) / Q18
@@ -731,7 +736,7 @@ __device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict_
     }
     __syncthreads();
     for (int k = tid; k < nseg; k += nth) {
-        if (!sm.seg[k].fused) continue;
+        if (!upd_seg(k)) continue;
         g.sden[sm.seg[k].h] = upd_sum(up, sm.sden[k], w * sm.pib[k]);   // Eq 10 denominator
         R z = (R)0;
         for (int p = sm.soff[k]; p < sm.soff[k + 1]; ++p) z = z + pos[p];
@@ -741,7 +746,7 @@ __device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict_
     bool bad = false;
     for (int p = tid; p < T.npairs; p += nth) {
         const int k = sm.pseg[p];
-        if (!sm.seg[k].fused) continue;
+        if (!upd_seg(k)) continue;
         const int a = p - sm.soff[k];
         const R z = sm.zs[k];
         const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)sm.seg[k].n;   // Eq 9
@@ -1062,6 +1067,7 @@ __global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, cons
         // phase C: fused update (Eq 8/15 or CFR+, Eq 10, Eq 9)
         for (int p = tid; p < npairs; p += nth) {
             const int k = rpseg[p];
+            if (g.upd_player != 0 && seg[k].owner != g.upd_player) continue;   // alternating updates
             const long long q = seg[k].qb + (p - seg[k].pair_off);
             const R r_t = rt[p];
             const R r = upd_regret(up, sreg[p], r_t);
@@ -1072,6 +1078,7 @@ __global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, cons
         }
         __syncthreads();
         for (int k = tid; k < nseg; k += nth) {
+            if (g.upd_player != 0 && seg[k].owner != g.upd_player) continue;
             g.sden[seg[k].h] = upd_sum(up, sden[k], w * pib_[k]);
             R z = (R)0;
             for (int p = seg[k].pair_off; p < seg[k].pair_off + seg[k].n; ++p) z = z + pos[p];
@@ -1080,6 +1087,7 @@ __global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, cons
         __syncthreads();
         for (int p = tid; p < npairs; p += nth) {
             const int k = rpseg[p];
+            if (g.upd_player != 0 && seg[k].owner != g.upd_player) continue;
             const int a = p - seg[k].pair_off;
             const R z = zs_[k];
             const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)seg[k].n;
@@ -1227,7 +1235,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
     }
     {
         int* ccnt = reinterpret_cast<int*>(B + L.o_ccnt);
-        for (int k = tid; k < 2 * L.maxseg; k += blockDim.x) ccnt[k] = 0;
+        for (int k = tid; k < 4 * L.maxseg; k += blockDim.x) ccnt[k] = 0;   // two tile buffers
     }
     __syncthreads();
     pdl_wait();
@@ -1366,7 +1374,10 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
     R* const rt = reinterpret_cast<R*>(B + L.o_rt);
     R* const pos = reinterpret_cast<R*>(B + L.o_pos);
     R* const pib = reinterpret_cast<R*>(B + L.o_pib);
-    int* const ccnt = reinterpret_cast<int*>(B + L.o_ccnt);
+    // compaction counters [pi_check | pi_hat][maxseg], double-buffered by tile parity:
+    // a tile's buffer is zeroed after its end barrier, while the next tile uses the other
+    int* const ccnt_buf = reinterpret_cast<int*>(B + L.o_ccnt);
+    int tpar = 0;
     const long long t_iter = g.ctrl[0] + 1;
     const Upd<R> up = make_upd<R>(g.variant, t_iter);
     const R w = up.w;
@@ -1381,6 +1392,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
     for (; t < L.ntiles; t += G) {
         unsigned char* S = B + (size_t)st * L.stage_bytes;
         const StreamHdr* hdp = reinterpret_cast<const StreamHdr*>(S);
+        int* const ccnt = ccnt_buf + tpar * 2 * L.maxseg;
         SPROF(0); mbar_wait(&full[st], ph & 1u); SPROF(1);
         const StreamHdr hd = *hdp;
         const R* rows = reinterpret_cast<const R*>(S + L.o_rows);
@@ -1400,6 +1412,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
             consumers_sync();
             if (tid == 0) mbar_arrive(&empty[st]);
             if (++st == L.stages) { st = 0; ++ph; }
+            tpar ^= 1;
             continue;
         }
 
@@ -1540,7 +1553,8 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         {
             const int warp = tid >> 5;
             const unsigned live = __ballot_sync(
-                0xffffffffu, lane < nseg && (all_live || ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0));
+                0xffffffffu, lane < nseg && (g.upd_player == 0 || own[lane] == g.upd_player) &&
+                                 (all_live || ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0));
             if (tid == 0) {
                 live_h += __popc(live);
                 all_h += nseg;
@@ -1624,11 +1638,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 const R* pk = pos + k * n;
 #pragma unroll 4
                 for (int b = 0; b < n; ++b) z = z + pk[b];   // broadcast reads, ascending
-                if (lane == 0) {
-                    if (!(L.debug & 8)) g.sden[ht + k] = upd_sum(up, sden[k], wp);   // Eq 10 denominator
-                    ccnt[k] = 0;                                 // compaction counters of the next tile
-                    ccnt[L.maxseg + k] = 0;
-                }
+                if (lane == 0 && !(L.debug & 8)) g.sden[ht + k] = upd_sum(up, sden[k], wp);   // Eq 10 denominator
                 for (int c = 0; c < n; c += 32) {
                     const int a = c + lane;
                     if (a < n) {
@@ -1643,6 +1653,8 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         SPROF(6); consumers_sync();   // every read of this stage is done
         SPROF(7);
         if (tid == 0) mbar_arrive(&empty[st]);
+        for (int k = tid; k < 2 * L.maxseg; k += kStreamConsumers) ccnt[k] = 0;   // for the tile after next
+        tpar ^= 1;
         if (++st == L.stages) { st = 0; ++ph; }
     }
 #ifdef CFR_STREAM_PROFILE
@@ -1695,6 +1707,11 @@ __device__ __forceinline__ void deferred_body(const DG<R, I>& g, int last) {
         g.acc_p[idx * 3 + 0] = 0;
         g.acc_p[idx * 3 + 1] = 0;
         g.acc_p[idx * 3 + 2] = 0;
+        if (g.upd_player != 0 && g.owner[h] != g.upd_player) {
+            // alternating updates: another player's infoset -- zero its sums only
+            for (int a = 0; a < 3 * n; ++a) g.acc_r[dq * 3 + a] = 0;
+            continue;
+        }
         const R pib = (R)xdec_ll(p0, p1, p2, g.rcp);
         const R wp = w * pib;
         R z = (R)0;
@@ -2076,7 +2093,7 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int ix, int stages
     f.o_pos = x; x += al((long long)maxpairs * w);
     f.o_pib = x; x += al((long long)f.maxseg * w);
     f.o_zs = x; x += al((long long)f.maxseg * w);
-    f.o_ccnt = x; x += al((long long)f.maxseg * 8);
+    f.o_ccnt = x; x += al((long long)f.maxseg * 16);   // 2 counters x 2 tile buffers
     f.o_bar = x; x += al(2 * stages * 8);
     f.bytes = x;
 }
@@ -2407,6 +2424,10 @@ struct Solver final : SolverBase {
             cfrb_set_error("non-zero-sum games with more than 4 players are not supported by the device kernels");
             return CFR_ERR_UNSUPPORTED;
         }
+        if (external && cfg.variant == CFR_PLUS_ALT) {
+            cfrb_set_error("alternating updates need the in-graph (NCCL) exchanges when sharded");
+            return CFR_ERR_UNSUPPORTED;
+        }
         use_graph = !(cfg.flags & CFR_FLAG_NO_GRAPH);
         use_fast_ = !(cfg.flags & CFR_FLAG_NO_PIPELINE);
         use_stream_ = !(cfg.flags & CFR_FLAG_NO_STREAM);
@@ -2450,6 +2471,7 @@ struct Solver final : SolverBase {
         dg.ndef = (long long)g.deferred_list.size();
         dg.P = g.P;
         dg.variant = cfg.variant;
+        dg.upd_player = 0;
         dg.sc0 = std::ldexp(1.0, 40 - E);
         dg.scp0 = std::ldexp(1.0, 40 - 1);
         for (int k = 0; k < 3; ++k) {
@@ -2715,7 +2737,8 @@ struct Solver final : SolverBase {
     cfr_status setup_persistent() {
         const Game& g = *gp;
         persist_ = false;
-        if (world > 1 || external || !(cfg.flags & CFR_FLAG_PERSISTENT) || g.NS == 0 || g.V > kPersistMaxNodes)
+        if (world > 1 || external || !(cfg.flags & CFR_FLAG_PERSISTENT) || g.NS == 0 || g.V > kPersistMaxNodes ||
+            cfg.variant == CFR_PLUS_ALT)
             return CFR_OK;
         int dev = 0, coop = 0;
         CU(cudaGetDevice(&dev));
@@ -2778,7 +2801,7 @@ struct Solver final : SolverBase {
         for (int L = g.D - 1; L >= 0; --L)
             if (g.tile_ptr[L + 1] > g.tile_ptr[L]) ++n;
         if (!g.deferred_list.empty()) ++n;
-        return n;
+        return (cfg.variant == CFR_PLUS_ALT) ? n * g.P : n;   // alternating updates: one pass per player
     }
 
     // the deepest level's reach rows in compact (actor-only) form: CFR iterations
@@ -2904,7 +2927,7 @@ struct Solver final : SolverBase {
             }
         const int stop = sharded() ? sh->cut : 0;
         for (int L = g.D - 1; L >= stop; --L) {
-            const int last = (mode == MODE_CFR && L == 0 && !has_def()) ? 1 : 0;
+            const int last = (mode == MODE_CFR && L == 0 && !has_def() && pass_final_) ? 1 : 0;
             if (mode == MODE_CFR) bwd_level<MODE_CFR>(st, sig, L, 0, last);
             else bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
             mark(st, ev, 1, L);
@@ -2923,7 +2946,7 @@ struct Solver final : SolverBase {
         const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148));
         k_cut_unpack<R><<<nb, 256, 0, st>>>(dg.U, at<long long>(plan.cutrow), at<R>(plan.cutbuf), n, g.Pc);
         for (int L = sh->cut - 1; L >= 0; --L) {
-            const int last = (mode == MODE_CFR && L == 0 && !has_def()) ? 1 : 0;
+            const int last = (mode == MODE_CFR && L == 0 && !has_def() && pass_final_) ? 1 : 0;
             if (mode == MODE_CFR) bwd_level<MODE_CFR>(st, sig, L, 0, last);
             else bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
             mark(st, ev, 1, L);
@@ -2931,7 +2954,7 @@ struct Solver final : SolverBase {
     }
     void launch_update(cudaStream_t st, std::vector<Mark>* ev) {
         if (has_def()) {
-            deferred_update(st, 1);
+            deferred_update(st, pass_final_ ? 1 : 0);
             mark(st, ev, 2, -1);
         }
     }
@@ -2946,21 +2969,34 @@ struct Solver final : SolverBase {
     }
     static ncclDataType_t rtype() { return sizeof(R) == 8 ? ncclFloat64 : ncclFloat32; }
 
+    // One iteration: one pass, or (alternating updates, variant 4) one pass per
+    // player, each a full forward + backward under the current profile updating
+    // only that player's infosets (reading Q19).  The iteration counter advances
+    // in the last kernel of the final pass.
+    int pass_final_ = 1;
     cfr_status launch_iteration(cudaStream_t st, std::vector<Mark>* ev) {
         const Game& g = *gp;
-        cfr_status s;
+        cfr_status s = CFR_OK;
+        const int passes = (cfg.variant == CFR_PLUS_ALT) ? g.P : 1;
         mark(st, ev, -1, 0);
-        launch_lower(st, MODE_CFR, dg.sig, ev);
-        if (sharded()) {
-            if ((s = nccl_sum(st, at<R>(plan.cutbuf), (size_t)ncut() * g.Pc, rtype()))) return s;
-            mark(st, ev, 3, -1);
-            launch_upper(st, MODE_CFR, dg.sig, ev);
+        for (int pass = 1; pass <= passes && !s; ++pass) {
+            dg.upd_player = (passes > 1) ? pass : 0;
+            pass_final_ = (pass == passes) ? 1 : 0;
+            launch_lower(st, MODE_CFR, dg.sig, ev);
+            if (sharded()) {
+                if ((s = nccl_sum(st, at<R>(plan.cutbuf), (size_t)ncut() * g.Pc, rtype()))) break;
+                mark(st, ev, 3, -1);
+                launch_upper(st, MODE_CFR, dg.sig, ev);
+            }
+            if (world > 1 && has_def()) {
+                if ((s = nccl_sum(st, dg.acc_r, acc_bytes() / 8, ncclInt64))) break;
+                mark(st, ev, 3, -1);
+            }
+            launch_update(st, ev);
         }
-        if (world > 1 && has_def()) {
-            if ((s = nccl_sum(st, dg.acc_r, acc_bytes() / 8, ncclInt64))) return s;
-            mark(st, ev, 3, -1);
-        }
-        launch_update(st, ev);
+        dg.upd_player = 0;
+        pass_final_ = 1;
+        if (s) return s;
         CU(cudaGetLastError());
         return CFR_OK;
     }
@@ -3488,7 +3524,7 @@ cfr_status cfr_solver_create(const cfr_game* g, const cfr_solver_config* cfg, vo
                              void* stream, const cfr_dist* dist, cfr_solver** out) {
     if (!g || !cfg || !out || !workspace) { cfrb_set_error("NULL argument"); return CFR_ERR_INVALID_ARG; }
     *out = nullptr;
-    if (cfg->variant < CFR_VANILLA || cfg->variant > CFR_DISCOUNTED) { cfrb_set_error("bad variant"); return CFR_ERR_INVALID_ARG; }
+    if (cfg->variant < CFR_VANILLA || cfg->variant > CFR_PLUS_ALT) { cfrb_set_error("bad variant"); return CFR_ERR_INVALID_ARG; }
     if (cfg->precision != 64 && cfg->precision != 32) { cfrb_set_error("precision must be 64 or 32"); return CFR_ERR_INVALID_ARG; }
     const Game* local = nullptr;
     const ShardInfo* info = nullptr;

@@ -35,3 +35,21 @@ def test_discounted_streaming_kernel(cuda, variant):
 
 def test_discounted_liars_dice(cuda):
     run_pair(gamegen.liars_dice(), 3, 64, 5)
+
+
+# ---- CFR+ with alternating updates (variant 4, reading Q19)
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("name", ["kuhn", "kuhn3", "leduc", "goofspiel"])
+def test_alternating_real_games(cuda, name, precision):
+    run_pair(gamegen.by_name(name), 4, precision, 25)
+
+
+def test_alternating_random_and_streaming(cuda):
+    for seed in range(6):
+        run_pair(gamegen.random_game(seed, num_players=2 + seed % 3), 4, 64, 12)
+    out, s, o = run_pair(gamegen.synthetic(n_types=3, seed=2), 4, 64, 3, flags=pb.FLAG_FORCE_STREAM,
+                         checks=("state",))
+    assert "k_bwd_stream" in s.level_kernels()
+    ref = pb.Solver(pb.Game(gamegen.kuhn(2)), variant="cfr+", precision=64)
+    alt = pb.Solver(pb.Game(gamegen.kuhn(2)), variant="cfr+alt", precision=64)
+    assert alt.launches_per_iteration() == 2 * ref.launches_per_iteration()
