@@ -64,3 +64,25 @@ def test_fused_forward_same_bits_as_separate_forward(cuda, precision):
     for k in ("regret", "snum", "sden"):
         assert np.array_equal(sa[k], sb[k]), k
     run_pair(desc, 1, precision, 5, flags=pb.FLAG_FORCE_STREAM | pb.FLAG_FUSED_FORWARD, checks=("state",))
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_stream_general_sum_and_multiplayer(cuda, precision):
+    """Value columns Pc > 1 (general-sum / 3-4 players) through the streaming kernel."""
+    for desc in (gamegen.kuhn(3), gamegen.signal_game()):
+        out, s, o = run_pair(desc, 1, precision, 12, flags=pb.FLAG_FORCE_STREAM)
+    hit = 0
+    for seed in range(12):
+        desc = gamegen.random_game(seed, num_players=2 + seed % 3)
+        out, s, o = run_pair(desc, seed % 5, precision, 8, flags=pb.FLAG_FORCE_STREAM)
+        hit += "k_bwd_stream" in s.level_kernels()
+    assert hit > 0
+
+
+def test_stream_degenerate_games(cuda):
+    """Tiny / degenerate trees under the forced streaming path: a single decision, a
+    chance-only game, one-infoset matrix game."""
+    for desc in (gamegen.single_decision(), gamegen.chance_pm1(2),
+                 gamegen.matrix_game([[1.0, -1.0], [-1.0, 1.0]])):
+        for variant in range(5):
+            run_pair(desc, variant, 64, 6, flags=pb.FLAG_FORCE_STREAM)
