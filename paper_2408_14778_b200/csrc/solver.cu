@@ -2195,7 +2195,7 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         }
         // the deepest decision level: no decision children, so no other forward
         // level reads its reach rows -- its forward pass runs inside this kernel
-        f.fused = (fuse_forward && L == g.D - 1) ? 1 : 0;
+        f.fused = (fuse_forward && L == g.D - 1 && f.maxm <= kStreamConsumers) ? 1 : 0;   // gathers: <= 8 per lane
         f.level = L;
         f.compact = (!f.fused && P == 2 && L == g.D - 1 && compact_reach) ? 1 : 0;
         stream_plan(f, P, Pc, w, ix, stages);
@@ -2567,7 +2567,9 @@ struct Solver final : SolverBase {
             int stages = 2;
             if (const char* e = std::getenv("CFR_STREAM_STAGES")) stages = std::max(2, std::min(8, std::atoi(e)));
             if (const char* e = std::getenv("CFR_STREAM_DEBUG")) stream_debug_ = std::atoi(e);
-            int tile = kStreamConsumers;
+            // members per tile: ~240 f64 / ~480 f32 keeps two CTAs (2-stage rings of
+            // ~50 KB) resident per SM (measured best, tools/stream_sweep.py)
+            int tile = (sizeof(R) == 4 && !(cfg.flags & CFR_FLAG_FUSED_FORWARD)) ? 2 * kStreamConsumers : kStreamConsumers;
             if (const char* e = std::getenv("CFR_STREAM_TILE")) tile = std::max(32, std::min(1024, std::atoi(e)));
             stream_ = stream_levels<R, I>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages, tile,
                                           (cfg.flags & CFR_FLAG_FUSED_FORWARD) != 0, std::getenv("CFR_NO_COMPACT") == nullptr);

@@ -12,6 +12,7 @@ import gamegen
 import paper_2408_14778_b200 as pb
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+prec = int(os.environ.get("SWEEP_PRECISION", "64"))
 configs = [tuple(int(x) for x in c.split(",")) for c in sys.argv[2:]] or [(240, 2, 0)]
 configs = [c if len(c) == 3 else (c[0], c[1], 0) for c in configs]
 d = gamegen.synthetic(n_types=n)
@@ -21,7 +22,7 @@ for tile, stages, dbg in configs:
     os.environ["CFR_STREAM_TILE"] = str(tile)
     os.environ["CFR_STREAM_STAGES"] = str(stages)
     os.environ["CFR_STREAM_DEBUG"] = str(dbg)
-    s = pb.Solver(g, variant="cfr+", precision=64)
+    s = pb.Solver(g, variant="cfr+", precision=prec)
     s.run(5) if dbg == 0 else s.enqueue(5)
     st = s.stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
