@@ -296,6 +296,15 @@ def main():
     live = None
     if 0 <= dom < len(cnt) and cnt[dom][2] > 0:
         live = round(cnt[dom][0] / cnt[dom][2], 4)
+    levels = []
+    for r in solver.level_profile():
+        e = {"level": r["level"], "bwd_kernel": r["bwd_kernel"], "bwd_ms": round(r["bwd_ms"], 4),
+             "fwd_ms": round(r["fwd_ms"], 4)}
+        if r["bwd_ms"] > 0 and r["bwd_bytes"] > 0:
+            e["bwd_GBps"] = round(r["bwd_bytes"] / (r["bwd_ms"] * 1e-3) / 1e9, 1)
+        if r["fwd_ms"] > 0 and r["fwd_bytes"] > 0:
+            e["fwd_GBps"] = round(r["fwd_bytes"] / (r["fwd_ms"] * 1e-3) / 1e9, 1)
+        levels.append(e)
     roofline = {
         "bound": "hbm", "kernel": f"{kernels[dom]} (parent level {dom})",
         "live_infoset_fraction": live,
@@ -305,6 +314,7 @@ def main():
         "algorithmic_bytes_per_launch": mb["dominant"], "launch_ms": dom_ms, "peak_source": peak_src,
         "step_share": round(dom_ms / (prof["fwd_ms"] + prof["bwd_ms"] + prof["deferred_ms"]), 4),
         "whole_step_model_GBps": round(mb["total"] / (ms * 1e-3) / 1e9, 1),
+        "levels": levels,
     }
 
     # ---- end to end through the public API with host buffers.  The host result

@@ -222,6 +222,11 @@ cfr_status cfr_solver_level_kernels(cfr_solver* s, int32_t* out, int32_t max_lev
  * (live fractions of the last cfr_solver_profile window). */
 cfr_status cfr_solver_counters(cfr_solver* s, int64_t* out /* [4 * max_levels] */, int32_t max_levels,
                                int32_t* num_levels);
+/* Per level L of the last cfr_solver_profile window: out[4L+0] forward ms (depth L),
+ * out[4L+1] backward ms (parent depth L), out[4L+2] / out[4L+3] the DESIGN.md §6
+ * model bytes of those two launches. */
+cfr_status cfr_solver_level_profile(cfr_solver* s, double* out /* [4 * max_levels] */, int32_t max_levels,
+                                    int32_t* num_levels);
 
 /* Writes a fresh ncclUniqueId (128 bytes) to `out` (rank 0 only). */
 cfr_status cfr_nccl_unique_id(void* out /* 128 bytes */);

@@ -288,6 +288,16 @@ class Solver:
         return dict(live_infosets=int(tot[0]), live_pairs=int(tot[1]), infosets=int(tot[2]), pairs=int(tot[3]),
                     per_level=per.tolist())
 
+    def level_profile(self) -> list:
+        """Per level of the last profile(): forward / backward ms and model bytes."""
+        out = np.zeros(4 * 64)
+        nl = ctypes.c_int32()
+        _native.check(self._L.cfr_solver_level_profile(self._h, _ptr(out), 64, ctypes.byref(nl)))
+        per = out[:4 * min(nl.value, 64)].reshape(-1, 4)
+        kern = self.level_kernels()
+        return [dict(level=L, fwd_ms=float(r[0]), bwd_ms=float(r[1]), fwd_bytes=float(r[2]), bwd_bytes=float(r[3]),
+                     bwd_kernel=kern[L] if L < len(kern) else None) for L, r in enumerate(per)]
+
     def model_bytes(self) -> dict:
         out = np.zeros(5)
         _native.check(self._L.cfr_solver_model_bytes(self._h, _ptr(out)))

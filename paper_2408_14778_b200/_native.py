@@ -128,6 +128,7 @@ SIGNATURES = {
     "cfr_solver_model_bytes": (ctypes.c_int, [_P, _P]),
     "cfr_solver_level_kernels": (ctypes.c_int, [_P, _P, _I32, _P]),
     "cfr_solver_counters": (ctypes.c_int, [_P, _P, _I32, _P]),
+    "cfr_solver_level_profile": (ctypes.c_int, [_P, _P, _I32, _P]),
     "cfr_nccl_unique_id": (ctypes.c_int, [_P]),
     "cfr_solver_phase": (ctypes.c_int, [_P, _I32, _P]),
     "cfr_solver_exchange_size": (ctypes.c_int, [_P, _I32, _P]),

@@ -1910,6 +1910,7 @@ struct SolverBase {
     virtual cfr_status model_bytes(double* out) = 0;
     virtual cfr_status level_kernels(int32_t* out, int32_t max_levels, int32_t* num_levels) = 0;
     virtual cfr_status counters(int64_t* out, int32_t max_levels, int32_t* num_levels) = 0;
+    virtual cfr_status level_profile(double* out, int32_t max_levels, int32_t* num_levels) = 0;
     virtual cfr_status phase(int ph, double* out) = 0;
     virtual cfr_status exchange_size(int which, size_t* bytes) = 0;
     virtual cfr_status exchange(int which, int put, void* host, size_t bytes) = 0;
@@ -3229,7 +3230,7 @@ struct Solver final : SolverBase {
             cfrb_set_error("profile needs NCCL or a single GPU");
             return CFR_ERR_UNSUPPORTED;
         }
-        std::vector<double> per_bwd(g.D, 0.0);
+        std::vector<double> per_bwd(g.D, 0.0), per_fwd(g.D, 0.0);
         std::vector<unsigned long long> c0, c1;
         cfr_status cs = read_lcnt(c0);
         if (cs) return cs;
@@ -3242,7 +3243,7 @@ struct Solver final : SolverBase {
                 float ms = 0;
                 cudaEventElapsedTime(&ms, ev[e - 1].e, ev[e].e);
                 switch (ev[e].tag) {
-                    case 0: out[0] += ms; break;
+                    case 0: out[0] += ms; per_fwd[ev[e].level] += ms; break;
                     case 1: out[1] += ms; per_bwd[ev[e].level] += ms; break;
                     case 2: out[2] += ms; break;
                     default: out[2] += ms; break;   // exchanges are reported with the update
@@ -3267,7 +3268,25 @@ struct Solver final : SolverBase {
         out[3] = per_bwd[dom] / iters;
         out[4] = dom;
         dom_level = dom;
+        prof_fwd_ms_.assign(g.D, 0.0);
+        prof_bwd_ms_.assign(g.D, 0.0);
+        for (int L = 0; L < g.D; ++L) {
+            prof_fwd_ms_[L] = per_fwd[L] / iters;
+            prof_bwd_ms_[L] = per_bwd[L] / iters;
+        }
         return sync();
+    }
+    std::vector<double> prof_fwd_ms_, prof_bwd_ms_;   // per level, last profile window
+    cfr_status level_profile(double* out, int32_t max_levels, int32_t* num_levels) override {
+        const Game& g = *gp;
+        *num_levels = g.D;
+        for (int L = 0; L < g.D && L < max_levels; ++L) {
+            out[4 * L + 0] = L < (int)prof_fwd_ms_.size() ? prof_fwd_ms_[L] : 0.0;
+            out[4 * L + 1] = L < (int)prof_bwd_ms_.size() ? prof_bwd_ms_[L] : 0.0;
+            out[4 * L + 2] = level_fwd_bytes(L);
+            out[4 * L + 3] = (g.tile_ptr[L + 1] > g.tile_ptr[L]) ? level_bwd_bytes(L) : 0.0;
+        }
+        return CFR_OK;
     }
 
     // ---- externally driven multi-GPU iteration (tests; world > 1 without NCCL)
@@ -3369,6 +3388,20 @@ struct Solver final : SolverBase {
     // Algorithmic DRAM bytes per iteration (DESIGN.md §6 byte model).
     int dom_level = -1;   // set by profile(): the backward level with the largest time
     std::vector<double> prof_live_;   // per level: live infosets, live pairs per iteration (last profile), -1 unknown
+    // forward pass of depth l: per decision node its parent slot, edge index and
+    // parent actor, its 2P factors written (compact: the actor and its 2 factors);
+    // every parent's 2P factors read once (parent rows and sigma are gathers made
+    // cache-local by the row-order slot numbering; sigma not counted)
+    double level_fwd_bytes(int l) const {
+        const Game& g = *gp;
+        if (l < 1 || l >= g.D || fwd_fused(l)) return 0.0;   // fused: inside the streaming kernel (not modelled)
+        const double w = sizeof(R), ix = sizeof(I);
+        const int P = g.P;
+        const double n = (double)(g.slot_ptr[l + 1] - g.slot_ptr[l]);
+        double b = fwd_compact(l) ? n * (2 * ix + 1 + 1 + 2 * w) : n * (2 * ix + 1 + 2 * P * w);
+        b += (double)(g.slot_ptr[l] - g.slot_ptr[l - 1]) * 2 * P * w;
+        return b;
+    }
     double level_bwd_bytes(int L) const {
         const Game& g = *gp;
         const double w = sizeof(R), ix = sizeof(I);
@@ -3416,17 +3449,7 @@ struct Solver final : SolverBase {
         const double w = sizeof(R), ix = sizeof(I);
         const int P = g.P;
         double fwd = 0, bwd = 0, upd = 0;
-        for (int l = 1; l < g.D; ++l) {
-            if (fwd_fused(l)) continue;   // inside the streaming backward kernel (not modelled)
-            const double n = (double)(g.slot_ptr[l + 1] - g.slot_ptr[l]);
-            // per decision node: parent slot + edge index + parent actor, its 2P factors
-            // written (compact: the actor and its 2 factors); every parent's 2P
-            // factors and the edge's sigma read once (parent rows and sigma are gathers
-            // made cache-local by the row-order slot numbering)
-            if (fwd_compact(l)) fwd += n * (2 * ix + 1 + 1 + 2 * w);
-            else fwd += n * (2 * ix + 1 + 2 * P * w);
-            fwd += (double)(g.slot_ptr[l] - g.slot_ptr[l - 1]) * 2 * P * w;
-        }
+        for (int l = 1; l < g.D; ++l) fwd += level_fwd_bytes(l);
         int big = 0;
         for (int L = g.D - 1; L >= 0; --L) {
             bwd += level_bwd_bytes(L);
@@ -3623,6 +3646,11 @@ cfr_status cfr_solver_level_kernels(cfr_solver* s, int32_t* out, int32_t max_lev
     CHK_S(s);
     if (!num_levels || (max_levels > 0 && !out)) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
     return s->impl->level_kernels(out, max_levels, num_levels);
+}
+cfr_status cfr_solver_level_profile(cfr_solver* s, double* out, int32_t max_levels, int32_t* num_levels) {
+    CHK_S(s);
+    if (!num_levels || (max_levels > 0 && !out)) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->level_profile(out, max_levels, num_levels);
 }
 cfr_status cfr_solver_counters(cfr_solver* s, int64_t* out, int32_t max_levels, int32_t* num_levels) {
     CHK_S(s);
