@@ -303,9 +303,21 @@ __device__ __forceinline__ void fwd_body(const DG<R, I>& g, const R* __restrict_
             R x[FW];
 #pragma unroll
             for (int k = 0; k < FW; ++k) {
-                const V2* src = reinterpret_cast<const V2*>(g.reach + p[k] * 4);
-                a[k] = src[0];   // pi_check(1), pi_check(2)
-                b[k] = src[1];   // pi_hat(1), pi_hat(2)
+                if (sizeof(R) == 8) {
+                    // the whole 32-byte parent row in one 256-bit load (one L1 request)
+                    double r0, r1, r2, r3;
+                    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n"
+                                 : "=d"(r0), "=d"(r1), "=d"(r2), "=d"(r3)
+                                 : "l"(g.reach + p[k] * 4));
+                    a[k].x = (R)r0;   // pi_check(1), pi_check(2)
+                    a[k].y = (R)r1;
+                    b[k].x = (R)r2;   // pi_hat(1), pi_hat(2)
+                    b[k].y = (R)r3;
+                } else {
+                    const V2* src = reinterpret_cast<const V2*>(g.reach + p[k] * 4);
+                    a[k] = src[0];
+                    b[k] = src[1];
+                }
                 x[k] = ld_hint(sig + e[k], pl);   // the edge's sigma: reused by every member of the parent's infoset
             }
 #pragma unroll
@@ -325,9 +337,17 @@ __device__ __forceinline__ void fwd_body(const DG<R, I>& g, const R* __restrict_
                     st_hint_v2(reinterpret_cast<V2*>(g.reach + d_begin * 4 + i * 2), c2, pf);
                     continue;
                 }
-                V2* dst = reinterpret_cast<V2*>(g.reach + (d_begin + i) * 4);
-                st_hint_v2(dst, ca, pf);
-                st_hint_v2(dst + 1, cb, pf);
+                if (sizeof(R) == 8) {
+                    // the 32-byte row in one 256-bit store
+                    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(
+                                     g.reach + (d_begin + i) * 4),
+                                 "d"((double)ca.x), "d"((double)ca.y), "d"((double)cb.x), "d"((double)cb.y), "l"(pf)
+                                 : "memory");
+                } else {
+                    V2* dst = reinterpret_cast<V2*>(g.reach + (d_begin + i) * 4);
+                    st_hint_v2(dst, ca, pf);
+                    st_hint_v2(dst + 1, cb, pf);
+                }
             }
         }
         return;
