@@ -132,7 +132,9 @@ typedef struct {
                          /* bit 5: use the streaming kernel on every eligible     */
                          /* level, however small (tests); bit 6: fuse the         */
                          /* deepest level's forward pass into its streaming       */
-                         /* backward kernel (experimental)                        */
+                         /* backward kernel (experimental); bit 7: disable the    */
+                         /* shared-memory single-CTA kernel of tiny games         */
+                         /* (k_tiny, default when the state fits one CTA)         */
     int32_t reserved;
 } cfr_solver_config;
 
@@ -143,6 +145,7 @@ typedef struct {
 #define CFR_FLAG_NO_STREAM 16
 #define CFR_FLAG_FORCE_STREAM 32
 #define CFR_FLAG_FUSED_FORWARD 64
+#define CFR_FLAG_NO_TINY 128
 
 /* Multi-GPU level sharding.  NULL or world_size == 1 means a
  * single GPU.  nccl_unique_id points to the 128-byte ncclUniqueId that rank 0

@@ -1843,6 +1843,168 @@ __global__ void __launch_bounds__(kTileSlots) k_persist(DG<R, I> g, const PLevel
     }
 }
 
+// ------------------------------------------------------------- tiny games
+// Games whose whole mutable state fits in one CTA's shared memory (Kuhn; Leduc in
+// f32) are bound by per-level latency, not bytes.  k_tiny runs T iterations in
+// ONE CTA: U, reach, sigma, R, S_num, S_den (and the per-level r~ / pi_bar) live
+// in shared memory; levels are separated by __syncthreads; read-only metadata
+// comes from global memory through L1.  Same operations, same order as the
+// per-level kernels (requires depth-homogeneous infosets: an infoset's members
+// are the contiguous slots mem_of[2h] .. mem_of[2h+1] of one level).
+struct TinyLevel {
+    long long s0, s1;   // slots of depth l
+    long long h0, h1;   // internal infosets at depth l (consecutive)
+};
+struct TinyPlan {
+    long long U, reach, sig, reg, snum, sden, rt, pib;   // element offsets in shared memory (R units)
+    long long nU, nreach, nsig, Q, H;
+    int bytes;
+};
+
+template <class R, class I, int PC>
+__global__ void __launch_bounds__(1024) k_tiny(DG<R, I> g, const TinyLevel* __restrict__ lv, const I* __restrict__ mem_of,
+                                                int D, long long T, TinyPlan tp) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R* const sm = reinterpret_cast<R*>(smem_raw);
+    R* const U = sm + tp.U;
+    R* const reach = sm + tp.reach;
+    R* const sig = sm + tp.sig;
+    R* const reg = sm + tp.reg;
+    R* const snum = sm + tp.snum;
+    R* const sden = sm + tp.sden;
+    R* const rtb = sm + tp.rt;
+    R* const pibb = sm + tp.pib;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int P = g.P;
+    pdl_trigger();
+    pdl_wait();
+    for (long long k = tid; k < tp.nU; k += nth) U[k] = g.U[k];
+    for (long long k = tid; k < tp.nreach; k += nth) reach[k] = g.reach[k];
+    for (long long k = tid; k < tp.nsig; k += nth) sig[k] = g.sig[k];
+    for (long long k = tid; k < tp.Q; k += nth) {
+        reg[k] = g.regret[k];
+        snum[k] = g.snum[k];
+    }
+    for (long long k = tid; k < tp.H; k += nth) sden[k] = g.sden[k];
+    __syncthreads();
+    long long t_iter = g.ctrl[0];
+    bool bad = false;
+    for (long long it = 0; it < T; ++it) {
+        ++t_iter;
+        const Upd<R> up = make_upd<R>(g.variant, t_iter);
+        const R w = up.w;
+        const int passes = (g.variant == 4) ? P : 1;
+        for (int pass = 1; pass <= passes; ++pass) {
+            const int upl = (passes > 1) ? pass : 0;
+            for (int l = 1; l < D; ++l) {   // forward (Eq 2, Eq 4 with reading Q1)
+                for (long long s = lv[l].s0 + tid; s < lv[l].s1; s += nth) {
+                    const long long p = (long long)g.f_parent[s];
+                    const R x = sig[g.f_e[s]];
+                    const int act = g.f_pact[s];
+                    for (int j = 0; j < P; ++j) {
+                        const R pc = reach[p * 2 * P + j], ph = reach[p * 2 * P + P + j];
+                        reach[s * 2 * P + j] = (act != j + 1) ? pc * x : pc;
+                        reach[s * 2 * P + P + j] = (act == j + 1) ? ph * x : ph;
+                    }
+                }
+                __syncthreads();
+            }
+            for (int L = D - 1; L >= 0; --L) {
+                for (long long s = lv[L].s0 + tid; s < lv[L].s1; s += nth) {   // values (Eq 1)
+                    const long long cb = (long long)g.s_cb[s], eb = (long long)g.s_ebase[s];
+                    const int nch = g.s_n[s];
+                    R v[PC];
+#pragma unroll
+                    for (int j = 0; j < PC; ++j) v[j] = (R)0;
+                    for (int a = 0; a < nch; ++a) {
+                        const R x = sig[eb + a];
+#pragma unroll
+                        for (int j = 0; j < PC; ++j) v[j] = v[j] + x * U[(cb + a) * PC + j];
+                    }
+                    const long long node = (long long)g.s_node[s];
+#pragma unroll
+                    for (int j = 0; j < PC; ++j) U[node * PC + j] = v[j];
+                }
+                __syncthreads();
+                const long long h0 = lv[L].h0, h1 = lv[L].h1;
+                if (h1 > h0) {
+                    const long long q0 = (long long)g.qbase[h0], q1 = (long long)g.qbase[h1];
+                    const long long items = (q1 - q0) + (h1 - h0);
+                    for (long long x = tid; x < items; x += nth) {   // exact sums
+                        double c0 = 0, c1 = 0, c2 = 0;
+                        if (x < q1 - q0) {
+                            const long long q = q0 + x;
+                            long long lo = h0, hi = h1 - 1;
+                            while (lo < hi) {
+                                const long long mid = (lo + hi + 1) >> 1;
+                                if ((long long)g.qbase[mid] <= q) lo = mid; else hi = mid - 1;
+                            }
+                            const long long h = lo;
+                            const int i = g.owner[h];
+                            if (upl != 0 && i != upl) continue;
+                            const int a = (int)(q - (long long)g.qbase[h]);
+                            const int col = (PC == 1) ? 0 : i - 1;
+                            for (long long d = (long long)mem_of[2 * h]; d < (long long)mem_of[2 * h + 1]; ++d) {
+                                const R pc = reach[d * 2 * P + (i - 1)];
+                                if (pc == (R)0) continue;   // exact zero terms
+                                const R u = U[((long long)g.s_cb[d] + a) * PC + col];
+                                const R v = U[(long long)g.s_node[d] * PC + col];
+                                xadd(c0, c1, c2, (double)(pc * (u - v)), g.sc0);
+                            }
+                            if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
+                            rtb[q] = (R)xdec(c0, c1, c2, g.rc);
+                        } else {
+                            const long long h = h0 + (x - (q1 - q0));
+                            const int i = g.owner[h];
+                            if (upl != 0 && i != upl) continue;
+                            for (long long d = (long long)mem_of[2 * h]; d < (long long)mem_of[2 * h + 1]; ++d)
+                                xadd(c0, c1, c2, (double)reach[d * 2 * P + P + (i - 1)], g.scp0);
+                            pibb[h] = (R)xdec(c0, c1, c2, g.rcp);
+                        }
+                    }
+                    __syncthreads();
+                    for (long long h = h0 + tid; h < h1; h += nth) {   // update (Eq 8/15 / CFR+ / Q18, Eq 10, Eq 9)
+                        const int i = g.owner[h];
+                        if (upl != 0 && i != upl) continue;
+                        const long long qb = (long long)g.qbase[h];
+                        const int n = (int)((long long)g.qbase[h + 1] - qb);
+                        const R wp = w * pibb[h];
+                        R z = (R)0;
+                        for (int a = 0; a < n; ++a) {
+                            const long long q = qb + a;
+                            const R r = upd_regret(up, reg[q], rtb[q]);
+                            reg[q] = r;
+                            snum[q] = upd_sum(up, snum[q], wp * sig[q]);
+                            z = z + ((r > (R)0) ? r : (R)0);
+                        }
+                        sden[h] = upd_sum(up, sden[h], wp);
+                        for (int a = 0; a < n; ++a) {
+                            const long long q = qb + a;
+                            const R r = reg[q];
+                            const R pos = (r > (R)0) ? r : (R)0;
+                            const R nsig = (z > (R)0) ? pos / z : (R)1 / (R)n;
+                            sig[q] = nsig;
+                            if (!finite_(rtb[q]) || !finite_(nsig) || !finite_(z)) bad = true;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // write the state back (readbacks and later launches read it from global)
+    for (long long k = tid; k < tp.nU; k += nth) g.U[k] = U[k];
+    for (long long k = tid; k < tp.nreach; k += nth) g.reach[k] = reach[k];
+    for (long long k = tid; k < tp.nsig; k += nth) g.sig[k] = sig[k];
+    for (long long k = tid; k < tp.Q; k += nth) {
+        g.regret[k] = reg[k];
+        g.snum[k] = snum[k];
+    }
+    for (long long k = tid; k < tp.H; k += nth) g.sden[k] = sden[k];
+    if (bad) atomicMin(&g.ctrl[1], t_iter);
+    if (tid == 0) g.ctrl[0] = t_iter;
+}
+
 // sigma_bar (Eq 10, reading Q5) into an evaluation strategy buffer: S_num/S_den,
 // uniform where S_den = 0.  Chance part copied.
 template <class R, class I>
@@ -2250,7 +2412,7 @@ struct Plan {
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, ctrl, lcnt, out;
-    size_t cutbuf, cutrow, cutown, report, pool, spool, plev, gbar;
+    size_t cutbuf, cutrow, cutown, report, pool, spool, plev, gbar, tlev, tmem_of;
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
         Layout L;
@@ -2293,6 +2455,8 @@ struct Plan {
         spool = L.take<int>(stream_pool_bound(g));
         plev = L.take<PLevel>((size_t)g.D + 1);
         gbar = L.take<unsigned>(4);
+        tlev = L.take<TinyLevel>((size_t)g.D + 1);
+        tmem_of = L.take<I>(g.V <= (int64_t(1) << 20) ? 2 * H + 2 : 2);
         total = L.off + 256;
     }
 };
@@ -2320,6 +2484,8 @@ struct Solver final : SolverBase {
     int64_t launches_per_iter = 0;
     bool use_graph = true;
     bool persist_ = false;        // small game: whole iterations in one cooperative launch (k_persist)
+    bool tiny_ = false;           // tiny game: whole iterations in one CTA, state in shared memory (k_tiny)
+    TinyPlan tiny_plan_{};
     int persist_grid_ = 0, persist_smem_ = 0;
     bool use_fast_ = true;
     bool use_stream_ = true;
@@ -2709,6 +2875,7 @@ struct Solver final : SolverBase {
         {
             cfr_status ps = setup_persistent();
             if (ps) return ps;
+            if ((ps = setup_tiny())) return ps;
         }
         if (use_graph && g.NS > 0 && !external) {
             CU(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
@@ -2815,6 +2982,97 @@ struct Solver final : SolverBase {
         return CFR_OK;
     }
     bool has_def_() const { return !gp->deferred_list.empty(); }
+
+    void* tiny_fn() const {
+        switch (gp->Pc) {
+            case 1: return (void*)k_tiny<R, I, 1>;
+            case 2: return (void*)k_tiny<R, I, 2>;
+            case 3: return (void*)k_tiny<R, I, 3>;
+            default: return (void*)k_tiny<R, I, 4>;
+        }
+    }
+    // Tiny-game mode (k_tiny): single-GPU, depth-homogeneous games whose mutable
+    // state fits one CTA's shared memory.  On by default (CFR_FLAG_NO_TINY to opt out).
+    cfr_status setup_tiny() {
+        const Game& g = *gp;
+        tiny_ = false;
+        if (world > 1 || external || persist_ || (cfg.flags & CFR_FLAG_NO_TINY) || !g.depth_homogeneous || g.NS == 0)
+            return CFR_OK;
+        const long long nU = (long long)(plan_u_rows()) * g.Pc, nreach = 2LL * g.P * g.NS, nsig = g.Q + g.C;
+        TinyPlan tp{};
+        long long o = 0;
+        auto take = [&](long long n) { const long long r = o; o += (n + 1) & ~1LL; return r; };   // 16-byte aligned
+        tp.U = take(nU);
+        tp.reach = take(nreach);
+        tp.sig = take(nsig);
+        tp.reg = take(g.Q);
+        tp.snum = take(g.Q);
+        tp.sden = take(g.H);
+        tp.rt = take(g.Q);
+        tp.pib = take(g.H);
+        tp.nU = nU;
+        tp.nreach = nreach;
+        tp.nsig = nsig;
+        tp.Q = g.Q;
+        tp.H = g.H;
+        const long long bytes = o * (long long)sizeof(R);
+        int dev = 0, optin = 0;
+        CU(cudaGetDevice(&dev));
+        CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        if (bytes > optin - 1024) return CFR_OK;
+        tp.bytes = (int)bytes;
+        // per level: slots and its (consecutive) infosets; members of each infoset
+        std::vector<TinyLevel> lv(g.D + 1, TinyLevel{0, 0, 0, 0});
+        std::vector<int64_t> mem(2 * (size_t)g.H + 2, -1);
+        for (int L = 0; L < g.D; ++L) {
+            lv[L].s0 = g.slot_ptr[L];
+            lv[L].s1 = g.slot_ptr[L + 1];
+            long long h0 = LLONG_MAX, h1 = -1;
+            for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1]; ++t)
+                for (int k = g.tiles[t].seg0; k < g.tiles[t].seg1; ++k) {
+                    const SegH& sg = g.segs[k];
+                    const int64_t h = sg.h;
+                    mem[2 * h] = mem[2 * h] < 0 ? sg.sb : std::min<int64_t>(mem[2 * h], sg.sb);
+                    mem[2 * h + 1] = std::max<int64_t>(mem[2 * h + 1], sg.se);
+                    h0 = std::min<long long>(h0, h);
+                    h1 = std::max<long long>(h1, h + 1);
+                }
+            if (h1 > h0) {
+                lv[L].h0 = h0;
+                lv[L].h1 = h1;
+            }
+        }
+        for (int64_t h = 0; h < g.H; ++h)
+            if (mem[2 * h] < 0) return CFR_OK;
+        for (int L = 0; L < g.D; ++L)   // each level's infosets must be a consecutive id range
+            for (long long h = lv[L].h0; h < lv[L].h1; ++h)
+                if (mem[2 * h] < g.slot_ptr[L] || mem[2 * h + 1] > g.slot_ptr[L + 1]) return CFR_OK;
+        CU(cudaFuncSetAttribute(tiny_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, tp.bytes));
+        cfr_status st = up(plan.tlev, lv);
+        if (st) return st;
+        if ((st = up(plan.tmem_of, narrow<I>(mem)))) return st;
+        CU(cudaStreamSynchronize(stream));
+        tiny_plan_ = tp;
+        tiny_ = true;
+        return CFR_OK;
+    }
+    long long plan_u_rows() const { return (long long)u_layout(*gp, sizeof(R)).back(); }
+    cfr_status launch_tiny(int64_t iters) {
+        const Game& g = *gp;
+        const TinyLevel* lv = reinterpret_cast<const TinyLevel*>(ws + plan.tlev);
+        const I* mem = reinterpret_cast<const I*>(ws + plan.tmem_of);
+        const int D = g.D;
+        const long long T = (long long)iters;
+        const TinyPlan tp = tiny_plan_;
+        switch (g.Pc) {
+            case 1: launch(pdl_, k_tiny<R, I, 1>, dim3(1), dim3(1024), (size_t)tp.bytes, stream, dg, lv, mem, D, T, tp); break;
+            case 2: launch(pdl_, k_tiny<R, I, 2>, dim3(1), dim3(1024), (size_t)tp.bytes, stream, dg, lv, mem, D, T, tp); break;
+            case 3: launch(pdl_, k_tiny<R, I, 3>, dim3(1), dim3(1024), (size_t)tp.bytes, stream, dg, lv, mem, D, T, tp); break;
+            default: launch(pdl_, k_tiny<R, I, 4>, dim3(1), dim3(1024), (size_t)tp.bytes, stream, dg, lv, mem, D, T, tp); break;
+        }
+        CU(cudaGetLastError());
+        return CFR_OK;
+    }
 
     int64_t count_launches() const {
         const Game& g = *gp;
@@ -3031,6 +3289,7 @@ struct Solver final : SolverBase {
             return CFR_ERR_UNSUPPORTED;
         }
         if (persist_ && iters > 0) return launch_persistent(iters);
+        if (tiny_ && iters > 0) return launch_tiny(iters);
         for (int64_t k = 0; k < iters; ++k) {
             if (gexec) CU(cudaGraphLaunch(gexec, stream));
             else {
@@ -3238,7 +3497,7 @@ struct Solver final : SolverBase {
     }
 
     cfr_status launches(int64_t* n) override {
-        *n = persist_ ? 1 : launches_per_iter;   // persistent: one launch per enqueue of T iterations
+        *n = (persist_ || tiny_) ? 1 : launches_per_iter;   // one launch per enqueue of T iterations
         return CFR_OK;
     }
 

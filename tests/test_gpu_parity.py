@@ -85,7 +85,7 @@ def test_persistent_matches_per_level_launches(cuda, name):
     g = pb.Game(desc)
     T = 7 if name == "liars_dice" else 40
     a = pb.Solver(g, variant="cfr+", precision=64, flags=pb.FLAG_PERSISTENT)
-    b = pb.Solver(g, variant="cfr+", precision=64)
+    b = pb.Solver(g, variant="cfr+", precision=64, flags=pb.FLAG_NO_TINY)
     assert a.launches_per_iteration() == 1 and b.launches_per_iteration() > 1
     a.run(T)
     b.run(T)
@@ -94,3 +94,30 @@ def test_persistent_matches_per_level_launches(cuda, name):
     for k in ("regret", "snum", "sden"):
         assert np.array_equal(sa[k], sb[k]), k
     assert np.array_equal(a.average_strategy(), b.average_strategy())
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+def test_tiny_shared_memory_kernel_matches_per_level_launches(cuda, variant, precision):
+    """k_tiny (one CTA, all state in shared memory, T iterations per launch) and the
+    per-level kernel graph give the same bits (and the oracle's: run_pair)."""
+    import paper_2408_14778_b200 as pb
+    games = [gamegen.kuhn(2), gamegen.kuhn(3), gamegen.matrix_game([[0, -1, 2], [1, 0, -1], [-1, 1, 0]]),
+             gamegen.signal_game(), gamegen.random_game(3, num_players=2)]
+    if precision == 32:
+        games.append(gamegen.leduc())
+    used = 0
+    for desc in games:
+        g = pb.Game(desc)
+        a = pb.Solver(g, variant=variant, precision=precision)
+        b = pb.Solver(g, variant=variant, precision=precision, flags=pb.FLAG_NO_TINY)
+        used += a.launches_per_iteration() == 1
+        a.run(17)
+        b.run(17)
+        sa, sb = a.state(), b.state()
+        for k in ("regret", "snum", "sden"):
+            assert np.array_equal(sa[k], sb[k]), (desc.name, k)
+        assert np.array_equal(a.current_strategy(), b.current_strategy())
+        assert np.array_equal(a.expected_values(), b.expected_values())
+    assert used >= 3
+    run_pair(gamegen.kuhn(2), variant, precision, 40)

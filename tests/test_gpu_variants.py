@@ -50,6 +50,6 @@ def test_alternating_random_and_streaming(cuda):
     out, s, o = run_pair(gamegen.synthetic(n_types=3, seed=2), 4, 64, 3, flags=pb.FLAG_FORCE_STREAM,
                          checks=("state",))
     assert "k_bwd_stream" in s.level_kernels()
-    ref = pb.Solver(pb.Game(gamegen.kuhn(2)), variant="cfr+", precision=64)
-    alt = pb.Solver(pb.Game(gamegen.kuhn(2)), variant="cfr+alt", precision=64)
+    ref = pb.Solver(pb.Game(gamegen.kuhn(2)), variant="cfr+", precision=64, flags=pb.FLAG_NO_TINY)
+    alt = pb.Solver(pb.Game(gamegen.kuhn(2)), variant="cfr+alt", precision=64, flags=pb.FLAG_NO_TINY)
     assert alt.launches_per_iteration() == 2 * ref.launches_per_iteration()

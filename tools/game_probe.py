@@ -6,7 +6,7 @@ import gamegen, paper_2408_14778_b200 as pb
 for name, iters in (("kuhn", 5000), ("leduc", 2000), ("goofspiel", 1000), ("liars_dice", 300)):
     d = gamegen.by_name(name)
     g = pb.Game(d)
-    for flags, tag in ((pb.FLAG_PERSISTENT, "persistent"), (0, "graph")):
+    for flags, tag in ((0, "default"), (pb.FLAG_NO_TINY, "graph")):
         for prec in (64, 32):
             s = pb.Solver(g, variant="cfr+", precision=prec, flags=flags)
             s.run(5)
