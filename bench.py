@@ -151,8 +151,8 @@ def cpu_baseline(n_types: int, variant: int, precision: int, seconds: float, V_f
 def per_game(pb, torch, variant: str, precision: int):
     """Secondary lines of the metric: it/s and node-updates/s per small game."""
     out = {}
-    for name, iters in (("kuhn", 2000), ("leduc", 1000), ("goofspiel", 500), ("liars_dice", 500)):
-        d = gamegen.by_name(name)
+    for name, iters in (("kuhn", 2000), ("leduc", 1000), ("goofspiel", 500), ("liars_dice", 500), ("goofspiel6", 200)):
+        d = gamegen.goofspiel(6) if name == "goofspiel6" else gamegen.by_name(name)
         g = pb.Game(d)
         s = pb.Solver(g, variant=variant, precision=precision)
         s.run(5)

@@ -1229,7 +1229,7 @@ extern "C" int cfr_debug_stream_profile(unsigned long long* out, int reset) {
 struct StreamHdr {
     int k0, nseg, m0, M;        // first infoset (level-relative), infosets, first member, members
     int po, ho, oo, hso;        // element offsets inside the windows: pairs, S_den, owner, hs
-    int no, pao, pad1, pad2;    // node-row / parent-actor window offsets
+    int no, pao, ro, rro;       // node-row / parent-actor / child-row / reach-row window offsets
 };
 
 #ifndef CFR_STREAM_MINB
@@ -1324,7 +1324,9 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 hd->hso = hso;
                 hd->no = no;
                 hd->pao = pao;
-                (void)o_rows; (void)o_reach; (void)po2; (void)po3;   // rows / reach windows are aligned (host check)
+                hd->ro = o_rows;
+                hd->rro = o_reach;
+                (void)po2; (void)po3;   // sigma / R / S_num share the pair window offset (same base alignment)
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 if (L.debug == 2) {   // timing experiment: no loads (consumers compute on stale data)
                     mbar_expect_tx(&full[st], 0);
@@ -1415,8 +1417,11 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         int* const ccnt = ccnt_buf + tpar * 2 * L.maxseg;
         SPROF(0); mbar_wait(&full[st], ph & 1u); SPROF(1);
         const StreamHdr hd = *hdp;
-        const R* rows = reinterpret_cast<const R*>(S + L.o_rows);
-        const R* reach = reinterpret_cast<const R*>(S + L.o_reach);
+        const R* rows = reinterpret_cast<const R*>(S + L.o_rows) + hd.ro;
+        const R* reach = reinterpret_cast<const R*>(S + L.o_reach) + hd.rro;
+        // 16-byte row reads need 16-byte aligned rows in the stage
+        const bool vec_rows = (((unsigned)L.rowlen * (unsigned)sizeof(R)) & 15u) == 0 &&
+                              (((unsigned)hd.ro * (unsigned)sizeof(R)) & 15u) == 0;
         const R* ssig = reinterpret_cast<const R*>(S + L.o_sig) + hd.po;
         const R* sreg = reinterpret_cast<const R*>(S + L.o_reg) + hd.po;
         const R* ssn = reinterpret_cast<const R*>(S + L.o_snum) + hd.po;
@@ -1463,8 +1468,8 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 const R* row = rows + (long long)m * L.rowlen;
                 const R* sg = ssig + k * n;
                 if (L.debug & 16) {   // timing experiment: no value loop
-                } else if (PC == 1) {
-                    // 16-byte row reads (rows are 16-byte multiples: host check)
+                } else if (PC == 1 && vec_rows) {
+                    // 16-byte row reads (vec_rows: rows 16-byte aligned in the stage)
                     using V = typename std::conditional<sizeof(R) == 8, double2, float4>::type;
                     constexpr int E = 16 / (int)sizeof(R);
                     const V* row4 = reinterpret_cast<const V*>(row);
@@ -2295,7 +2300,7 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         StreamLevel f{};
         const int64_t s0 = g.slot_ptr[L], s1 = g.slot_ptr[L + 1];
         if (s1 <= s0) { out[L] = f; continue; }
-        bool ok = ((2 * P * w) % 16 == 0) && s1 < INT32_MAX;
+        bool ok = s1 < INT32_MAX;
         std::vector<int> hs;
         int64_t h_prev = -1, next = s0;
         int n = -1;
@@ -2313,7 +2318,11 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
             }
         if (!ok || next != s1 || n <= 0) { out[L] = f; continue; }
         const int64_t row0 = cb_u[s0];
-        if ((row0 * Pc * w) % 16 != 0 || ((int64_t)n * Pc * w) % 16 != 0) { out[L] = f; continue; }
+        // (rows and reach rows of any alignment: the TMA windows are 16-byte aligned
+        // supersets and the consumers apply the element offsets).  Rows shorter than
+        // 16 bytes stay on the tile kernel: their per-member work is too small to
+        // amortise the streaming pipeline (measured on Goofspiel-6's one-action levels).
+        if ((int64_t)n * Pc * w < 16) { out[L] = f; continue; }
         for (int64_t s = s0; s < s1 && ok; ++s) ok = (cb_u[s] == row0 + (s - s0) * n);
         if (!ok) { out[L] = f; continue; }
         const int nh = (int)hs.size();
@@ -2378,7 +2387,7 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         }
         // the deepest decision level: no decision children, so no other forward
         // level reads its reach rows -- its forward pass runs inside this kernel
-        f.fused = (fuse_forward && L == g.D - 1 && f.maxm <= kStreamConsumers) ? 1 : 0;   // gathers: <= 8 per lane
+        f.fused = (fuse_forward && L == g.D - 1 && f.maxm <= kStreamConsumers && (2 * P * w) % 16 == 0) ? 1 : 0;   // gathers: <= 8 per lane, 16-byte pieces
         f.level = L;
         f.compact = (!f.fused && P == 2 && L == g.D - 1 && compact_reach) ? 1 : 0;
         stream_plan(f, P, Pc, w, ix, stages);
