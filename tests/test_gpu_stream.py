@@ -86,3 +86,14 @@ def test_stream_degenerate_games(cuda):
                  gamegen.matrix_game([[1.0, -1.0], [-1.0, 1.0]])):
         for variant in range(5):
             run_pair(desc, variant, 64, 6, flags=pb.FLAG_FORCE_STREAM)
+
+
+@pytest.mark.parametrize("name", ["goofspiel", "liars_dice", "leduc"])
+def test_stream_f32_unaligned_windows(cuda, name):
+    """f32 through the streaming kernel: compact reach rows are 8 bytes, so tiles
+    starting at an odd member need the TMA window offsets (child rows of odd
+    length likewise)."""
+    desc = gamegen.by_name(name)
+    T = 4 if name == "liars_dice" else 12
+    for variant in (1, 3):
+        out, s, o = run_pair(desc, variant, 32, T, flags=pb.FLAG_FORCE_STREAM)
