@@ -15,7 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _CSRC = os.path.join(_HERE, "csrc")
 LIB_PATH = os.path.join(_HERE, "libcfr_b200.so")
 SOURCES = [os.path.join(_CSRC, f) for f in ("solver.cu", "flatten.cpp", "shard.cpp", "store.cpp", "cabi.cpp")]
-HEADERS = [os.path.join(_CSRC, "game.hpp"), os.path.join(os.path.dirname(_HERE), "include", "cfr_b200.h")]
+HEADERS = [os.path.join(_CSRC, "game.hpp"), os.path.join(os.path.dirname(_HERE), "include", "cfr_b200.h")] + [
+    os.path.join(_CSRC, "kernels", f) for f in sorted(os.listdir(os.path.join(_CSRC, "kernels"))) if f.endswith(".cuh")]
 
 _NCCL = os.path.join(os.path.dirname(os.path.dirname(os.__file__)), "site-packages", "nvidia", "nccl")
 if not os.path.isdir(_NCCL):

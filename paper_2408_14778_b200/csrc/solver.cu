@@ -34,2027 +34,16 @@
 
 #include "game.hpp"
 
+// device code, one header per kernel family
+#include "kernels/common.cuh"
+#include "kernels/forward.cuh"
+#include "kernels/tile.cuh"
+#include "kernels/pipelined.cuh"
+#include "kernels/stream.cuh"
+#include "kernels/update.cuh"
+#include "kernels/small.cuh"
+
 namespace cfrb {
-
-// Device tile / segment records (built by the solver from the game's TileH /
-// SegH plus the precision-dependent staging layout).
-struct TileD {
-    long long s0, s1;    // slot range
-    int seg0, seg1;      // segments
-    int npairs;          // (h, a) pairs of the tile's segments
-    int staged;          // 0: children read from global; 1: uniform rows, chunked; 2: generic rows
-    int rowlen;          // elements per row (mode 1)
-    int cpr;             // chunks per row (mode 1)
-    int stride;          // row stride in elements (mode 1)
-    float inv_cpr;       // 1 / cpr
-    int contrib;         // 1: add this tile's deferred partial sums (trunk tiles: rank 0 only)
-    int pad;
-};
-struct SegD {
-    long long h, qb;     // internal infoset, qbase[h]
-    long long sb, se;    // member slots
-    long long dq, dh;    // compact accumulator pair base / infoset index (deferred only)
-    int pair_off, n, owner, fused;
-};
-
-enum { MODE_CFR = 0, MODE_VALUES = 1, MODE_BR = 2 };
-
-template <class R, class I>
-struct DG {
-    R* U;          // [V * Pc] node values, canonical order; terminal rows = u
-    R* reach;      // [ND][2P] AoS, canonical decision order: pi_check(., 1..P), pi_hat(., 1..P)
-    R* sig;        // [Q + C] sigma_ext = current strategy (internal q order) | chance
-    R* regret;     // [Q] cumulative regret
-    R* snum;       // [Q] sum_t w_t pi_bar sigma
-    R* sden;       // [H] sum_t w_t pi_bar
-    unsigned long long* acc_r;  // [ndef pairs][3] exact slices of the deferred infosets (compact)
-    unsigned long long* acc_p;  // [ndef][3]; acc_r and acc_p are one contiguous exchange block
-    const long long* dqbase;    // [ndef + 1] compact pair base of each deferred infoset
-    const I* f_parent;            // [NS] slot order: parent slot, incoming sigma_ext edge, parent actor
-    const I* f_e;
-    const unsigned char* f_pact;
-    const I* s_node;              // [NS] backward pass (slot order)
-    const I* s_cb;
-    const int* s_n;
-    const I* s_ebase;
-    const unsigned char* s_actor;
-    const I* s_dec;
-    const int* s_coff;
-    const I* qbase;               // [H+1] internal
-    const unsigned char* owner;   // [H]
-    const TileD* tiles;
-    const SegD* segs;
-    const I* deferred;            // [ndef]
-    long long* ctrl;              // [0] iterations done, [1] first bad iteration, [2] done counter
-    unsigned long long* lcnt;     // [D][4] streaming-level work counters (updated / visited infosets, pairs)
-    long long ndef;
-    int P;
-    int variant;
-    int upd_player;               // alternating updates (variant 4): the player updated by this pass; 0 = all
-    double sc0, rc[3];            // 2^(40-E), 2^(E-40k): regret / BR sums
-    double scp0, rcp[3];          // same with E = 1: pi_bar sums
-};
-
-// ---------------------------------------------------------------- exact sums
-// Three 40-bit slices per term:
-// c_k = rint(x * 2^(40k-E)), x <- x - c_k 2^(E-40k).  Implemented with FP64 adds
-// only: y = x*2^(40-E) is exact; rint(y) = (y + 1.5*2^52) - 1.5*2^52 (round half
-// to even, |y| < 2^51); y - c is exact and y' = (y - c) * 2^40 is the next slice's
-// input, identical to x_k * 2^(40(k+1)-E).  The slices are integers, so partial
-// sums of <= 2^13 of them are exact in binary64; they are converted to int64 only
-// for global accumulation.  decode = ((C1 2^(E-40) + C2 2^(E-80)) + C3 2^(E-120)).
-__device__ __forceinline__ double rint_magic(double y) {
-    const double M = 6755399441055744.0;  // 1.5 * 2^52
-    return (y + M) - M;
-}
-__device__ __forceinline__ void xadd(double& a0, double& a1, double& a2, double x, double sc0) {
-    double y = x * sc0;
-    const double c0 = rint_magic(y);
-    y = (y - c0) * 1099511627776.0;   // 2^40
-    const double c1 = rint_magic(y);
-    y = (y - c1) * 1099511627776.0;
-    const double c2 = rint_magic(y);
-    a0 += c0;
-    a1 += c1;
-    a2 += c2;
-}
-__device__ __forceinline__ double xdec(double c0, double c1, double c2, const double (&rc)[3]) {
-    return (c0 * rc[0] + c1 * rc[1]) + c2 * rc[2];
-}
-__device__ __forceinline__ double xdec_ll(long long c0, long long c1, long long c2, const double (&rc)[3]) {
-    return (__ll2double_rn(c0) * rc[0] + __ll2double_rn(c1) * rc[1]) + __ll2double_rn(c2) * rc[2];
-}
-
-// cp.async (LDGSTS): global -> shared without register staging, many in flight.
-template <int BYTES>
-__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
-
-// Programmatic dependent launch (PDL): a kernel lets its successor launch early
-// (launch_dependents) and waits for its predecessor's completion + memory flush
-// (wait) only before touching data the predecessor may write.  Both are no-ops
-// without a programmatic dependency.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-
-// L2 eviction-priority policies (createpolicy) for loads / stores with a cache hint:
-// streams read or written once go first, small reused gather tables stay
-__device__ __forceinline__ unsigned long long policy_evict_first() {
-    unsigned long long p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ unsigned long long policy_evict_normal() {
-    unsigned long long p;
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ unsigned long long policy_evict_last() {
-    unsigned long long p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-    return p;
-}
-template <class T>
-__device__ __forceinline__ T ld_hint(const T* p, unsigned long long pol);
-template <>
-__device__ __forceinline__ double ld_hint<double>(const double* p, unsigned long long pol) {
-    double v;
-    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(p), "l"(pol));
-    return v;
-}
-template <>
-__device__ __forceinline__ float ld_hint<float>(const float* p, unsigned long long pol) {
-    float v;
-    asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(pol));
-    return v;
-}
-template <>
-__device__ __forceinline__ int ld_hint<int>(const int* p, unsigned long long pol) {
-    int v;
-    asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;\n" : "=r"(v) : "l"(p), "l"(pol));
-    return v;
-}
-template <>
-__device__ __forceinline__ long long ld_hint<long long>(const long long* p, unsigned long long pol) {
-    long long v;
-    asm volatile("ld.global.L2::cache_hint.s64 %0, [%1], %2;\n" : "=l"(v) : "l"(p), "l"(pol));
-    return v;
-}
-template <>
-__device__ __forceinline__ unsigned char ld_hint<unsigned char>(const unsigned char* p, unsigned long long pol) {
-    unsigned short v;
-    asm volatile("ld.global.L2::cache_hint.u8 %0, [%1], %2;\n" : "=h"(v) : "l"(p), "l"(pol));
-    return (unsigned char)v;
-}
-__device__ __forceinline__ void st_hint_v2(double2* p, double2 v, unsigned long long pol) {
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
-                 : "memory");
-}
-__device__ __forceinline__ void st_hint_v2(float2* p, float2 v, unsigned long long pol) {
-    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;\n" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol)
-                 : "memory");
-}
-
-template <class R>
-__device__ __forceinline__ bool finite_(R x) {
-    return isfinite(x);
-}
-
-// Per-iteration update rule (cfr_solver_config.variant): 0 CFR (Eq 8/15
-// cumulative, reading Q4), 1 CFR+ (RM+, w_t = t; reading Q6) and 4 its
-// alternating-update form (reading Q19: same rule, one player per pass), 2 linear CFR and 3
-// DCFR(3/2, 0, 2) -- Brown & Sandholm's discounting of Eq 14/15 (reading
-// Q18): after iteration t's terms are added, positive regrets x t^a/(t^a+1),
-// others x t^b/(t^b+1), both average-strategy sums x (t/(t+1))^g.  Only correctly
-// rounded operations (t^(3/2) = t * sqrt(t)), so CPU and GPU agree bit for bit.
-template <class R>
-struct Upd {
-    int variant;
-    R w;                  // weight of pi_bar inside the average sums: t for CFR+, else 1
-    R dpos, dneg, dsum;   // discount factors (variants 2, 3)
-};
-template <class R>
-__device__ __forceinline__ Upd<R> make_upd(int variant, long long t) {
-    Upd<R> u;
-    u.variant = variant;
-    u.w = (variant == 1 || variant == 4) ? (R)t : (R)1;
-    u.dpos = u.dneg = u.dsum = (R)1;
-    const R tt = (R)t;
-    if (variant == 2) {
-        const R f = tt / (tt + (R)1);
-        u.dpos = f;
-        u.dneg = f;
-        u.dsum = f;
-    } else if (variant == 3) {
-        const R a = tt * sqrt(tt);
-        u.dpos = a / (a + (R)1);
-        u.dneg = (R)1 / ((R)1 + (R)1);
-        const R f = tt / (tt + (R)1);
-        u.dsum = f * f;
-    }
-    return u;
-}
-template <class R>
-__device__ __forceinline__ R upd_regret(const Upd<R>& u, R reg, R rt) {
-    const R x = reg + rt;
-    if (u.variant == 0) return x;
-    if (u.variant == 1 || u.variant == 4) {
-        R r = (x > (R)0) ? x : (R)0;
-        if (!finite_(x)) r = x;
-        return r;
-    }
-    return (x > (R)0) ? x * u.dpos : x * u.dneg;
-}
-// S_num (add = (w pi_bar) sigma) or S_den (add = w pi_bar)
-template <class R>
-__device__ __forceinline__ R upd_sum(const Upd<R>& u, R s, R add) {
-    return (u.variant == 2 || u.variant == 3) ? (s + add) * u.dsum : s + add;
-}
-
-// ------------------------------------------------------------ forward pass
-// Decision nodes of one depth in canonical order (streaming reads of the
-// parents' rows, streaming writes).  Eq 2: pi_check(v,i) =
-// pi_check(parent,i) * (sigma if the parent's actor != i else 1); Eq 4 (P:97,
-// reading Q1): pi_hat(v,i) = pi_hat(parent,i) * (sigma if actor == i else 1).
-// compact != 0 (two players, the deepest decision level when its backward pass
-// is the streaming kernel): no forward level reads these rows, and the backward
-// pass needs only the acting player's pi_check and pi_hat -- 2 values per slot
-// are written at reach + d_begin*2P + (d - d_begin)*2 instead of the 2P-value row.
-template <class R, class I, int PT>
-__device__ __forceinline__ void fwd_body(const DG<R, I>& g, const R* __restrict__ sig, long long d_begin,
-                                         long long d_end, int compact) {
-    const int P = (PT > 0) ? PT : g.P;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    pdl_trigger();
-    if (PT == 2) {
-        // two players: 4-value rows (32 B) moved as two 16-byte vectors; FW rows
-        // per thread with every load issued before the first use (the parent rows
-        // are gathers: memory-level parallelism, not bandwidth, bounds this pass)
-#ifndef CFR_FWD_FW
-#define CFR_FWD_FW 4
-#endif
-        constexpr int FW = CFR_FWD_FW;
-        using V2 = typename std::conditional<sizeof(R) == 8, double2, float2>::type;
-        const long long n = d_end - d_begin;
-        const long long chunk = (long long)blockDim.x * FW;
-#ifndef CFR_FWD_HINTS
-#define CFR_FWD_HINTS 1
-#endif
-        const unsigned long long pf = CFR_FWD_HINTS ? policy_evict_first() : policy_evict_normal();
-        const unsigned long long pl = CFR_FWD_HINTS ? policy_evict_last() : policy_evict_normal();
-        pdl_wait();
-        for (long long base = (long long)blockIdx.x * chunk; base < n; base += (long long)gridDim.x * chunk) {
-            long long p[FW];
-            long long e[FW];
-            int act[FW], own[FW];
-#pragma unroll
-            for (int k = 0; k < FW; ++k) {
-                const long long i = base + k * blockDim.x + threadIdx.x;
-                const long long d = d_begin + (i < n ? i : 0);
-                p[k] = (long long)ld_hint(g.f_parent + d, pf);
-                e[k] = (long long)ld_hint(g.f_e + d, pf);
-                act[k] = ld_hint(g.f_pact + d, pf);
-                own[k] = compact ? (int)ld_hint(g.s_actor + d, pf) : 0;
-            }
-            V2 a[FW], b[FW];
-            R x[FW];
-#pragma unroll
-            for (int k = 0; k < FW; ++k) {
-                if (sizeof(R) == 8) {
-                    // the whole 32-byte parent row in one 256-bit load (one L1 request)
-                    double r0, r1, r2, r3;
-                    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n"
-                                 : "=d"(r0), "=d"(r1), "=d"(r2), "=d"(r3)
-                                 : "l"(g.reach + p[k] * 4));
-                    a[k].x = (R)r0;   // pi_check(1), pi_check(2)
-                    a[k].y = (R)r1;
-                    b[k].x = (R)r2;   // pi_hat(1), pi_hat(2)
-                    b[k].y = (R)r3;
-                } else {
-                    const V2* src = reinterpret_cast<const V2*>(g.reach + p[k] * 4);
-                    a[k] = src[0];
-                    b[k] = src[1];
-                }
-                x[k] = ld_hint(sig + e[k], pl);   // the edge's sigma: reused by every member of the parent's infoset
-            }
-#pragma unroll
-            for (int k = 0; k < FW; ++k) {
-                const long long i = base + k * blockDim.x + threadIdx.x;
-                if (i >= n) continue;
-                V2 ca, cb;
-                ca.x = (act[k] != 1) ? a[k].x * x[k] : a[k].x;
-                ca.y = (act[k] != 2) ? a[k].y * x[k] : a[k].y;
-                cb.x = (act[k] == 1) ? b[k].x * x[k] : b[k].x;
-                cb.y = (act[k] == 2) ? b[k].y * x[k] : b[k].y;
-                if (compact) {
-                    // the slot's actor: (pi_check, pi_hat) of that player only
-                    V2 c2;
-                    c2.x = (own[k] == 2) ? ca.y : ca.x;
-                    c2.y = (own[k] == 2) ? cb.y : cb.x;
-                    st_hint_v2(reinterpret_cast<V2*>(g.reach + d_begin * 4 + i * 2), c2, pf);
-                    continue;
-                }
-                if (sizeof(R) == 8) {
-                    // the 32-byte row in one 256-bit store
-                    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(
-                                     g.reach + (d_begin + i) * 4),
-                                 "d"((double)ca.x), "d"((double)ca.y), "d"((double)cb.x), "d"((double)cb.y), "l"(pf)
-                                 : "memory");
-                } else {
-                    V2* dst = reinterpret_cast<V2*>(g.reach + (d_begin + i) * 4);
-                    st_hint_v2(dst, ca, pf);
-                    st_hint_v2(dst + 1, cb, pf);
-                }
-            }
-        }
-        return;
-    }
-    pdl_wait();
-    for (long long d = d_begin + (long long)blockIdx.x * blockDim.x + threadIdx.x; d < d_end; d += stride) {
-        const long long p = (long long)g.f_parent[d];
-        const R x = sig[g.f_e[d]];
-        const int act = g.f_pact[d];
-        const R* __restrict__ src = g.reach + p * 2 * P;
-        R* __restrict__ dst = g.reach + d * 2 * P;
-#pragma unroll
-        for (int j = 0; j < ((PT > 0) ? PT : 16); ++j) {
-            if (PT == 0 && j >= P) break;
-            const R pc = src[j];
-            const R ph = src[P + j];
-            dst[j] = (act != j + 1) ? pc * x : pc;
-            dst[P + j] = (act == j + 1) ? ph * x : ph;
-        }
-    }
-}
-
-template <class R, class I, int PT>
-__global__ void __launch_bounds__(256) k_fwd(DG<R, I> g, const R* __restrict__ sig, long long d_begin,
-                                             long long d_end, int compact) {
-    fwd_body<R, I, PT>(g, sig, d_begin, d_end, compact);
-}
-
-// ----------------------------------------------------------- backward pass
-// One CTA (kTileSlots threads) per tile of whole infosets.  Global memory is
-// touched in three dependency steps only (metadata; reach + sigma + children +
-// update state; writes), everything else runs out of shared memory.
-struct SegS {
-    long long h;     // internal infoset
-    long long qb;    // qbase[h]
-    long long dq, dh;  // compact accumulator indices (deferred)
-    int sb, se;      // tile-local member slots
-    int pair_off;    // first pair of the segment in the tile
-    int n;           // |A(h)|
-    int owner;       // acting player
-    int fused;
-};
-
-// Shared-memory layout of one backward launch (per level: sized by the
-// level's largest tile so small tiles leave room for more resident CTAs).
-struct SmemLayout {
-    int ch, sv, spc, sph, ssig, sreg, ssn, pib, zs, sden, seg, soff, best, scoff, spoff, sn, scb, pseg, cm, ccnt;
-    int bytes;
-};
-template <class R>
-struct TileView {
-    R *ch, *sv, *spc, *sph, *ssig, *sreg, *ssn, *pib, *zs, *sden;
-    SegS* seg;
-    int *soff, *best, *scoff, *spoff, *sn;
-    long long* scb;
-    unsigned char* pseg;
-    short* cm;     // per segment: members with nonzero pi_check (tile-local slots)
-    int* ccnt;
-};
-template <class R>
-__device__ __forceinline__ TileView<R> make_view(unsigned char* b, const SmemLayout& L) {
-    TileView<R> v;
-    v.ch = (R*)(b + L.ch);
-    v.sv = (R*)(b + L.sv);
-    v.spc = (R*)(b + L.spc);
-    v.sph = (R*)(b + L.sph);
-    v.ssig = (R*)(b + L.ssig);
-    v.sreg = (R*)(b + L.sreg);
-    v.ssn = (R*)(b + L.ssn);
-    v.pib = (R*)(b + L.pib);
-    v.zs = (R*)(b + L.zs);
-    v.sden = (R*)(b + L.sden);
-    v.seg = (SegS*)(b + L.seg);
-    v.soff = (int*)(b + L.soff);
-    v.best = (int*)(b + L.best);
-    v.scoff = (int*)(b + L.scoff);
-    v.spoff = (int*)(b + L.spoff);
-    v.sn = (int*)(b + L.sn);
-    v.scb = (long long*)(b + L.scb);
-    v.pseg = (unsigned char*)(b + L.pseg);
-    v.cm = (short*)(b + L.cm);
-    v.ccnt = (int*)(b + L.ccnt);
-    return v;
-}
-
-// rt / pos alias ch after phase B (the host sizes ch >= 2 * pairs)
-
-__device__ __forceinline__ int seg_of_pair(const int* soff, int nseg, int p) {
-    int lo = 0, hi = nseg - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (soff[mid] <= p) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
-
-template <class R, class I, int PC, int MODE>
-__device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict__ sig, long long tile, int br_player,
-                                         int last, const SmemLayout& lay, unsigned char* smem_raw) {
-    const TileView<R> sm = make_view<R>(smem_raw, lay);
-    const TileD T = g.tiles[tile];
-    const int nslot = (int)(T.s1 - T.s0);
-    const int nseg = T.seg1 - T.seg0;
-    const int tid = threadIdx.x, nth = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
-    const int P = g.P;
-    R* const rt = sm.ch;                  // valid after phase B
-    R* const pos = sm.ch + (lay.sreg - lay.ssig) / (int)sizeof(R);  // = ch + (pairs capacity)
-    const bool sig_staged = T.npairs <= kTilePairs;
-    const bool staged = T.staged != 0;
-    constexpr int CH = (sizeof(R) == 8) ? 16 : 8;     // cp.async chunk (bytes) of uniform tiles
-    constexpr int CE = CH / (int)sizeof(R);            // elements per chunk
-
-    // ---- step 1: per-slot metadata (thread = slot), owner reach, segment + run tables
-    // (metadata is constant: loaded before waiting for the previous kernel)
-    pdl_trigger();
-    long long my_node = 0, my_cb = 0, my_eb = 0, my_dec = 0;
-    int my_n = 0, my_actor = 0;
-    if (tid < nslot) {
-        const long long s = T.s0 + tid;
-        my_node = (long long)g.s_node[s];
-        my_cb = (long long)g.s_cb[s];
-        my_n = g.s_n[s];
-        my_eb = (long long)g.s_ebase[s];
-        my_actor = g.s_actor[s];
-        my_dec = (long long)g.s_dec[s];
-        sm.scoff[tid] = g.s_coff[s];
-        sm.scb[tid] = my_cb;
-        sm.sn[tid] = my_n;
-        sm.spoff[tid] = -1;
-    }
-    pdl_wait();
-    const long long t_iter = (MODE == MODE_CFR) ? g.ctrl[0] + 1 : 0;
-    if (tid < nslot && MODE != MODE_VALUES && my_actor >= 1) {
-        sm.spc[tid] = g.reach[my_dec * 2 * P + (my_actor - 1)];
-        sm.sph[tid] = g.reach[my_dec * 2 * P + P + (my_actor - 1)];
-    }
-    if (tid < nseg) {
-        const SegD sg = g.segs[T.seg0 + tid];
-        SegS ss;
-        ss.h = sg.h;
-        ss.qb = sg.qb;
-        ss.dq = sg.dq;
-        ss.dh = sg.dh;
-        ss.n = sg.n;
-        ss.owner = sg.owner;
-        ss.sb = (int)(sg.sb - T.s0);
-        ss.se = (int)(sg.se - T.s0);
-        ss.pair_off = sg.pair_off;
-        ss.fused = sg.fused;
-        sm.seg[tid] = ss;
-        sm.soff[tid] = sg.pair_off;
-        if (MODE == MODE_CFR && sg.fused) sm.sden[tid] = g.sden[sg.h];
-    }
-    if (tid == 0) sm.soff[nseg] = T.npairs;
-    __syncthreads();
-
-    // ---- step 2: children (cp.async, every lane keeps issuing; nothing waits
-    // until cp.async.wait_all), sigma and update state of the tile's pairs
-    if (T.staged == 1) {
-        // uniform rows: flat loop over 16-B (f64) / 8-B (f32) chunks, all lanes busy
-        const int total = nslot * T.cpr;
-        for (int c = tid; c < total; c += nth) {
-            const int row = __float2int_rd(((float)c + 0.5f) * T.inv_cpr);
-            const int k = c - row * T.cpr;
-            cp_async<CH>(sm.ch + row * T.stride + k * CE, g.U + sm.scb[row] * PC + k * CE);
-        }
-    } else if (T.staged == 2) {
-        // generic rows: a warp per row, lanes over the row's elements
-        for (int ls = warp; ls < nslot; ls += nwarps) {
-            const R* __restrict__ src = g.U + sm.scb[ls] * PC;
-            R* dst = sm.ch + sm.scoff[ls];
-            const int cnt = sm.sn[ls] * PC;
-            for (int e = lane; e < cnt; e += 32) cp_async<(int)sizeof(R)>(dst + e, src + e);
-        }
-    }
-    if (sig_staged) {
-        for (int p = tid; p < T.npairs; p += nth) {
-            const int k = seg_of_pair(sm.soff, nseg, p);
-            sm.pseg[p] = (unsigned char)k;
-            const long long q = sm.seg[k].qb + (p - sm.soff[k]);
-            sm.ssig[p] = sig[q];
-            if (MODE == MODE_CFR && sm.seg[k].fused) {
-                sm.sreg[p] = g.regret[q];
-                sm.ssn[p] = g.snum[q];
-            }
-        }
-    }
-    for (int k = warp; k < nseg; k += nwarps)
-        for (int s = sm.seg[k].sb + lane; s < sm.seg[k].se; s += 32) sm.spoff[s] = sm.soff[k];
-    cp_async_wait_all();
-    __syncthreads();
-
-    // ---- phase A: node values, Eq 1 in ascending action order from +0
-    if (tid < nslot) {
-        R v[PC];
-#pragma unroll
-        for (int j = 0; j < PC; ++j) v[j] = (R)0;
-        const int po = sig_staged ? sm.spoff[tid] : -1;
-        if (staged && po >= 0) {
-            const R* row = sm.ch + sm.scoff[tid];
-            const R* sg = sm.ssig + po;
-            for (int a = 0; a < my_n; ++a) {
-                const R x = sg[a];
-#pragma unroll
-                for (int j = 0; j < PC; ++j) v[j] = v[j] + x * row[a * PC + j];
-            }
-        } else {
-            for (int a = 0; a < my_n; ++a) {
-                const R x = (po >= 0) ? sm.ssig[po + a] : sig[my_eb + a];
-#pragma unroll
-                for (int j = 0; j < PC; ++j) {
-                    const R u = staged ? sm.ch[sm.scoff[tid] + a * PC + j] : g.U[(my_cb + a) * PC + j];
-                    v[j] = v[j] + x * u;
-                }
-            }
-        }
-        const bool skip = (MODE == MODE_BR) && (my_actor == br_player);
-        if (!skip) {
-#pragma unroll
-            for (int j = 0; j < PC; ++j) g.U[my_node * PC + j] = v[j];
-        }
-#pragma unroll
-        for (int j = 0; j < PC; ++j) sm.sv[tid * PC + j] = v[j];
-    }
-    if (MODE == MODE_VALUES) return;
-    // members with pi_check == 0 add exact zeros to every sum: compact them away
-    for (int k = warp; k < nseg; k += nwarps) {
-        const int sb = sm.seg[k].sb, se = sm.seg[k].se;
-        int cnt = 0;
-        for (int base = sb; base < se; base += 32) {
-            const int s2 = base + lane;
-            const bool f = (s2 < se) && (sm.spc[s2] != (R)0);
-            const unsigned m = __ballot_sync(0xffffffffu, f);
-            if (f) sm.cm[sb + cnt + __popc(m & ((1u << lane) - 1u))] = (short)s2;
-            cnt += __popc(m);
-        }
-        if (lane == 0) sm.ccnt[k] = cnt;
-    }
-    __syncthreads();
-
-    // ---- phase B: exact sums.  Work items: every (infoset, action) pair (r~ or BR
-    // sums) plus one pi_bar item per segment (CFR mode).  Each item is split over
-    // `ns` adjacent lanes (members strided); partial slice sums are exact
-    // integer-valued doubles combined with shuffles.  The player-2 sign of the
-    // zero-sum storage (u2 = -u1) is applied to the sums: slices of -t are -slices of t.
-    const int nitems = T.npairs + ((MODE == MODE_CFR) ? nseg : 0);
-    int ns = 1;
-    int lns = 0;                      // ns = 2^lns (shifts, no integer division)
-    while (ns < 8 && nitems * ns * 2 <= nth) { ns <<= 1; ++lns; }
-    const int rounds = (nitems * ns + nth - 1) / nth;
-    double kr0 = 0, kr1 = 0, kr2 = 0, kr3 = 0, kr4 = 0;
-    for (int rd = 0; rd < rounds; ++rd) {
-        const int wi = rd * nth + tid;
-        const int it = wi >> lns, part = wi & (ns - 1);
-        double c0 = 0, c1 = 0, c2 = 0;
-        int k = 0, a = 0;
-        bool is_pair = false, neg = false, active = false;
-        if (it < T.npairs) {
-            k = sig_staged ? (int)sm.pseg[it] : seg_of_pair(sm.soff, nseg, it);
-            a = it - sm.soff[k];
-            is_pair = true;
-            const int i = sm.seg[k].owner;
-            active = !(MODE == MODE_BR && i != br_player);
-            neg = (PC == 1) && (i == 2) && (MODE == MODE_CFR);
-        } else if (it < nitems) {
-            k = it - T.npairs;
-            active = true;
-        }
-        if (active) {
-            const SegS& sg = sm.seg[k];
-            const int col = (PC == 1) ? 0 : sg.owner - 1;
-            if (!is_pair) {
-                for (int ls = sg.sb + part; ls < sg.se; ls += ns) xadd(c0, c1, c2, (double)sm.sph[ls], g.scp0);
-            } else if (staged) {
-                double e0 = 0, e1 = 0, e2 = 0;   // second independent chain (ILP)
-                const short* mem = sm.cm + sg.sb;
-                const int cnt = sm.ccnt[k];
-                int j = part;
-                for (; j + ns < cnt; j += 2 * ns) {
-                    const int la = mem[j], lb = mem[j + ns];
-                    const R ua = sm.ch[sm.scoff[la] + a * PC + col];
-                    const R ub = sm.ch[sm.scoff[lb] + a * PC + col];
-                    const R ta = (MODE == MODE_CFR) ? sm.spc[la] * (ua - sm.sv[la * PC + col]) : sm.spc[la] * ua;
-                    const R tb = (MODE == MODE_CFR) ? sm.spc[lb] * (ub - sm.sv[lb * PC + col]) : sm.spc[lb] * ub;
-                    xadd(c0, c1, c2, (double)ta, g.sc0);
-                    xadd(e0, e1, e2, (double)tb, g.sc0);
-                }
-                if (j < cnt) {
-                    const int la = mem[j];
-                    const R ua = sm.ch[sm.scoff[la] + a * PC + col];
-                    const R ta = (MODE == MODE_CFR) ? sm.spc[la] * (ua - sm.sv[la * PC + col]) : sm.spc[la] * ua;
-                    xadd(c0, c1, c2, (double)ta, g.sc0);
-                }
-                c0 += e0;
-                c1 += e1;
-                c2 += e2;
-            } else {
-                const short* mem = sm.cm + sg.sb;
-                for (int j = part; j < sm.ccnt[k]; j += ns) {
-                    const int ls = mem[j];
-                    const R uc = g.U[(sm.scb[ls] + a) * PC + col];
-                    const R t = (MODE == MODE_CFR) ? sm.spc[ls] * (uc - sm.sv[ls * PC + col]) : sm.spc[ls] * uc;
-                    xadd(c0, c1, c2, (double)t, g.sc0);
-                }
-            }
-            if (neg) { c0 = -c0; c1 = -c1; c2 = -c2; }
-        }
-        // combine the ns partial sums (exact: integer-valued doubles < 2^53)
-        for (int o = 1; o < ns; o <<= 1) {
-            c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-            c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-            c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-        }
-        if (active && part == 0) {
-            const bool keep = (MODE == MODE_BR) || sm.seg[k].fused;
-            if (keep) {
-                const double x = is_pair ? xdec(c0, c1, c2, g.rc) : xdec(c0, c1, c2, g.rcp);
-                if (rd == 0) kr0 = x;
-                else if (rd == 1) kr1 = x;
-                else if (rd == 2) kr2 = x;
-                else if (rd == 3) kr3 = x;
-                else kr4 = x;
-            } else if (MODE == MODE_CFR && T.contrib) {
-                if (is_pair) {
-                    const long long q = sm.seg[k].dq + a;
-                    atomicAdd(&g.acc_r[q * 3 + 0], (unsigned long long)(long long)c0);
-                    atomicAdd(&g.acc_r[q * 3 + 1], (unsigned long long)(long long)c1);
-                    atomicAdd(&g.acc_r[q * 3 + 2], (unsigned long long)(long long)c2);
-                } else {
-                    const long long h = sm.seg[k].dh;
-                    atomicAdd(&g.acc_p[h * 3 + 0], (unsigned long long)(long long)c0);
-                    atomicAdd(&g.acc_p[h * 3 + 1], (unsigned long long)(long long)c1);
-                    atomicAdd(&g.acc_p[h * 3 + 2], (unsigned long long)(long long)c2);
-                }
-            }
-        }
-    }
-    __syncthreads();   // all reads of sm.ch done: rt / pos alias it from here on
-    if (sig_staged) {
-        for (int rd = 0; rd < rounds && rd < 5; ++rd) {
-            const int wi = rd * nth + tid;
-            const int it = wi >> lns, part = wi & (ns - 1);
-            if (it < nitems && part == 0) {
-                const double x = rd == 0 ? kr0 : rd == 1 ? kr1 : rd == 2 ? kr2 : rd == 3 ? kr3 : kr4;
-                if (it < T.npairs) rt[it] = (R)x;
-                else sm.pib[it - T.npairs] = (R)x;
-            }
-        }
-    }
-    __syncthreads();
-
-    if (MODE == MODE_BR) {
-        // argmax per segment (ties to the lowest action); for u2 = -u1 storage the
-        // stored sums are negated, so player 2 takes the argmin.
-        for (int k = tid; k < nseg; k += nth) {
-            if (sm.seg[k].owner != br_player) continue;
-            const int n = sm.seg[k].n;
-            const bool neg = (PC == 1) && (br_player == 2);
-            int best = 0;
-            R bv = rt[sm.soff[k]];
-            for (int a = 1; a < n; ++a) {
-                const R x = rt[sm.soff[k] + a];
-                if (neg ? (x < bv) : (x > bv)) { bv = x; best = a; }
-            }
-            sm.best[k] = best;
-        }
-        __syncthreads();
-        for (int k = 0; k < nseg; ++k) {
-            if (sm.seg[k].owner != br_player) continue;
-            const int best = sm.best[k];
-            for (int ls = sm.seg[k].sb + tid; ls < sm.seg[k].se; ls += nth) {
-                const long long s = T.s0 + ls;
-                const long long src = ((long long)g.s_cb[s] + best) * PC;
-                const long long dst = (long long)g.s_node[s] * PC;
-#pragma unroll
-                for (int j = 0; j < PC; ++j) g.U[dst + j] = g.U[src + j];
-            }
-        }
-        return;
-    }
-
-    // ---- phase C: fused update of complete single-depth infosets
-    const Upd<R> up = make_upd<R>(g.variant, t_iter);
-    const R w = up.w;
-    if (!sig_staged) {   // split tile: every segment is deferred
-        if (last) {
-            __syncthreads();
-            if (tid == 0) g.ctrl[0] = t_iter;
-        }
-        return;
-    }
-    auto upd_seg = [&](int k) {   // fused and (alternating updates) owned by this pass's player
-        return sm.seg[k].fused && (g.upd_player == 0 || sm.seg[k].owner == g.upd_player);
-    };
-    for (int p = tid; p < T.npairs; p += nth) {
-        const int k = sm.pseg[p];
-        if (!upd_seg(k)) continue;
-        const long long q = sm.seg[k].qb + (p - sm.soff[k]);
-        const R r_t = rt[p];
-        const R r = upd_regret(up, sm.sreg[p], r_t);   // Eq 8/15 (Q4) / CFR+ (Q6) / Q18
-        g.regret[q] = r;
-        const R wp = w * sm.pib[k];
-        g.snum[q] = upd_sum(up, sm.ssn[p], wp * sm.ssig[p]);   // Eq 10 numerator
-        pos[p] = (r > (R)0) ? r : (R)0;
-    }
-    __syncthreads();
-    for (int k = tid; k < nseg; k += nth) {
-        if (!upd_seg(k)) continue;
-        g.sden[sm.seg[k].h] = upd_sum(up, sm.sden[k], w * sm.pib[k]);   // Eq 10 denominator
-        R z = (R)0;
-        for (int p = sm.soff[k]; p < sm.soff[k + 1]; ++p) z = z + pos[p];
-        sm.zs[k] = z;
-    }
-    __syncthreads();
-    bool bad = false;
-    for (int p = tid; p < T.npairs; p += nth) {
-        const int k = sm.pseg[p];
-        if (!upd_seg(k)) continue;
-        const int a = p - sm.soff[k];
-        const R z = sm.zs[k];
-        const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)sm.seg[k].n;   // Eq 9
-        g.sig[sm.seg[k].qb + a] = nsig;
-        if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
-    }
-    if (bad) atomicMin(&g.ctrl[1], t_iter);
-    if (last) {
-        __syncthreads();
-        if (tid == 0) g.ctrl[0] = t_iter;
-    }
-}
-
-template <class R, class I, int PC, int MODE>
-__global__ void __launch_bounds__(kTileSlots) k_bwd(DG<R, I> g, const R* __restrict__ sig, long long tile0,
-                                                    int br_player, int last, SmemLayout lay) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    bwd_tile<R, I, PC, MODE>(g, sig, tile0 + blockIdx.x, br_player, last, lay, smem_raw);
-}
-
-// ------------------------------------------------- pipelined backward pass
-// Persistent variant of k_bwd (MODE_CFR) for levels whose tiles are all "fast":
-// uniform child rows staged in 16/8-byte chunks, every infoset complete in its
-// tile (fused update), no chance nodes.  Each CTA walks tiles blockIdx.x,
-// blockIdx.x + gridDim.x, ... with a three-stage cp.async pipeline: while tile i
-// is computed, the data of tile i+1 and the metadata record of tile i+2 are in
-// flight, so the global-memory latency of one tile hides behind another's work.
-// The arithmetic is the same as k_bwd's (same order of every FP operation).
-struct FastHdr {
-    long long s0;    // first slot
-    int nslot, nseg, npairs, pad;
-};
-struct FastSeg {
-    long long h, qb;
-    int pair_off, n, owner, sb, se, pad;
-};
-struct FastLevel {
-    long long tile0, ntiles;   // tiles of the level
-    long long rec;             // byte offset of the level's records in the record pool
-    int recsize;               // bytes per record (16-byte multiple)
-    int maxslot, maxseg, maxpairs, maxch;
-    int rowlen, cpr, stride;   // uniform child rows
-    float inv_cpr;
-    int last;                  // 1: this launch ends the iteration
-    int pad;
-};
-
-// Shared-memory plan of k_bwd_fast: 3 metadata records, 2 data buffers (each
-// holding ch | ssig | sreg | ssn | spc | sph | sden), then per-tile work arrays.
-// Buffers are addressed as base + index * stride (no dynamically indexed
-// pointer arrays, which would live in local memory).
-struct FastPlan {
-    int meta, mstride;        // meta record k at meta + k * mstride
-    int data, dstride;        // data buffer k at data + k * dstride
-    int o_ssig, o_sreg, o_ssn, o_spc, o_sph, o_sden;   // offsets inside a data buffer
-    int sv, pib, zs, spoff, pseg, cm, ccnt;
-    int bytes;
-};
-__host__ __device__ inline FastPlan fast_plan(const FastLevel& L, int Pc, int w) {
-    FastPlan f;
-    auto al = [](int x) { return (x + 15) & ~15; };
-    const int pairs_b = al(L.maxpairs * w);
-    f.meta = 0;
-    f.mstride = al(L.recsize);
-    f.data = 3 * f.mstride;
-    int o = al(L.maxch * w > 2 * pairs_b ? L.maxch * w : 2 * pairs_b);
-    f.o_ssig = o; o += pairs_b;
-    f.o_sreg = o; o += pairs_b;
-    f.o_ssn = o; o += pairs_b;
-    f.o_spc = o; o += al(L.maxslot * w);
-    f.o_sph = o; o += al(L.maxslot * w);
-    f.o_sden = o; o += al(L.maxseg * w);
-    f.dstride = o;
-    int x = f.data + 2 * f.dstride;
-    f.sv = x; x += al(L.maxslot * Pc * w);
-    f.pib = x; x += al(L.maxseg * w);
-    f.zs = x; x += al(L.maxseg * w);
-    f.spoff = x; x += al(L.maxslot * 4);
-    f.pseg = x; x += al(L.maxpairs);
-    f.cm = x; x += al(L.maxslot * 2);
-    f.ccnt = x; x += al(L.maxseg * 4);
-    f.bytes = x;
-    return f;
-}
-
-// t = tile index within the level (records are level-local)
-template <class R, class I, int PC>
-__device__ __forceinline__ void fast_issue_meta(const unsigned char* __restrict__ pool, const FastLevel& L, long long t,
-                                                unsigned char* dst) {
-    const unsigned char* src = pool + L.rec + t * (long long)L.recsize;
-    for (int c = threadIdx.x; c < L.recsize / 16; c += blockDim.x) cp_async<16>(dst + c * 16, src + c * 16);
-}
-
-template <class R, class I, int PC>
-__device__ __forceinline__ void fast_issue_data(const DG<R, I>& g, const FastLevel& L, const unsigned char* meta,
-                                                R* ch, R* ssig, R* sreg, R* ssn, R* spc, R* sph, R* sden) {
-    constexpr int CH = (sizeof(R) == 8) ? 16 : 8;
-    constexpr int CE = CH / (int)sizeof(R);
-    const FastHdr& hd = *reinterpret_cast<const FastHdr*>(meta);
-    const FastSeg* seg = reinterpret_cast<const FastSeg*>(meta + 32);
-    const I* node = reinterpret_cast<const I*>(meta + 32 + hd.nseg * (int)sizeof(FastSeg));
-    const I* cb = node + hd.nslot;
-    const I* dec = cb + hd.nslot;
-    const unsigned char* sseg = reinterpret_cast<const unsigned char*>(dec + hd.nslot);
-    const unsigned char* pseg = sseg + hd.nslot;
-    (void)node;
-    const int P = g.P;
-    {
-        // 2-D walk: thread -> (row r0 + j * rpp, chunk k), no per-chunk division
-        const int rpp = blockDim.x / L.cpr;
-        const int r0 = threadIdx.x / L.cpr, k = threadIdx.x - r0 * L.cpr;
-        if (r0 < rpp)
-            for (int row = r0; row < hd.nslot; row += rpp)
-                cp_async<CH>(ch + row * L.stride + k * CE, g.U + (long long)cb[row] * PC + k * CE);
-    }
-    for (int s = threadIdx.x; s < hd.nslot; s += blockDim.x) {
-        const int k = sseg[s];
-        const long long d = (long long)dec[s];
-        const int i = seg[k].owner;
-        cp_async<(int)sizeof(R)>(spc + s, g.reach + d * 2 * P + (i - 1));
-        cp_async<(int)sizeof(R)>(sph + s, g.reach + d * 2 * P + P + (i - 1));
-    }
-    for (int p = threadIdx.x; p < hd.npairs; p += blockDim.x) {
-        const int k = pseg[p];
-        const long long q = seg[k].qb + (p - seg[k].pair_off);
-        cp_async<(int)sizeof(R)>(ssig + p, g.sig + q);
-        cp_async<(int)sizeof(R)>(sreg + p, g.regret + q);
-        cp_async<(int)sizeof(R)>(ssn + p, g.snum + q);
-    }
-    for (int k = threadIdx.x; k < hd.nseg; k += blockDim.x) cp_async<(int)sizeof(R)>(sden + k, g.sden + seg[k].h);
-    asm volatile("cp.async.commit_group;\n" ::);
-}
-
-template <class R, class I, int PC>
-__global__ void __launch_bounds__(2 * kTileSlots, 4) k_bwd_fast(DG<R, I> g, const unsigned char* __restrict__ pool,
-                                                         FastLevel L) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const FastPlan F = fast_plan(L, PC, (int)sizeof(R));
-    unsigned char* const B = smem_raw;
-    auto META = [&](int k) { return B + F.meta + k * F.mstride; };
-    auto DATA = [&](int k) { return B + F.data + k * F.dstride; };
-    R* const sv_ = (R*)(B + F.sv);
-    R* const pib_ = (R*)(B + F.pib);
-    R* const zs_ = (R*)(B + F.zs);
-    int* const spoff_ = (int*)(B + F.spoff);
-    unsigned char* const pseg_ = B + F.pseg;
-    short* const cm_ = (short*)(B + F.cm);      // members with nonzero pi_check, per segment
-    int* const ccnt_ = (int*)(B + F.ccnt);
-    auto ISSUE = [&](int mk, int dk) {
-        unsigned char* d = DATA(dk);
-        fast_issue_data<R, I, PC>(g, L, META(mk), (R*)d, (R*)(d + F.o_ssig), (R*)(d + F.o_sreg), (R*)(d + F.o_ssn),
-                                  (R*)(d + F.o_spc), (R*)(d + F.o_sph), (R*)(d + F.o_sden));
-    };
-    const int tid = threadIdx.x, nth = blockDim.x;
-    pdl_trigger();
-    long long t = blockIdx.x;
-    if (t >= L.ntiles) return;
-    // prologue: meta(t) (constant records: before the PDL wait) -> data(t), meta(t + G)
-    fast_issue_meta<R, I, PC>(pool, L, t, META(0));
-    asm volatile("cp.async.commit_group;\n" ::);
-    pdl_wait();
-    const long long t_iter = g.ctrl[0] + 1;
-    const Upd<R> up = make_upd<R>(g.variant, t_iter);
-    const R w = up.w;
-    cp_async_wait_all();
-    __syncthreads();
-    ISSUE(0, 0);
-    if (t + gridDim.x < L.ntiles) fast_issue_meta<R, I, PC>(pool, L, t + gridDim.x, META(1));
-    asm volatile("cp.async.commit_group;\n" ::);
-    bool bad = false;
-    for (int it = 0;; ++it) {
-        const int mb = it % 3, db = it & 1;
-        const long long tn = t + gridDim.x, tnn = t + 2 * (long long)gridDim.x;
-        cp_async_wait_all();      // data(t) and meta(tn) have landed
-        __syncthreads();
-        if (tn < L.ntiles) {
-            ISSUE((it + 1) % 3, db ^ 1);
-            if (tnn < L.ntiles) fast_issue_meta<R, I, PC>(pool, L, tnn, META((it + 2) % 3));
-            asm volatile("cp.async.commit_group;\n" ::);
-        }
-        // ---- compute tile t
-        const unsigned char* meta = META(mb);
-        const FastHdr hd = *reinterpret_cast<const FastHdr*>(meta);
-        const FastSeg* seg = reinterpret_cast<const FastSeg*>(meta + 32);
-        const I* node = reinterpret_cast<const I*>(meta + 32 + hd.nseg * (int)sizeof(FastSeg));
-        const unsigned char* rsseg = reinterpret_cast<const unsigned char*>(node + 3 * hd.nslot);
-        const unsigned char* rpseg = rsseg + hd.nslot;
-        unsigned char* dbuf = DATA(db);
-        R* ch = (R*)dbuf;
-        const R* ssig = (const R*)(dbuf + F.o_ssig);
-        const R* sreg = (const R*)(dbuf + F.o_sreg);
-        const R* ssn = (const R*)(dbuf + F.o_ssn);
-        const R* spc = (const R*)(dbuf + F.o_spc);
-        const R* sph = (const R*)(dbuf + F.o_sph);
-        const R* sden = (const R*)(dbuf + F.o_sden);
-        const int nslot = hd.nslot, nseg = hd.nseg, npairs = hd.npairs;
-        (void)pseg_;
-        (void)spoff_;
-        // phase A: node values (Eq 1), ascending actions from +0
-        if (tid < nslot) {
-            R v[PC];
-#pragma unroll
-            for (int j = 0; j < PC; ++j) v[j] = (R)0;
-            const R* row = ch + tid * L.stride;
-            const R* sg = ssig + seg[rsseg[tid]].pair_off;
-            const int n = L.rowlen / PC;
-            for (int a = 0; a < n; ++a) {
-                const R x = sg[a];
-#pragma unroll
-                for (int j = 0; j < PC; ++j) v[j] = v[j] + x * row[a * PC + j];
-            }
-            const long long nd = (long long)node[tid];
-#pragma unroll
-            for (int j = 0; j < PC; ++j) {
-                g.U[nd * PC + j] = v[j];
-                sv_[tid * PC + j] = v[j];
-            }
-        }
-        // members whose pi_check is zero contribute exact zeros to every r~ sum
-        // (slices of +-0 are 0): compact them away (warp ballot per segment)
-        {
-            const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
-            for (int k = warp; k < nseg; k += nwarps) {
-                const int sb = seg[k].sb, se = seg[k].se;
-                int cnt = 0;
-                for (int base = sb; base < se; base += 32) {
-                    const int s2 = base + lane;
-                    const bool f = (s2 < se) && (spc[s2] != (R)0);
-                    const unsigned m = __ballot_sync(0xffffffffu, f);
-                    if (f) cm_[sb + cnt + __popc(m & ((1u << lane) - 1u))] = (short)s2;
-                    cnt += __popc(m);
-                }
-                if (lane == 0) ccnt_[k] = cnt;
-            }
-        }
-        __syncthreads();
-        // phase B: exact sums (pairs, then one pi_bar item per segment)
-        const int nitems = npairs + nseg;
-        int ns = 1;
-        int lns = 0;                  // ns = 2^lns (shifts, no integer division)
-        while (ns < 8 && nitems * ns * 2 <= nth) { ns <<= 1; ++lns; }
-        const int rounds = (nitems * ns + nth - 1) / nth;
-        double kr0 = 0, kr1 = 0, kr2 = 0, kr3 = 0, kr4 = 0;
-        for (int rd = 0; rd < rounds; ++rd) {
-            const int wi = rd * nth + tid;
-            const int itm = wi >> lns, part = wi & (ns - 1);
-            double c0 = 0, c1 = 0, c2 = 0;
-            bool is_pair = false, neg = false;
-            int k = 0, a = 0;
-            if (itm < npairs) {
-                k = rpseg[itm];
-                a = itm - seg[k].pair_off;
-                is_pair = true;
-                neg = (PC == 1) && (seg[k].owner == 2);
-            } else if (itm < nitems) {
-                k = itm - npairs;
-            }
-            if (itm < nitems) {
-                const int col = (PC == 1) ? 0 : seg[k].owner - 1;
-                const int sb = seg[k].sb, se = seg[k].se;
-                if (!is_pair) {
-                    for (int ls = sb + part; ls < se; ls += ns) xadd(c0, c1, c2, (double)sph[ls], g.scp0);
-                } else {
-                    // two independent slice chains (ILP); integer-valued partial sums
-                    // combine exactly
-                    double e0 = 0, e1 = 0, e2 = 0;
-                    const short* mem = cm_ + sb;
-                    const int cnt = ccnt_[k];
-                    int j = part;
-                    for (; j + ns < cnt; j += 2 * ns) {
-                        const int la = mem[j], lb = mem[j + ns];
-                        const R ua = ch[la * L.stride + a * PC + col];
-                        const R ub = ch[lb * L.stride + a * PC + col];
-                        const R ta = spc[la] * (ua - sv_[la * PC + col]);
-                        const R tb = spc[lb] * (ub - sv_[lb * PC + col]);
-                        xadd(c0, c1, c2, (double)ta, g.sc0);
-                        xadd(e0, e1, e2, (double)tb, g.sc0);
-                    }
-                    if (j < cnt) {
-                        const int la = mem[j];
-                        const R ua = ch[la * L.stride + a * PC + col];
-                        const R ta = spc[la] * (ua - sv_[la * PC + col]);
-                        xadd(c0, c1, c2, (double)ta, g.sc0);
-                    }
-                    c0 += e0;
-                    c1 += e1;
-                    c2 += e2;
-                }
-                if (neg) { c0 = -c0; c1 = -c1; c2 = -c2; }
-            }
-            for (int o = 1; o < ns; o <<= 1) {
-                c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-                c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-                c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-            }
-            if (itm < nitems && part == 0) {
-                const double x = is_pair ? xdec(c0, c1, c2, g.rc) : xdec(c0, c1, c2, g.rcp);
-                if (rd == 0) kr0 = x;
-                else if (rd == 1) kr1 = x;
-                else if (rd == 2) kr2 = x;
-                else if (rd == 3) kr3 = x;
-                else kr4 = x;
-            }
-        }
-        __syncthreads();   // reads of ch done: rt / pos alias it
-        R* rt = ch;
-        R* pos = ch + (((npairs * (int)sizeof(R) + 15) & ~15) / (int)sizeof(R));
-        for (int rd = 0; rd < rounds && rd < 5; ++rd) {
-            const int wi = rd * nth + tid;
-            const int itm = wi >> lns, part = wi & (ns - 1);
-            if (itm < nitems && part == 0) {
-                const double x = rd == 0 ? kr0 : rd == 1 ? kr1 : rd == 2 ? kr2 : rd == 3 ? kr3 : kr4;
-                if (itm < npairs) rt[itm] = (R)x;
-                else pib_[itm - npairs] = (R)x;
-            }
-        }
-        __syncthreads();
-        // phase C: fused update (Eq 8/15 or CFR+, Eq 10, Eq 9)
-        for (int p = tid; p < npairs; p += nth) {
-            const int k = rpseg[p];
-            if (g.upd_player != 0 && seg[k].owner != g.upd_player) continue;   // alternating updates
-            const long long q = seg[k].qb + (p - seg[k].pair_off);
-            const R r_t = rt[p];
-            const R r = upd_regret(up, sreg[p], r_t);
-            g.regret[q] = r;
-            const R wp = w * pib_[k];
-            g.snum[q] = upd_sum(up, ssn[p], wp * ssig[p]);
-            pos[p] = (r > (R)0) ? r : (R)0;
-        }
-        __syncthreads();
-        for (int k = tid; k < nseg; k += nth) {
-            if (g.upd_player != 0 && seg[k].owner != g.upd_player) continue;
-            g.sden[seg[k].h] = upd_sum(up, sden[k], w * pib_[k]);
-            R z = (R)0;
-            for (int p = seg[k].pair_off; p < seg[k].pair_off + seg[k].n; ++p) z = z + pos[p];
-            zs_[k] = z;
-        }
-        __syncthreads();
-        for (int p = tid; p < npairs; p += nth) {
-            const int k = rpseg[p];
-            if (g.upd_player != 0 && seg[k].owner != g.upd_player) continue;
-            const int a = p - seg[k].pair_off;
-            const R z = zs_[k];
-            const R nsig = (z > (R)0) ? pos[p] / z : (R)1 / (R)seg[k].n;
-            g.sig[seg[k].qb + a] = nsig;
-            if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
-        }
-        __syncthreads();   // buffers of tile t may be refilled from here on
-        t = tn;
-        if (t >= L.ntiles) break;
-    }
-    if (bad) atomicMin(&g.ctrl[1], t_iter);
-    if (L.last) {
-        // last-block-done: the iteration counter advances once every CTA is done
-        if (tid == 0) {
-            __threadfence();
-            const unsigned long long prev = atomicAdd((unsigned long long*)&g.ctrl[2], 1ULL);
-            if (prev == gridDim.x - 1) {
-                g.ctrl[0] = t_iter;
-                g.ctrl[2] = 0;
-            }
-        }
-    }
-}
-
-// ------------------------------------------------- streaming backward pass
-// k_bwd_stream (MODE_CFR) serves levels whose slots are all player nodes with one
-// |A(h)| = n and whose infosets are complete in the level (fused update).  In the
-// slot-ordered device layout (u_rows) a tile of whole infosets reads ONE
-// contiguous block from every stream: child rows, reach rows, sigma / R / S_num of
-// its (h, a) pairs, S_den / owner of its infosets and the infosets' member starts.
-// A producer warp moves the blocks with TMA bulk copies (cp.async.bulk, mbarrier
-// complete_tx) into an S-stage ring; eight consumer warps compute the tile: Eq 1
-// values (phase A), exact sums of the cancelled-form regret terms (Eq 7, matrix
-// form P:313) and of pi_hat (Eq 5) (phase B), and the fused update Eq 8/15 + Eq 10
-// + Eq 9 (phase C).  Every FP operation and its order is k_bwd's.
-struct StreamLevel {
-    long long s0;           // first slot of the level
-    long long h0, q0;       // first internal infoset of the level, qbase[h0]
-    long long row0;         // U row of the level's first child row
-    long long ntiles;
-    long long rec;          // int4 offset of the level's tile records {k0, k1, m0, m1} in the pool
-    long long hs;           // int offset of the level's infoset member starts hs[nh + 1] in the pool
-    int n, rowlen;          // |A(h)|, n * Pc
-    int maxm, maxseg;       // per-tile maxima (members, infosets)
-    int stages, stage_bytes;
-    int o_rows, o_reach, o_sig, o_reg, o_snum, o_sden, o_own, o_hs, o_node;   // byte offsets inside a stage
-    int fused;              // 1: deepest decision level -- its forward pass (Eq 2 / Eq 4) is fused here
-    int o_pact, o_gsig;     // fused: parent actors, gathered incoming-edge sigma (reach area = parent rows)
-    unsigned ndiv_m;        // p / n == (p * ndiv_m) >> ndiv_s (64-bit) for p < 2^16 (host-verified)
-    int ndiv_s;
-    int umem;               // > 0: every infoset of the level has umem members (m / umem by udiv)
-    unsigned udiv_m;
-    int udiv_s;
-    int o_sv, o_cm, o_rt, o_pos, o_pib, o_zs, o_ccnt, o_bar;          // work arrays / barriers
-    int bytes;              // dynamic shared memory
-    int last;
-    int debug;              // timing experiments only: 1 consumers skip compute, 2 producer skips loads
-    int level;              // parent level (work counters)
-    int compact;            // 1: reach rows of this level are compact (pi_check, pi_hat of the actor; k_fwd compact)
-};
-constexpr int kStreamConsumers = 256;   // 8 consumer warps
-constexpr int kStreamThreads = kStreamConsumers + 32;   // + 1 producer warp
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(void* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(void* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// global -> shared bulk copy of a 16-byte-aligned window; completes on `bar`
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, void* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(kStreamConsumers) : "memory"); }
-
-// 16-byte window [lo, hi) around [p, p + bytes): returns lo, sets the window size
-// and the element offset of p inside it
-template <class T>
-__device__ __forceinline__ const unsigned char* window16(const T* p, long long count, unsigned* wbytes, int* off) {
-    const unsigned long long a = (unsigned long long)p;
-    const unsigned long long lo = a & ~15ull;
-    const unsigned long long hi = (a + (unsigned long long)count * sizeof(T) + 15ull) & ~15ull;
-    *wbytes = (unsigned)(hi - lo);
-    *off = (int)((a - lo) / sizeof(T));
-    return reinterpret_cast<const unsigned char*>(lo);
-}
-
-#ifdef CFR_STREAM_PROFILE
-__device__ unsigned long long g_stream_prof[80];   // [warp][8] cycles, [64] tiles
-extern "C" int cfr_debug_stream_profile(unsigned long long* out, int reset) {
-    cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, g_stream_prof, sizeof(g_stream_prof));
-    if (reset) {
-        unsigned long long z[80] = {0};
-        cudaMemcpyToSymbol(g_stream_prof, z, sizeof(z));
-    }
-    return 0;
-}
-#endif
-struct StreamHdr {
-    int k0, nseg, m0, M;        // first infoset (level-relative), infosets, first member, members
-    int po, ho, oo, hso;        // element offsets inside the windows: pairs, S_den, owner, hs
-    int no, pao, ro, rro;       // node-row / parent-actor / child-row / reach-row window offsets
-};
-
-#ifndef CFR_STREAM_MINB
-#define CFR_STREAM_MINB 2
-#endif
-template <class R, class I, int PC>
-__global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(DG<R, I> g, const int* __restrict__ pool,
-                                                                   StreamLevel L) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned char* const B = smem_raw;
-    unsigned long long* const full = reinterpret_cast<unsigned long long*>(B + L.o_bar);
-    unsigned long long* const empty = full + L.stages;
-    const int tid = threadIdx.x;
-    const int P = g.P;
-    const int n = L.n;
-    pdl_trigger();
-    if (tid == 0) {
-        for (int s = 0; s < L.stages; ++s) {
-            mbar_init(&full[s], L.fused ? 33 : 1);   // fused: + the producer lanes' cp.async arrivals
-            mbar_init(&empty[s], 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    {
-        int* ccnt = reinterpret_cast<int*>(B + L.o_ccnt);
-        for (int k = tid; k < 4 * L.maxseg; k += blockDim.x) ccnt[k] = 0;   // two tile buffers
-    }
-    __syncthreads();
-    pdl_wait();
-    const long long G = gridDim.x;
-
-    if (tid >= kStreamConsumers) {
-        // ------------------------------------------------------------ producer
-        // Lane 0 arms the stage and issues the TMA bulk copies.  On the fused level
-        // all 32 lanes also gather each member's parent reach row and incoming-edge
-        // sigma (cp.async, completion counted on the same barrier); the parent /
-        // edge indices of the next tile are prefetched into registers meanwhile.
-        const int plane = tid - kStreamConsumers;
-        if (!L.fused && plane != 0) return;   // lane 0 alone issues
-        const int4* recs = reinterpret_cast<const int4*>(pool) + L.rec;
-        const int* hs = pool + L.hs;
-        constexpr int GMAX = kStreamConsumers / 32;   // members per lane (maxm <= kStreamConsumers)
-        long long t = blockIdx.x;
-        int4 rec = (t < L.ntiles) ? recs[t] : make_int4(0, 0, 0, 0);
-        long long fp[GMAX], fe[GMAX];
-        auto prefetch = [&](const int4& r) {
-#pragma unroll
-            for (int q = 0; q < GMAX; ++q) {
-                const int m = q * 32 + plane;
-                const long long s = L.s0 + r.z + m;
-                fp[q] = (m < r.w - r.z) ? (long long)g.f_parent[s] : 0;
-                fe[q] = (m < r.w - r.z) ? (long long)g.f_e[s] : 0;
-            }
-        };
-        if (L.fused && t < L.ntiles) prefetch(rec);
-        int st = 0;
-        unsigned ph = 0;   // ring pass (parity of the empty barrier's phase to wait for)
-        for (int it = 0; t < L.ntiles; ++it, t += G) {
-            const int4 cur = rec;
-            if (t + G < L.ntiles) rec = recs[t + G];    // next record in flight during the wait
-            if (it >= L.stages) mbar_wait(&empty[st], (ph - 1u) & 1u);
-            unsigned char* S = B + (size_t)st * L.stage_bytes;
-            const int k0 = cur.x, k1 = cur.y, m0 = cur.z, m1 = cur.w;
-            const int nseg = k1 - k0, M = m1 - m0;
-            const long long slot = L.s0 + m0;
-            if (plane == 0) {
-                const long long q = L.q0 + (long long)k0 * n;
-                const long long h = L.h0 + k0;
-                unsigned b_rows, b_reach = 0, b_sig, b_reg, b_snum, b_sden, b_own, b_hs, b_node, b_pact = 0;
-                int o_rows, o_reach = 0, po, po2, po3, ho, oo, hso, no, pao = 0;
-                const unsigned char* w_rows = window16(g.U + (L.row0 + (long long)m0 * n) * PC, (long long)M * L.rowlen, &b_rows, &o_rows);
-                const unsigned char* w_reach = nullptr;
-                const unsigned char* w_pact = nullptr;
-                if (L.fused) w_pact = window16(g.f_pact + slot, M, &b_pact, &pao);
-                else if (L.compact) w_reach = window16(g.reach + L.s0 * 2 * P + (long long)m0 * 2, (long long)M * 2, &b_reach, &o_reach);
-                else w_reach = window16(g.reach + slot * 2 * P, (long long)M * 2 * P, &b_reach, &o_reach);
-                const unsigned char* w_sig = window16(g.sig + q, (long long)nseg * n, &b_sig, &po);
-                const unsigned char* w_reg = window16(g.regret + q, (long long)nseg * n, &b_reg, &po2);
-                const unsigned char* w_snum = window16(g.snum + q, (long long)nseg * n, &b_snum, &po3);
-                const unsigned char* w_sden = window16(g.sden + h, nseg, &b_sden, &ho);
-                const unsigned char* w_own = window16(g.owner + h, nseg, &b_own, &oo);
-                const unsigned char* w_hs = window16(hs + k0, nseg + 1, &b_hs, &hso);
-                const unsigned char* w_node = window16(g.s_node + slot, M, &b_node, &no);
-                StreamHdr* hd = reinterpret_cast<StreamHdr*>(S);
-                hd->k0 = k0;
-                hd->nseg = nseg;
-                hd->m0 = m0;
-                hd->M = M;
-                hd->po = po;
-                hd->ho = ho;
-                hd->oo = oo;
-                hd->hso = hso;
-                hd->no = no;
-                hd->pao = pao;
-                hd->ro = o_rows;
-                hd->rro = o_reach;
-                (void)po2; (void)po3;   // sigma / R / S_num share the pair window offset (same base alignment)
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                if (L.debug == 2) {   // timing experiment: no loads (consumers compute on stale data)
-                    mbar_expect_tx(&full[st], 0);
-                } else {
-                    mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs + b_node + b_pact);
-                    bulk_g2s(S + L.o_node, w_node, b_node, &full[st]);
-                    bulk_g2s(S + L.o_rows, w_rows, b_rows, &full[st]);
-                    if (L.fused) bulk_g2s(S + L.o_pact, w_pact, b_pact, &full[st]);
-                    else bulk_g2s(S + L.o_reach, w_reach, b_reach, &full[st]);
-                    bulk_g2s(S + L.o_sig, w_sig, b_sig, &full[st]);
-                    bulk_g2s(S + L.o_reg, w_reg, b_reg, &full[st]);
-                    bulk_g2s(S + L.o_snum, w_snum, b_snum, &full[st]);
-                    bulk_g2s(S + L.o_sden, w_sden, b_sden, &full[st]);
-                    bulk_g2s(S + L.o_own, w_own, b_own, &full[st]);
-                    bulk_g2s(S + L.o_hs, w_hs, b_hs, &full[st]);
-                }
-            }
-            if (L.fused) {
-                // gathers: parent reach row (2P values, 16-byte pieces) and sigma of
-                // the incoming edge, per member, into the stage
-                constexpr int RB = 2 * 2 * (int)sizeof(R);   // P = 2 fast path is the common case
-                R* prow = reinterpret_cast<R*>(S + L.o_reach);
-                R* gsig = reinterpret_cast<R*>(S + L.o_gsig);
-                const int rowb = 2 * P * (int)sizeof(R);
-                (void)RB;
-#pragma unroll
-                for (int q = 0; q < GMAX; ++q) {
-                    const int m = q * 32 + plane;
-                    if (m < M) {
-                        const unsigned char* src = reinterpret_cast<const unsigned char*>(g.reach + fp[q] * 2 * P);
-                        unsigned char* dst = reinterpret_cast<unsigned char*>(prow + (long long)m * 2 * P);
-                        for (int c = 0; c < rowb; c += 16) cp_async<16>(dst + c, src + c);
-                        cp_async<(int)sizeof(R)>(gsig + m, g.sig + fe[q]);
-                    }
-                }
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[st]))
-                             : "memory");
-                if (t + G < L.ntiles) prefetch(rec);
-            }
-            if (++st == L.stages) { st = 0; ++ph; }
-        }
-        return;
-    }
-
-    // -------------------------------------------------------------- consumers
-    const int lane = tid & 31;
-#ifdef CFR_STREAM_PROFILE
-    // timing experiment: per consumer warp, cycles between the marks below
-    unsigned long long sp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    auto sp_clock = []() {
-        long long c;
-        asm volatile("mov.u64 %0, %%clock64;\n" : "=l"(c)::"memory");
-        return c;
-    };
-    long long sp_last = sp_clock();
-#define SPROF(k)                                      \
-    do {                                              \
-        const long long now_ = sp_clock();            \
-        sp_acc[k] += (unsigned long long)(now_ - sp_last); \
-        sp_last = now_;                               \
-    } while (0)
-#else
-#define SPROF(k) do { } while (0)
-#endif
-    R* const sv = reinterpret_cast<R*>(B + L.o_sv);
-    short* const cm = reinterpret_cast<short*>(B + L.o_cm);
-    R* const rt = reinterpret_cast<R*>(B + L.o_rt);
-    R* const pos = reinterpret_cast<R*>(B + L.o_pos);
-    R* const pib = reinterpret_cast<R*>(B + L.o_pib);
-    // compaction counters [pi_check | pi_hat][maxseg], double-buffered by tile parity:
-    // a tile's buffer is zeroed after its end barrier, while the next tile uses the other
-    int* const ccnt_buf = reinterpret_cast<int*>(B + L.o_ccnt);
-    int tpar = 0;
-    const long long t_iter = g.ctrl[0] + 1;
-    const Upd<R> up = make_upd<R>(g.variant, t_iter);
-    const R w = up.w;
-    bool bad = false;
-    const bool all_live = g.variant >= 2;   // discounting changes every infoset: no identity updates
-    const R inv_n = (R)1 / (R)n;   // uniform strategy of the level's infosets (Eq 9, z = 0)
-    const int rs = L.compact ? 2 : 2 * P;   // reach row stride in the stage (elements)
-    unsigned long long live_h = 0, all_h = 0;   // updated / visited infosets (thread 0)
-    long long t = blockIdx.x;
-    int st = 0;
-    unsigned ph = 0;
-    for (; t < L.ntiles; t += G) {
-        unsigned char* S = B + (size_t)st * L.stage_bytes;
-        const StreamHdr* hdp = reinterpret_cast<const StreamHdr*>(S);
-        int* const ccnt = ccnt_buf + tpar * 2 * L.maxseg;
-        SPROF(0); mbar_wait(&full[st], ph & 1u); SPROF(1);
-        const StreamHdr hd = *hdp;
-        const R* rows = reinterpret_cast<const R*>(S + L.o_rows) + hd.ro;
-        const R* reach = reinterpret_cast<const R*>(S + L.o_reach) + hd.rro;
-        // 16-byte row reads need 16-byte aligned rows in the stage
-        const bool vec_rows = (((unsigned)L.rowlen * (unsigned)sizeof(R)) & 15u) == 0 &&
-                              (((unsigned)hd.ro * (unsigned)sizeof(R)) & 15u) == 0;
-        const R* ssig = reinterpret_cast<const R*>(S + L.o_sig) + hd.po;
-        const R* sreg = reinterpret_cast<const R*>(S + L.o_reg) + hd.po;
-        const R* ssn = reinterpret_cast<const R*>(S + L.o_snum) + hd.po;
-        const R* sden = reinterpret_cast<const R*>(S + L.o_sden) + hd.ho;
-        const unsigned char* own = reinterpret_cast<const unsigned char*>(S + L.o_own) + hd.oo;
-        const int* hs = reinterpret_cast<const int*>(S + L.o_hs) + hd.hso;   // level-relative member starts
-        const I* snode = reinterpret_cast<const I*>(S + L.o_node) + hd.no;   // U rows of the members
-        const unsigned char* pact = reinterpret_cast<const unsigned char*>(S + L.o_pact) + hd.pao;   // fused only
-        const R* gsig = reinterpret_cast<const R*>(S + L.o_gsig);                                  // fused only
-        const int nseg = hd.nseg, M = hd.M, m0 = hd.m0;
-
-        if (L.debug == 1) {   // timing experiment: data movement only
-            consumers_sync();
-            if (tid == 0) mbar_arrive(&empty[st]);
-            if (++st == L.stages) { st = 0; ++ph; }
-            tpar ^= 1;
-            continue;
-        }
-
-        // ---- phase A: node values (Eq 1, ascending actions from +0); compaction of
-        // the members with nonzero pi_check (their regret terms are exact zeros)
-        // and of those with nonzero pi_hat (their pi_bar terms are exact zeros)
-        for (int base = 0; base < M; base += kStreamConsumers) {
-            const int m = base + tid;
-            const bool active = m < M;
-            int k = 0;
-            R pc = (R)0, ph = (R)0;
-            if (active) {
-                const long long node = (long long)snode[m];
-                if (L.umem > 0) {
-                    // every infoset of the level has umem members: k = m / umem
-                    k = (int)(((unsigned long long)(unsigned)m * L.udiv_m) >> L.udiv_s);
-                } else {
-                    int lo = 0, hi = nseg - 1;
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (hs[mid] - m0 <= m) lo = mid; else hi = mid - 1;
-                    }
-                    k = lo;
-                }
-                R v[PC];
-#pragma unroll
-                for (int j = 0; j < PC; ++j) v[j] = (R)0;
-                const R* row = rows + (long long)m * L.rowlen;
-                const R* sg = ssig + k * n;
-                if (L.debug & 16) {   // timing experiment: no value loop
-                } else if (PC == 1 && vec_rows) {
-                    // 16-byte row reads (vec_rows: rows 16-byte aligned in the stage)
-                    using V = typename std::conditional<sizeof(R) == 8, double2, float4>::type;
-                    constexpr int E = 16 / (int)sizeof(R);
-                    const V* row4 = reinterpret_cast<const V*>(row);
-                    if ((reinterpret_cast<unsigned long long>(sg) & 15ull) == 0) {
-                        // sigma row 16-byte aligned: vector loads of it too.  Row chunks
-                        // are read in pairs, each lane starting with chunk 2j + d, d =
-                        // bit 2 of the member: rows of 8 consecutive members then fall
-                        // in 8 distinct 16-byte bank groups (a row of an even number of
-                        // chunks would otherwise give 2-way conflicts); the additions
-                        // stay in ascending action order
-                        const V* sg4 = reinterpret_cast<const V*>(sg);
-                        const int d = (m >> 2) & 1;
-                        const int nc = n / E;
-                        int c = 0;
-                        for (; c + 1 < nc; c += 2) {
-                            const V p0 = row4[c + d];
-                            const V p1 = row4[c + 1 - d];
-                            const V x0 = sg4[c], x1 = sg4[c + 1];
-                            const R* ua = reinterpret_cast<const R*>(d ? &p1 : &p0);
-                            const R* ub = reinterpret_cast<const R*>(d ? &p0 : &p1);
-                            const R* xa = reinterpret_cast<const R*>(&x0);
-                            const R* xb = reinterpret_cast<const R*>(&x1);
-#pragma unroll
-                            for (int e = 0; e < E; ++e) v[0] = v[0] + xa[e] * ua[e];
-#pragma unroll
-                            for (int e = 0; e < E; ++e) v[0] = v[0] + xb[e] * ub[e];
-                        }
-                        if (c < nc) {
-                            const V u = row4[c];
-                            const V x = sg4[c];
-                            const R* ue = reinterpret_cast<const R*>(&u);
-                            const R* xe = reinterpret_cast<const R*>(&x);
-#pragma unroll
-                            for (int e = 0; e < E; ++e) v[0] = v[0] + xe[e] * ue[e];
-                        }
-                    } else {
-                        for (int a = 0; a < n; a += E) {
-                            const V u = row4[a / E];
-                            const R* ue = reinterpret_cast<const R*>(&u);
-#pragma unroll
-                            for (int e = 0; e < E; ++e) v[0] = v[0] + sg[a + e] * ue[e];
-                        }
-                    }
-                } else {
-                    for (int a = 0; a < n; ++a) {
-                        const R x = sg[a];
-#pragma unroll
-                        for (int j = 0; j < PC; ++j) v[j] = v[j] + x * row[a * PC + j];
-                    }
-                }
-                SPROF(2);
-#pragma unroll
-                for (int j = 0; j < PC; ++j) {
-                    if (!(L.debug & 4)) g.U[node * PC + j] = v[j];   // (debug bit 4: timing experiment)
-                    sv[m * PC + j] = v[j];
-                }
-                const int i = own[k];
-                if (L.fused) {
-                    // forward pass of this member (Eq 2 pi_check and Eq 4 pi_hat, reading
-                    // Q1; the k_fwd arithmetic) from its gathered parent row and edge
-                    // sigma; the actor's two factors replace the parent row in place
-                    R* prow = const_cast<R*>(reach) + (long long)m * 2 * P;
-                    const R x = gsig[m];
-                    const int act = pact[m];
-                    const R pcp = prow[i - 1], php = prow[P + i - 1];
-                    pc = (act != i) ? pcp * x : pcp;
-                    ph = (act == i) ? php * x : php;
-                    prow[0] = pc;
-                    prow[1] = ph;
-                } else {
-                    pc = reach[(long long)m * rs + (L.compact ? 0 : i - 1)];
-                    ph = reach[(long long)m * rs + (L.compact ? 1 : P + i - 1)];
-                }
-            }
-            SPROF(3);
-            if (L.debug & 32) continue;   // timing experiment: no compaction
-            // a warp whose members all have zero reach has nothing to compact
-            if (__ballot_sync(0xffffffffu, active && (pc != (R)0 || ph != (R)0)) == 0u) continue;
-            const int key = active ? k : -1;
-            const unsigned grp = __match_any_sync(0xffffffffu, key);
-            const int leader = __ffs(grp) - 1;
-            const unsigned lt = (1u << lane) - 1u;
-            const unsigned nzc = grp & __ballot_sync(0xffffffffu, active && pc != (R)0);
-            const unsigned nzh = grp & __ballot_sync(0xffffffffu, active && ph != (R)0);
-            int bc = 0, bh = 0;
-            if (lane == leader && key >= 0) {
-                if (nzc) bc = atomicAdd(&ccnt[k], __popc(nzc));
-                if (nzh) bh = atomicAdd(&ccnt[L.maxseg + k], __popc(nzh));
-            }
-            bc = __shfl_sync(0xffffffffu, bc, leader);
-            bh = __shfl_sync(0xffffffffu, bh, leader);
-            if (active && pc != (R)0) cm[(hs[k] - m0) + bc + __popc(nzc & lt)] = (short)m;
-            if (active && ph != (R)0) cm[L.maxm + (hs[k] - m0) + bh + __popc(nzh & lt)] = (short)m;
-        }
-        SPROF(4); consumers_sync(); SPROF(5);
-
-        // ---- phases B + C, a warp per LIVE infoset (no CTA barrier in between).
-        // Live: some member has a nonzero pi_check (r~ may be nonzero) or pi_hat
-        // (pi_bar may be nonzero).  For a dead infoset every term is an exact zero:
-        // r~ = +0 and pi_bar = +0, so R, S_num, S_den and sigma keep their bits and
-        // its update (and its writes) are skipped.  (Splitting a live infoset's
-        // members over several warps, combined after a CTA barrier, was measured
-        // slower: live infosets mostly have few live members.)
-        const long long qt = L.q0 + (long long)hd.k0 * n;
-        const long long ht = L.h0 + hd.k0;
-        {
-            const int warp = tid >> 5;
-            const unsigned live = __ballot_sync(
-                0xffffffffu, lane < nseg && (g.upd_player == 0 || own[lane] == g.upd_player) &&
-                                 (all_live || ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0));
-            if (tid == 0) {
-                live_h += __popc(live);
-                all_h += nseg;
-            }
-            // phase B items of one infoset: n pairs (r~) + 1 pi_bar, ns lanes each
-            int ns = 1, lns = 0;
-            while (ns < 32 && (n + 1) * ns * 2 <= 32) { ns <<= 1; ++lns; }
-            const int ipr = 32 >> lns;   // items per round
-            int j = 0;
-            for (unsigned lm = live; lm; lm &= lm - 1u, ++j) {
-                if ((j & (kStreamConsumers / 32 - 1)) != warp) continue;
-                const int k = __ffs(lm) - 1;
-                const int i = own[k];
-                const int col = (PC == 1) ? 0 : i - 1;
-                const int sb = hs[k] - m0;
-                const int cntc = ccnt[k], cnth = ccnt[L.maxseg + k];
-                const short* memc = cm + sb;
-                const short* memh = cm + L.maxm + sb;
-                const bool two = L.fused || L.compact;
-                const int oc = two ? 0 : i - 1, oh = two ? 1 : P + i - 1;   // pi_check / pi_hat in a reach row
-                // ---- phase B: exact sums (slices of integer-valued doubles combine
-                // exactly in any order)
-                for (int base = 0; base <= n; base += ipr) {
-                    const int itm = base + (lane >> lns), part = lane & (ns - 1);
-                    double c0 = 0, c1 = 0, c2 = 0;
-                    if (itm < n) {
-                        const int a = itm;
-                        double e0 = 0, e1 = 0, e2 = 0;   // second independent slice chain (ILP)
-                        int jj = part;
-                        for (; jj + ns < cntc; jj += 2 * ns) {
-                            const int la = memc[jj], lb = memc[jj + ns];
-                            const R ua = rows[(long long)la * L.rowlen + a * PC + col];
-                            const R ub = rows[(long long)lb * L.rowlen + a * PC + col];
-                            const R ta = reach[(long long)la * rs + oc] * (ua - sv[la * PC + col]);
-                            const R tb = reach[(long long)lb * rs + oc] * (ub - sv[lb * PC + col]);
-                            xadd(c0, c1, c2, (double)ta, g.sc0);
-                            xadd(e0, e1, e2, (double)tb, g.sc0);
-                        }
-                        if (jj < cntc) {
-                            const int la = memc[jj];
-                            const R ua = rows[(long long)la * L.rowlen + a * PC + col];
-                            const R ta = reach[(long long)la * rs + oc] * (ua - sv[la * PC + col]);
-                            xadd(c0, c1, c2, (double)ta, g.sc0);
-                        }
-                        c0 += e0;
-                        c1 += e1;
-                        c2 += e2;
-                        if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
-                    } else if (itm == n) {
-                        for (int jj = part; jj < cnth; jj += ns)
-                            xadd(c0, c1, c2, (double)reach[(long long)memh[jj] * rs + oh], g.scp0);
-                    }
-                    for (int o = 1; o < ns; o <<= 1) {
-                        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-                        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-                        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-                    }
-                    if (part == 0) {
-                        if (itm < n) rt[k * n + itm] = (R)xdec(c0, c1, c2, g.rc);
-                        else if (itm == n) pib[k] = (R)xdec(c0, c1, c2, g.rcp);
-                    }
-                }
-                __syncwarp();
-                // ---- phase C: Eq 8/15 or CFR+, Eq 10, then Eq 9 (z ascending)
-                const R wp = w * pib[k];
-                for (int c = 0; c < n; c += 32) {
-                    const int a = c + lane;
-                    if (a < n) {
-                        const int p = k * n + a;
-                        const R r_t = rt[p];
-                        const R r = upd_regret(up, sreg[p], r_t);   // Eq 8/15 (Q4) / CFR+ (Q6) / Q18
-                        if (!(L.debug & 8)) {   // (debug bit 8: timing experiment)
-                            g.regret[qt + p] = r;
-                            g.snum[qt + p] = upd_sum(up, ssn[p], wp * ssig[p]);  // Eq 10 numerator
-                        }
-                        pos[p] = (r > (R)0) ? r : (R)0;
-                    }
-                }
-                __syncwarp();
-                R z = (R)0;
-                const R* pk = pos + k * n;
-#pragma unroll 4
-                for (int b = 0; b < n; ++b) z = z + pk[b];   // broadcast reads, ascending
-                if (lane == 0 && !(L.debug & 8)) g.sden[ht + k] = upd_sum(up, sden[k], wp);   // Eq 10 denominator
-                for (int c = 0; c < n; c += 32) {
-                    const int a = c + lane;
-                    if (a < n) {
-                        const int p = k * n + a;
-                        const R nsig = (z > (R)0) ? pos[p] / z : inv_n;   // Eq 9
-                        if (!(L.debug & 8)) g.sig[qt + p] = nsig;
-                        if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
-                    }
-                }
-            }
-        }
-        SPROF(6); consumers_sync();   // every read of this stage is done
-        SPROF(7);
-        if (tid == 0) mbar_arrive(&empty[st]);
-        for (int k = tid; k < 2 * L.maxseg; k += kStreamConsumers) ccnt[k] = 0;   // for the tile after next
-        tpar ^= 1;
-        if (++st == L.stages) { st = 0; ++ph; }
-    }
-#ifdef CFR_STREAM_PROFILE
-    if (lane == 0)
-        for (int k = 0; k < 8; ++k) atomicAdd(&g_stream_prof[(tid >> 5) * 8 + k], sp_acc[k]);
-    if (tid == 0) atomicAdd(&g_stream_prof[64], (unsigned long long)((L.ntiles - blockIdx.x + G - 1) / G));
-#endif
-#undef SPROF
-    if (bad) atomicMin(&g.ctrl[1], t_iter);
-    if (tid == 0) {
-        // cumulative: infosets updated / visited by the streaming levels (bench.py's
-        // byte model counts update writes of live infosets only)
-        unsigned long long* c = g.lcnt + 4 * L.level;
-        atomicAdd(c + 0, live_h);
-        atomicAdd(c + 1, live_h * (unsigned long long)n);
-        atomicAdd(c + 2, all_h);
-        atomicAdd(c + 3, all_h * (unsigned long long)n);
-    }
-    if (L.last) {
-        consumers_sync();
-        if (tid == 0) {
-            __threadfence();
-            const unsigned long long prev = atomicAdd((unsigned long long*)&g.ctrl[2], 1ULL);
-            if (prev == gridDim.x - 1) {
-                g.ctrl[0] = t_iter;
-                g.ctrl[2] = 0;
-            }
-        }
-    }
-}
-
-// Update of deferred infosets (span several depths / tiles): decode the global
-// exact sums, then the same Eq 8/15, Eq 10, Eq 9 steps; zero the accumulators.
-template <class R, class I>
-__device__ __forceinline__ void deferred_body(const DG<R, I>& g, int last) {
-    pdl_trigger();
-    pdl_wait();
-    const long long t_iter = g.ctrl[0] + 1;
-    const Upd<R> up = make_upd<R>(g.variant, t_iter);
-    const R w = up.w;
-    bool bad = false;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < g.ndef; idx += stride) {
-        const long long h = (long long)g.deferred[idx];
-        const long long qb = (long long)g.qbase[h];
-        const int n = (int)((long long)g.qbase[h + 1] - qb);
-        const long long dq = g.dqbase[idx];
-        const long long p0 = (long long)g.acc_p[idx * 3 + 0], p1 = (long long)g.acc_p[idx * 3 + 1],
-                        p2 = (long long)g.acc_p[idx * 3 + 2];
-        g.acc_p[idx * 3 + 0] = 0;
-        g.acc_p[idx * 3 + 1] = 0;
-        g.acc_p[idx * 3 + 2] = 0;
-        if (g.upd_player != 0 && g.owner[h] != g.upd_player) {
-            // alternating updates: another player's infoset -- zero its sums only
-            for (int a = 0; a < 3 * n; ++a) g.acc_r[dq * 3 + a] = 0;
-            continue;
-        }
-        const R pib = (R)xdec_ll(p0, p1, p2, g.rcp);
-        const R wp = w * pib;
-        R z = (R)0;
-        for (int a = 0; a < n; ++a) {
-            const long long q = qb + a;
-            const long long cq = dq + a;
-            const long long c0 = (long long)g.acc_r[cq * 3 + 0], c1 = (long long)g.acc_r[cq * 3 + 1],
-                            c2 = (long long)g.acc_r[cq * 3 + 2];
-            g.acc_r[cq * 3 + 0] = 0;
-            g.acc_r[cq * 3 + 1] = 0;
-            g.acc_r[cq * 3 + 2] = 0;
-            const R rt = (R)xdec_ll(c0, c1, c2, g.rc);
-            g.regret[q] = upd_regret(up, g.regret[q], rt);
-            g.snum[q] = upd_sum(up, g.snum[q], wp * g.sig[q]);
-        }
-        g.sden[h] = upd_sum(up, g.sden[h], wp);
-        for (int a = 0; a < n; ++a) {
-            const R r = g.regret[qb + a];
-            z = z + ((r > (R)0) ? r : (R)0);
-        }
-        for (int a = 0; a < n; ++a) {
-            const R r = g.regret[qb + a];
-            const R pos = (r > (R)0) ? r : (R)0;
-            const R nsig = (z > (R)0) ? pos / z : (R)1 / (R)n;
-            g.sig[qb + a] = nsig;
-            if (!finite_(r) || !finite_(nsig)) bad = true;
-        }
-    }
-    if (bad) atomicMin(&g.ctrl[1], t_iter);
-    if (last) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            const unsigned long long prev = atomicAdd((unsigned long long*)&g.ctrl[2], 1ULL);
-            if (prev == gridDim.x - 1) {
-                g.ctrl[0] = t_iter;
-                g.ctrl[2] = 0;
-            }
-        }
-    }
-}
-
-template <class R, class I>
-__global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
-    deferred_body<R, I>(g, last);
-}
-
-// --------------------------------------------------- persistent iteration
-// Small games are launch-latency bound (2D kernels per iteration).  k_persist runs
-// T whole iterations in ONE cooperative launch: every CTA is resident; the levels
-// of an iteration are separated by grid-wide barriers (the same forward, tile and
-// deferred bodies as the per-level kernels, so the arithmetic is identical).
-struct PLevel {
-    long long s0, s1;   // slots of depth l (forward pass of level l)
-    long long t0, t1;   // tiles of parent depth L (backward pass)
-    SmemLayout lay;     // tile shared-memory layout of depth L
-};
-
-// Sense-free grid barrier: bar[0] arrivals, bar[1] generation.  Thread 0 arrives
-// after a gpu-scope fence (the block's writes are visible) and leaves after one
-// (other blocks' writes are visible to the block, L1 included).
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g0 = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g0) __nanosleep(32);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-template <class R, class I, int PC, int PT>
-__global__ void __launch_bounds__(kTileSlots) k_persist(DG<R, I> g, const PLevel* __restrict__ lv, int D, int has_def,
-                                                         long long T, unsigned* bar) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    long long t_done = g.ctrl[0];
-    for (long long it = 0; it < T; ++it) {
-        for (int l = 1; l < D; ++l) {   // forward pass, depth 1 .. D-1
-            const long long s0 = lv[l].s0, s1 = lv[l].s1;
-            if (s1 <= s0) continue;
-            fwd_body<R, I, PT>(g, g.sig, s0, s1, 0);
-            grid_sync(bar);
-        }
-        for (int L = D - 1; L >= 0; --L) {   // backward pass, parent depth D-1 .. 0
-            const long long t0 = lv[L].t0, t1 = lv[L].t1;
-            if (t1 <= t0) continue;
-            const SmemLayout lay = lv[L].lay;
-            for (long long t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
-                __syncthreads();   // the previous tile's shared-memory reads are done
-                bwd_tile<R, I, PC, MODE_CFR>(g, g.sig, t, 0, 0, lay, smem_raw);
-            }
-            grid_sync(bar);
-        }
-        if (has_def) {
-            deferred_body<R, I>(g, 0);
-            grid_sync(bar);
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) g.ctrl[0] = ++t_done;   // the iteration is complete
-        else ++t_done;
-        grid_sync(bar);
-    }
-}
-
-// ------------------------------------------------------------- tiny games
-// Games whose whole mutable state fits in one CTA's shared memory (Kuhn; Leduc in
-// f32) are bound by per-level latency, not bytes.  k_tiny runs T iterations in
-// ONE CTA: U, reach, sigma, R, S_num, S_den (and the per-level r~ / pi_bar) live
-// in shared memory; levels are separated by __syncthreads; read-only metadata
-// comes from global memory through L1.  Same operations, same order as the
-// per-level kernels (requires depth-homogeneous infosets: an infoset's members
-// are the contiguous slots mem_of[2h] .. mem_of[2h+1] of one level).
-struct TinyLevel {
-    long long s0, s1;   // slots of depth l
-    long long h0, h1;   // internal infosets at depth l (consecutive)
-};
-struct TinyPlan {
-    long long U, reach, sig, reg, snum, sden, rt, pib;   // element offsets in shared memory (R units)
-    long long nU, nreach, nsig, Q, H;
-    int bytes;
-};
-
-template <class R, class I, int PC>
-__global__ void __launch_bounds__(1024) k_tiny(DG<R, I> g, const TinyLevel* __restrict__ lv, const I* __restrict__ mem_of,
-                                                int D, long long T, TinyPlan tp) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    R* const sm = reinterpret_cast<R*>(smem_raw);
-    R* const U = sm + tp.U;
-    R* const reach = sm + tp.reach;
-    R* const sig = sm + tp.sig;
-    R* const reg = sm + tp.reg;
-    R* const snum = sm + tp.snum;
-    R* const sden = sm + tp.sden;
-    R* const rtb = sm + tp.rt;
-    R* const pibb = sm + tp.pib;
-    const int tid = threadIdx.x, nth = blockDim.x;
-    const int P = g.P;
-    pdl_trigger();
-    pdl_wait();
-    for (long long k = tid; k < tp.nU; k += nth) U[k] = g.U[k];
-    for (long long k = tid; k < tp.nreach; k += nth) reach[k] = g.reach[k];
-    for (long long k = tid; k < tp.nsig; k += nth) sig[k] = g.sig[k];
-    for (long long k = tid; k < tp.Q; k += nth) {
-        reg[k] = g.regret[k];
-        snum[k] = g.snum[k];
-    }
-    for (long long k = tid; k < tp.H; k += nth) sden[k] = g.sden[k];
-    __syncthreads();
-    long long t_iter = g.ctrl[0];
-    bool bad = false;
-    for (long long it = 0; it < T; ++it) {
-        ++t_iter;
-        const Upd<R> up = make_upd<R>(g.variant, t_iter);
-        const R w = up.w;
-        const int passes = (g.variant == 4) ? P : 1;
-        for (int pass = 1; pass <= passes; ++pass) {
-            const int upl = (passes > 1) ? pass : 0;
-            for (int l = 1; l < D; ++l) {   // forward (Eq 2, Eq 4 with reading Q1)
-                for (long long s = lv[l].s0 + tid; s < lv[l].s1; s += nth) {
-                    const long long p = (long long)g.f_parent[s];
-                    const R x = sig[g.f_e[s]];
-                    const int act = g.f_pact[s];
-                    for (int j = 0; j < P; ++j) {
-                        const R pc = reach[p * 2 * P + j], ph = reach[p * 2 * P + P + j];
-                        reach[s * 2 * P + j] = (act != j + 1) ? pc * x : pc;
-                        reach[s * 2 * P + P + j] = (act == j + 1) ? ph * x : ph;
-                    }
-                }
-                __syncthreads();
-            }
-            for (int L = D - 1; L >= 0; --L) {
-                for (long long s = lv[L].s0 + tid; s < lv[L].s1; s += nth) {   // values (Eq 1)
-                    const long long cb = (long long)g.s_cb[s], eb = (long long)g.s_ebase[s];
-                    const int nch = g.s_n[s];
-                    R v[PC];
-#pragma unroll
-                    for (int j = 0; j < PC; ++j) v[j] = (R)0;
-                    for (int a = 0; a < nch; ++a) {
-                        const R x = sig[eb + a];
-#pragma unroll
-                        for (int j = 0; j < PC; ++j) v[j] = v[j] + x * U[(cb + a) * PC + j];
-                    }
-                    const long long node = (long long)g.s_node[s];
-#pragma unroll
-                    for (int j = 0; j < PC; ++j) U[node * PC + j] = v[j];
-                }
-                __syncthreads();
-                const long long h0 = lv[L].h0, h1 = lv[L].h1;
-                if (h1 > h0) {
-                    const long long q0 = (long long)g.qbase[h0], q1 = (long long)g.qbase[h1];
-                    const long long items = (q1 - q0) + (h1 - h0);
-                    for (long long x = tid; x < items; x += nth) {   // exact sums
-                        double c0 = 0, c1 = 0, c2 = 0;
-                        if (x < q1 - q0) {
-                            const long long q = q0 + x;
-                            long long lo = h0, hi = h1 - 1;
-                            while (lo < hi) {
-                                const long long mid = (lo + hi + 1) >> 1;
-                                if ((long long)g.qbase[mid] <= q) lo = mid; else hi = mid - 1;
-                            }
-                            const long long h = lo;
-                            const int i = g.owner[h];
-                            if (upl != 0 && i != upl) continue;
-                            const int a = (int)(q - (long long)g.qbase[h]);
-                            const int col = (PC == 1) ? 0 : i - 1;
-                            for (long long d = (long long)mem_of[2 * h]; d < (long long)mem_of[2 * h + 1]; ++d) {
-                                const R pc = reach[d * 2 * P + (i - 1)];
-                                if (pc == (R)0) continue;   // exact zero terms
-                                const R u = U[((long long)g.s_cb[d] + a) * PC + col];
-                                const R v = U[(long long)g.s_node[d] * PC + col];
-                                xadd(c0, c1, c2, (double)(pc * (u - v)), g.sc0);
-                            }
-                            if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
-                            rtb[q] = (R)xdec(c0, c1, c2, g.rc);
-                        } else {
-                            const long long h = h0 + (x - (q1 - q0));
-                            const int i = g.owner[h];
-                            if (upl != 0 && i != upl) continue;
-                            for (long long d = (long long)mem_of[2 * h]; d < (long long)mem_of[2 * h + 1]; ++d)
-                                xadd(c0, c1, c2, (double)reach[d * 2 * P + P + (i - 1)], g.scp0);
-                            pibb[h] = (R)xdec(c0, c1, c2, g.rcp);
-                        }
-                    }
-                    __syncthreads();
-                    for (long long h = h0 + tid; h < h1; h += nth) {   // update (Eq 8/15 / CFR+ / Q18, Eq 10, Eq 9)
-                        const int i = g.owner[h];
-                        if (upl != 0 && i != upl) continue;
-                        const long long qb = (long long)g.qbase[h];
-                        const int n = (int)((long long)g.qbase[h + 1] - qb);
-                        const R wp = w * pibb[h];
-                        R z = (R)0;
-                        for (int a = 0; a < n; ++a) {
-                            const long long q = qb + a;
-                            const R r = upd_regret(up, reg[q], rtb[q]);
-                            reg[q] = r;
-                            snum[q] = upd_sum(up, snum[q], wp * sig[q]);
-                            z = z + ((r > (R)0) ? r : (R)0);
-                        }
-                        sden[h] = upd_sum(up, sden[h], wp);
-                        for (int a = 0; a < n; ++a) {
-                            const long long q = qb + a;
-                            const R r = reg[q];
-                            const R pos = (r > (R)0) ? r : (R)0;
-                            const R nsig = (z > (R)0) ? pos / z : (R)1 / (R)n;
-                            sig[q] = nsig;
-                            if (!finite_(rtb[q]) || !finite_(nsig) || !finite_(z)) bad = true;
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    // write the state back (readbacks and later launches read it from global)
-    for (long long k = tid; k < tp.nU; k += nth) g.U[k] = U[k];
-    for (long long k = tid; k < tp.nreach; k += nth) g.reach[k] = reach[k];
-    for (long long k = tid; k < tp.nsig; k += nth) g.sig[k] = sig[k];
-    for (long long k = tid; k < tp.Q; k += nth) {
-        g.regret[k] = reg[k];
-        g.snum[k] = snum[k];
-    }
-    for (long long k = tid; k < tp.H; k += nth) g.sden[k] = sden[k];
-    if (bad) atomicMin(&g.ctrl[1], t_iter);
-    if (tid == 0) g.ctrl[0] = t_iter;
-}
-
-// sigma_bar (Eq 10, reading Q5) into an evaluation strategy buffer: S_num/S_den,
-// uniform where S_den = 0.  Chance part copied.
-template <class R, class I>
-__global__ void k_average(DG<R, I> g, R* out, long long H, long long Q, long long C) {
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < H; h += stride) {
-        const long long qb = (long long)g.qbase[h];
-        const int n = (int)((long long)g.qbase[h + 1] - qb);
-        const R den = g.sden[h];
-        for (int a = 0; a < n; ++a) out[qb + a] = (den > (R)0) ? g.snum[qb + a] / den : (R)1 / (R)n;
-    }
-    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < C; c += stride) out[Q + c] = g.sig[Q + c];
-}
-
-// Multi-GPU exchange 1: cut-level decision values.  Each row is
-// written by exactly one rank (others contribute zeros), so a sum-allreduce is exact.
-template <class R>
-__global__ void k_cut_pack(const R* __restrict__ U, const long long* __restrict__ rows,
-                           const unsigned char* __restrict__ owned, R* __restrict__ buf, long long n, int Pc) {
-    pdl_trigger();
-    pdl_wait();
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        for (int j = 0; j < Pc; ++j) buf[i * Pc + j] = owned[i] ? U[rows[i] * Pc + j] : (R)0;
-}
-template <class R>
-__global__ void k_cut_unpack(R* __restrict__ U, const long long* __restrict__ rows, const R* __restrict__ buf, long long n,
-                             int Pc) {
-    pdl_trigger();
-    pdl_wait();
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        for (int j = 0; j < Pc; ++j) U[rows[i] * Pc + j] = buf[i * Pc + j];
-}
-// Readback combination: zero the (h, a) entries this rank does not report.
-template <class R, class I>
-__global__ void k_mask_q(R* __restrict__ out, const I* __restrict__ qbase, const unsigned char* __restrict__ report,
-                         long long H) {
-    for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < H; h += (long long)gridDim.x * blockDim.x)
-        if (!report[h])
-            for (long long q = (long long)qbase[h]; q < (long long)qbase[h + 1]; ++q) out[q] = (R)0;
-}
-template <class R>
-__global__ void k_mask_h(R* __restrict__ out, const unsigned char* __restrict__ report, long long H) {
-    for (long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x; h < H; h += (long long)gridDim.x * blockDim.x)
-        if (!report[h]) out[h] = (R)0;
-}
 
 // --------------------------------------------------------------- host side
 #define CU(call)                                                                                   \
