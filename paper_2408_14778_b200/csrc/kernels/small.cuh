@@ -81,7 +81,7 @@ struct TinyLevel {
     long long h0, h1;   // internal infosets at depth l (consecutive)
 };
 struct TinyPlan {
-    long long U, reach, sig, reg, snum, sden, rt, pib;   // element offsets in shared memory (R units)
+    long long U, reach, sig, reg, snum, sden, rt, pib;   // element offsets in shared memory (R units); U < 0: U in global
     long long nU, nreach, nsig, Q, H;
     int bytes;
 };
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(1024) k_tiny(DG<R, I> g, const TinyLevel* __re
                                                 int D, long long T, TinyPlan tp) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R* const sm = reinterpret_cast<R*>(smem_raw);
-    R* const U = sm + tp.U;
+    R* const U = (tp.U >= 0) ? sm + tp.U : g.U;   // global: this CTA's stores are seen by its later loads
     R* const reach = sm + tp.reach;
     R* const sig = sm + tp.sig;
     R* const reg = sm + tp.reg;
@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(1024) k_tiny(DG<R, I> g, const TinyLevel* __re
     const int P = g.P;
     pdl_trigger();
     pdl_wait();
-    for (long long k = tid; k < tp.nU; k += nth) U[k] = g.U[k];
+    if (tp.U >= 0)
+        for (long long k = tid; k < tp.nU; k += nth) U[k] = g.U[k];
     for (long long k = tid; k < tp.nreach; k += nth) reach[k] = g.reach[k];
     for (long long k = tid; k < tp.nsig; k += nth) sig[k] = g.sig[k];
     for (long long k = tid; k < tp.Q; k += nth) {
@@ -218,7 +219,8 @@ __global__ void __launch_bounds__(1024) k_tiny(DG<R, I> g, const TinyLevel* __re
         }
     }
     // write the state back (readbacks and later launches read it from global)
-    for (long long k = tid; k < tp.nU; k += nth) g.U[k] = U[k];
+    if (tp.U >= 0)
+        for (long long k = tid; k < tp.nU; k += nth) g.U[k] = U[k];
     for (long long k = tid; k < tp.nreach; k += nth) g.reach[k] = reach[k];
     for (long long k = tid; k < tp.nsig; k += nth) g.sig[k] = sig[k];
     for (long long k = tid; k < tp.Q; k += nth) {

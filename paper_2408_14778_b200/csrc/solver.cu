@@ -997,26 +997,33 @@ struct Solver final : SolverBase {
         if (world > 1 || external || persist_ || (cfg.flags & CFR_FLAG_NO_TINY) || !g.depth_homogeneous || g.NS == 0)
             return CFR_OK;
         const long long nU = (long long)(plan_u_rows()) * g.Pc, nreach = 2LL * g.P * g.NS, nsig = g.Q + g.C;
-        TinyPlan tp{};
-        long long o = 0;
-        auto take = [&](long long n) { const long long r = o; o += (n + 1) & ~1LL; return r; };   // 16-byte aligned
-        tp.U = take(nU);
-        tp.reach = take(nreach);
-        tp.sig = take(nsig);
-        tp.reg = take(g.Q);
-        tp.snum = take(g.Q);
-        tp.sden = take(g.H);
-        tp.rt = take(g.Q);
-        tp.pib = take(g.H);
-        tp.nU = nU;
-        tp.nreach = nreach;
-        tp.nsig = nsig;
-        tp.Q = g.Q;
-        tp.H = g.H;
-        const long long bytes = o * (long long)sizeof(R);
         int dev = 0, optin = 0;
         CU(cudaGetDevice(&dev));
         CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        // everything in shared memory if it fits, else node values U stay in global
+        // memory (L1 / L2) and the rest is shared (e.g. Leduc in f64)
+        TinyPlan tp{};
+        long long bytes = 0;
+        for (int u_global = 0; u_global <= 1; ++u_global) {
+            tp = TinyPlan{};
+            long long o = 0;
+            auto take = [&](long long n) { const long long r = o; o += (n + 1) & ~1LL; return r; };   // 16-byte aligned
+            tp.U = u_global ? -1 : take(nU);
+            tp.reach = take(nreach);
+            tp.sig = take(nsig);
+            tp.reg = take(g.Q);
+            tp.snum = take(g.Q);
+            tp.sden = take(g.H);
+            tp.rt = take(g.Q);
+            tp.pib = take(g.H);
+            tp.nU = nU;
+            tp.nreach = nreach;
+            tp.nsig = nsig;
+            tp.Q = g.Q;
+            tp.H = g.H;
+            bytes = o * (long long)sizeof(R);
+            if (bytes <= optin - 1024) break;
+        }
         if (bytes > optin - 1024) return CFR_OK;
         tp.bytes = (int)bytes;
         // per level: slots and its (consecutive) infosets; members of each infoset
