@@ -4,8 +4,11 @@
  * The library runs whole counterfactual-regret-minimization iterations
  * (§3.2: regret matching, level-by-level forward reach pass,
  * level-by-level backward value pass, per-infoset aggregation, regret and
- * average-strategy accumulation) as hand-written sm_100a CUDA kernels captured
- * in a CUDA Graph.  Everything below is plain C: host or device pointers and
+ * average-strategy accumulation) as hand-written sm_100a CUDA kernels: per-level
+ * kernels captured in a CUDA Graph (big levels through the TMA-streamed backward
+ * kernel), or, for games whose state fits one CTA's shared memory, one
+ * single-CTA launch per enqueue.  Update rules: CFR, CFR+, linear CFR, DCFR and
+ * alternating-update CFR+ (cfr_variant).  Everything below is plain C: host or device pointers and
  * sizes, no C++ or torch types.  No exception ever crosses this boundary; every
  * call returns a cfr_status and, on failure, leaves a message in
  * cfr_last_error() (thread-local).  A handle is not thread-safe; distinct
