@@ -137,7 +137,9 @@ typedef struct {
                          /* deepest level's forward pass into its streaming       */
                          /* backward kernel (experimental); bit 7: disable the    */
                          /* shared-memory single-CTA kernel of tiny games         */
-                         /* (k_tiny, default when the state fits one CTA)         */
+                         /* (k_tiny, default when the state fits one CTA); bit 8: */
+                         /* 64-bit device indices even when 32 bits suffice       */
+                         /* (they are used automatically for >= 2^31 entries)     */
     int32_t reserved;
 } cfr_solver_config;
 
@@ -149,6 +151,7 @@ typedef struct {
 #define CFR_FLAG_FORCE_STREAM 32
 #define CFR_FLAG_FUSED_FORWARD 64
 #define CFR_FLAG_NO_TINY 128
+#define CFR_FLAG_INDEX64 256
 
 /* Multi-GPU level sharding.  NULL or world_size == 1 means a
  * single GPU.  nccl_unique_id points to the 128-byte ncclUniqueId that rank 0

@@ -39,6 +39,7 @@ FLAG_NO_STREAM = 16
 FLAG_FORCE_STREAM = 32
 FLAG_FUSED_FORWARD = 64
 FLAG_NO_TINY = 128
+FLAG_INDEX64 = 256
 
 
 def _ptr(a: np.ndarray) -> ctypes.c_void_p:

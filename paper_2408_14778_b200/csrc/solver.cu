@@ -1799,8 +1799,8 @@ static cfr_status view_for(cfr_game* G, const cfr_dist* dist, const Game** local
     return CFR_OK;
 }
 
-static size_t bytes_for(const Game& g, const ShardInfo* sh, int precision) {
-    const bool i32 = use_idx32(g);
+static size_t bytes_for(const Game& g, const ShardInfo* sh, int precision, int flags) {
+    const bool i32 = use_idx32(g) && !(flags & CFR_FLAG_INDEX64);
     if (precision == 64) return i32 ? Plan<double, int>(g, sh).total : Plan<double, long long>(g, sh).total;
     return i32 ? Plan<float, int>(g, sh).total : Plan<float, long long>(g, sh).total;
 }
@@ -1825,7 +1825,7 @@ cfr_status cfr_solver_workspace_bytes(const cfr_game* g, const cfr_solver_config
     std::shared_ptr<cfr_game::Shard> keep;
     cfr_status s = view_for(const_cast<cfr_game*>(g), dist, &local, &info, &keep);
     if (s) return s;
-    *bytes = bytes_for(*local, info, cfg->precision);
+    *bytes = bytes_for(*local, info, cfg->precision, cfg->flags);
     return CFR_OK;
 }
 
@@ -1840,13 +1840,13 @@ cfr_status cfr_solver_create(const cfr_game* g, const cfr_solver_config* cfg, vo
     std::shared_ptr<cfr_game::Shard> keep;
     cfr_status s = view_for(const_cast<cfr_game*>(g), dist, &local, &info, &keep);
     if (s) return s;
-    const size_t need = bytes_for(*local, info, cfg->precision);
+    const size_t need = bytes_for(*local, info, cfg->precision, cfg->flags);
     if (workspace_bytes < need) {
         cfrb_set_error("workspace too small: need " + std::to_string(need) + " bytes");
         return CFR_ERR_OOM;
     }
     if (((uintptr_t)workspace & 255) != 0) { cfrb_set_error("workspace must be 256-byte aligned"); return CFR_ERR_INVALID_ARG; }
-    const bool i32 = use_idx32(*local);
+    const bool i32 = use_idx32(*local) && !(cfg->flags & CFR_FLAG_INDEX64);
     std::unique_ptr<SolverBase> impl;
     cudaStream_t st = (cudaStream_t)stream;
     const void* nid = (dist && dist->world_size > 1) ? dist->nccl_unique_id : nullptr;

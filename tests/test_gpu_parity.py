@@ -121,3 +121,16 @@ def test_tiny_shared_memory_kernel_matches_per_level_launches(cuda, variant, pre
     assert used >= 4
     run_pair(gamegen.kuhn(2), variant, precision, 40)
     run_pair(gamegen.leduc(), variant, precision, 15)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_int64_index_kernels(cuda, precision):
+    """The 64-bit-index instantiations (used automatically for >= 2^31 nodes / pairs)
+    on small games: tile, streaming and tiny paths, against the oracle."""
+    import paper_2408_14778_b200 as pb
+    F = pb.FLAG_INDEX64
+    run_pair(gamegen.leduc(), 1, precision, 10, flags=F)
+    run_pair(gamegen.goofspiel(), 3, precision, 6, flags=F | pb.FLAG_FORCE_STREAM)
+    run_pair(gamegen.synthetic(n_types=2, seed=7), 1, precision, 2, flags=F | pb.FLAG_FORCE_STREAM, checks=("state",))
+    for seed in range(4):
+        run_pair(gamegen.random_game(seed, num_players=2 + seed % 3), 4, precision, 6, flags=F)
