@@ -1178,7 +1178,8 @@ struct Solver final : SolverBase {
     void deferred_update(cudaStream_t st, int last) {
         const long long n = dg.ndef;
         const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 8));
-        launch(pdl_, k_deferred<R, I>, dim3(blocks), dim3(256), 0, st, dg, last);
+        // no programmatic (PDL) edge when an NCCL all-reduce precedes it (sharded)
+        launch(pdl_ && world == 1, k_deferred<R, I>, dim3(blocks), dim3(256), 0, st, dg, last);
     }
 
     // ---- iteration phases.  One iteration = lower (forward + backward of the
