@@ -1732,7 +1732,6 @@ struct Solver final : SolverBase {
     cfr_status model_bytes(double* out) override {
         const Game& g = *gp;
         const double w = sizeof(R), ix = sizeof(I);
-        const int P = g.P;
         double fwd = 0, bwd = 0, upd = 0;
         for (int l = 1; l < g.D; ++l) fwd += level_fwd_bytes(l);
         int big = 0;
