@@ -6,6 +6,10 @@ size, so the checks are:
     kernels (k_bwd, FLAG_NO_STREAM: a separately written backward kernel) reach
     bit-identical state after T iterations -- the exact accumulation (reading
     Q8) makes the result independent of how members are grouped and summed;
+  * sampled outputs against the oracle: after one iteration, the regrets of
+    randomly drawn deepest-level infosets equal oracle/sampled.py (Eq 6/7 from
+    the definitions, pinned against the full oracle in test_oracle_pins.py)
+    within the north-star tolerance (1e-10 relative, f64);
   * properties that hold at any size: sigma and sigma_bar are distributions per
     infoset, CFR+ regrets are non-negative, the game is zero-sum so the two
     expected values cancel."""
@@ -17,15 +21,16 @@ import pytest
 import gamegen
 from gamegen.synthetic_tree import synthetic_counts
 import paper_2408_14778_b200 as pb
+from oracle.sampled import first_iteration_regrets, qbase
 
 pytestmark = pytest.mark.gpu
 
 T = 3
 
 
-def _run(game, flags):
+def _run(game, flags, iters=T):
     s = pb.Solver(game, variant="cfr+", precision=64, flags=flags)
-    s.run(T)
+    s.run(iters)
     out = dict(kernels=s.level_kernels(), avg=s.average_strategy(), cur=s.current_strategy(),
                ev=s.expected_values(), **s.state())
     del s
@@ -36,9 +41,23 @@ def _run(game, flags):
 def test_full_size_stream_vs_tile_and_invariants(cuda):
     desc = gamegen.synthetic(n_types=40, seed=0)
     game = pb.Game(desc)
-    del desc
     cnt = synthetic_counts(40)
     assert game.V == cnt["V"] and game.H == cnt["H"] and game.Q == cnt["Q"]
+
+    one = _run(game, 0, 1)
+    assert "k_bwd_stream" in one["kernels"], one["kernels"]
+    q = qbase(desc)
+    dec = np.flatnonzero(desc.player > 0)
+    rng = np.random.default_rng(2408)
+    hs = np.unique(desc.infoset[rng.choice(dec[-len(dec) // 10:], 8, replace=False)])
+    ref = first_iteration_regrets(desc, hs, plus=True)
+    for h in hs:
+        got = one["regret"][q[h]:q[h + 1]]
+        tol = 1e-10 * np.abs(ref[h]).max()
+        assert np.abs(ref[h]).max() > 0
+        assert np.all(np.abs(got - ref[h]) <= tol), (h, got, ref[h])
+    del desc, one, dec
+    gc.collect()
 
     a = _run(game, 0)
     assert "k_bwd_stream" in a["kernels"], a["kernels"]

@@ -427,3 +427,23 @@ def test_alternating_cfr_plus_converges_faster_on_kuhn():
     alt = oracle.Oracle(d).run(1000, 4).exploitability()["nash_conv"]
     sim = oracle.Oracle(d).run(1000, 1).exploitability()["nash_conv"]
     assert alt < sim and alt < 3e-3, (alt, sim)
+
+
+@pytest.mark.parametrize("n_types,seed", [(2, 1), (3, 4)])
+def test_sampled_first_iteration_regrets_match_full_oracle(n_types, seed):
+    """oracle/sampled.py (used at full size, where the full oracle cannot run) against
+    the full oracle: R^1 of every sampled deepest-level infoset, CFR and CFR+."""
+    from oracle.sampled import first_iteration_regrets, qbase
+    d = gamegen.synthetic(n_types=n_types, seed=seed)
+    q = qbase(d)
+    assert np.array_equal(q, oracle.Oracle(d).qbase)
+    dec = np.flatnonzero(d.player > 0)
+    rng = np.random.default_rng(seed)
+    hs = np.unique(d.infoset[rng.choice(dec[-len(dec) // 10:], 40, replace=False)])
+    for plus in (False, True):
+        reg = oracle.Oracle(d).run(1, int(plus)).state()["regret"]
+        res = first_iteration_regrets(d, hs, plus)
+        for h in hs:
+            ref = reg[q[h]:q[h + 1]]
+            assert np.allclose(res[h], ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max()), h
+            assert np.abs(ref).max() > 0
