@@ -28,8 +28,8 @@ pytestmark = pytest.mark.gpu
 T = 3
 
 
-def _run(game, flags, iters=T):
-    s = pb.Solver(game, variant="cfr+", precision=64, flags=flags)
+def _run(game, flags, iters=T, variant="cfr+"):
+    s = pb.Solver(game, variant=variant, precision=64, flags=flags)
     s.run(iters)
     out = dict(kernels=s.level_kernels(), avg=s.average_strategy(), cur=s.current_strategy(),
                ev=s.expected_values(), **s.state())
@@ -44,19 +44,23 @@ def test_full_size_stream_vs_tile_and_invariants(cuda):
     cnt = synthetic_counts(40)
     assert game.V == cnt["V"] and game.H == cnt["H"] and game.Q == cnt["Q"]
 
-    one = _run(game, 0, 1)
-    assert "k_bwd_stream" in one["kernels"], one["kernels"]
     q = qbase(desc)
     dec = np.flatnonzero(desc.player > 0)
     rng = np.random.default_rng(2408)
     hs = np.unique(desc.infoset[rng.choice(dec[-len(dec) // 10:], 8, replace=False)])
-    ref = first_iteration_regrets(desc, hs, plus=True)
-    for h in hs:
-        got = one["regret"][q[h]:q[h + 1]]
-        tol = 1e-10 * np.abs(ref[h]).max()
-        assert np.abs(ref[h]).max() > 0
-        assert np.all(np.abs(got - ref[h]) <= tol), (h, got, ref[h])
-    del desc, one, dec
+    for variant, plus in (("cfr+", True), ("cfr", False)):   # CFR: signed regrets
+        one = _run(game, 0, 1, variant)
+        assert "k_bwd_stream" in one["kernels"], one["kernels"]
+        ref = first_iteration_regrets(desc, hs, plus=plus)
+        for h in hs:
+            got = one["regret"][q[h]:q[h + 1]]
+            tol = 1e-10 * np.abs(ref[h]).max()
+            assert np.abs(ref[h]).max() > 0
+            assert np.all(np.abs(got - ref[h]) <= tol), (variant, h, got, ref[h])
+        if not plus:
+            assert any((ref[h] < 0).any() for h in hs)
+        del one
+    del desc, dec
     gc.collect()
 
     a = _run(game, 0)
