@@ -256,11 +256,14 @@ def signal_game() -> GameDesc:
 # ------------------------------------------------------------------- random games
 def random_game(seed: int, max_depth: int = 6, max_branching: int = 4, num_players: int = 2,
                 chance_fraction: float = 0.2, terminal_ramp: float = 0.6, pool: int = 2,
-                zero_sum: bool | None = None, max_nodes: int = 4000) -> GameDesc:
+                zero_sum: bool | None = None, max_nodes: int = 4000, span_depths: bool = False) -> GameDesc:
     """Seeded random perfect-recall game (SPEC S:128-162 idea): infosets pool
     same-depth nodes of one player with the same own (infoset, action) history and a
     random bucket in [0, pool); |A(h)| is a function of that history so pooled nodes
-    agree.  Payoffs uniform in [-1, 1] (zero-sum when P = 2 and zero_sum)."""
+    agree.  Payoffs uniform in [-1, 1] (zero-sum when P = 2 and zero_sum).
+    span_depths: the depth is left out of the pooling key, so one infoset may hold
+    nodes of several depths (still perfect recall: pooled nodes share the player's
+    own history, and a member's descendants always extend it)."""
     rng = np.random.default_rng(seed)
     P = num_players
     if zero_sum is None:
@@ -290,12 +293,13 @@ def random_game(seed: int, max_depth: int = 6, max_branching: int = 4, num_playe
                 gen(c, depth + 1, own)
             return
         pl = int(rng.integers(1, P + 1))
-        hkey = (pl, depth, own[pl])
+        dkey = -1 if span_depths else depth
+        hkey = (pl, dkey, own[pl])
         if hkey not in nact_of:
             nact_of[hkey] = int(rng.integers(1 if rng.random() < 0.1 else 2, max_branching + 1))
         k = nact_of[hkey]
         bucket = int(rng.integers(0, pool))
-        key = (depth, own[pl], bucket)
+        key = (dkey, own[pl], bucket)
         b.set_player(v, pl, key, k)
         h = b.infoset[v]
         for a in range(k):

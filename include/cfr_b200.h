@@ -201,11 +201,25 @@ cfr_status cfr_solver_get_state(cfr_solver* s, double* regret, double* s_num, do
  * average (Q10) or current strategy, computed on the device, [P]. */
 cfr_status cfr_solver_expected_values(cfr_solver* s, int32_t which, double* out /* [P] */);
 /* Best response to sigma_bar per player (ties to the lowest action), NashConv =
- * sum_i (BR_i - EV_i) and exploitability = NashConv / P (reading Q11), on the
- * device.  br may be NULL.  CFR_ERR_UNSUPPORTED if an infoset spans several
- * depths or does not fit one tile (reading Q17). */
+ * sum_i (BR_i - EV_i) and exploitability = NashConv / P (reading Q11, PAPER.md
+ * Fig 3 / P:557-560), on the device, for any perfect-recall game and any world
+ * size (sharded solvers need the NCCL id; external mode: cfr_solver_br_phase).
+ * Infosets whose members span tiles, depths or ranks are decided after a pass
+ * from exact global sums; the pass repeats until every such decision below is
+ * final (reading Q17; cfr_solver_br_passes).  br may be NULL. */
 cfr_status cfr_solver_exploitability(cfr_solver* s, double* nash_conv, double* exploitability,
                                      double* br /* [P] or NULL */);
+/* Exploitability curve (Fig 3): runs `iterations` iterations and, after
+ * every `every` of them, evaluates sigma_bar's EV and best responses on the
+ * device inside one CUDA graph, without a host synchronisation per evaluation.
+ * out (host, caller-owned) receives floor(iterations / every) rows of 2 + 2P
+ * doubles: T, NashConv, EV_1..EV_P, BR_1..BR_P; *rows = rows written.  The
+ * values equal cfr_solver_exploitability at the same T bit for bit. */
+cfr_status cfr_solver_run_tracked(cfr_solver* s, int64_t iterations, int64_t every, double* out,
+                                  int64_t* rows);
+/* Number of MODE_BR backward passes per player of one best response (1 when no
+ * infoset is deferred; D + 1 otherwise). */
+cfr_status cfr_solver_br_passes(cfr_solver* s, int32_t* passes);
 
 /* Instrumentation for bench.py: kernels launched per iteration, and the mean
  * per-kernel-class device time (CUDA events on the solver stream, ms) over
@@ -253,13 +267,21 @@ cfr_status cfr_nccl_unique_id(void* out /* 128 bytes */);
  * ("external" mode, used by the tests) the caller drives the phases and performs
  * the two sums itself; readbacks then return this rank's part (zeros for the
  * infosets another rank reports) and the caller sums them.
- * cfr_solver_exploitability is single-GPU only (CFR_ERR_UNSUPPORTED otherwise). */
+ * Best response in external mode: CFR_BR_SETUP once, then per player i and per
+ * pass (cfr_solver_br_passes): CFR_BR_LOWER, sum CFR_XCHG_CUT, CFR_BR_UPPER, sum
+ * CFR_XCHG_ACC, CFR_BR_DECIDE (out = root values [P] of that pass; the last
+ * pass's entry i is BR_i). */
 #define CFR_PHASE_LOWER 0     /* forward pass + backward of the owned depths (+ cut pack) */
 #define CFR_PHASE_UPPER 1     /* cut unpack + trunk backward                              */
 #define CFR_PHASE_UPDATE 2    /* deferred-infoset update; ends the iteration (T += 1)     */
 #define CFR_PHASE_EV_LOWER 3  /* sigma_bar + values pass of the owned depths (+ cut pack) */
 #define CFR_PHASE_EV_UPPER 4  /* cut unpack + trunk values pass; out = root values [P]    */
 cfr_status cfr_solver_phase(cfr_solver* s, int32_t phase, double* out /* [P] or NULL */);
+#define CFR_BR_SETUP 0        /* sigma_bar + its forward pass (reach of every level)      */
+#define CFR_BR_LOWER 1        /* best-response pass of the owned depths (+ cut pack)      */
+#define CFR_BR_UPPER 2        /* cut unpack + trunk best-response pass                    */
+#define CFR_BR_DECIDE 3       /* deferred infosets' argmax (k_br_decide); out = root [P]  */
+cfr_status cfr_solver_br_phase(cfr_solver* s, int32_t phase, int32_t player, double* out /* [P] or NULL */);
 #define CFR_XCHG_CUT 0
 #define CFR_XCHG_ACC 1
 cfr_status cfr_solver_exchange_size(cfr_solver* s, int32_t which, size_t* bytes);

@@ -158,11 +158,19 @@ class Solver:
         if dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
-        torch.cuda.set_device(dev)
-        self.workspace = torch.empty(self.workspace_bytes + 256, dtype=torch.uint8, device=dev)
+        with torch.cuda.device(dev):
+            self.stream = stream if stream is not None else torch.cuda.Stream(dev)
+            # The workspace comes from torch's caching allocator on the current
+            # stream; every kernel runs on self.stream.  Order the two: the solver
+            # stream waits for pending work on the allocating stream (a reused
+            # block may still be in use there), and the block is recorded as used
+            # by the solver stream so the allocator never hands it out while
+            # solver kernels may still write it.
+            self.workspace = torch.empty(self.workspace_bytes + 256, dtype=torch.uint8, device=dev)
+            self.stream.wait_stream(torch.cuda.current_stream(dev))
+            self.workspace.record_stream(self.stream)
         base = self.workspace.data_ptr()
         aligned = (base + 255) & ~255
-        self.stream = stream if stream is not None else torch.cuda.Stream(dev)
         h = ctypes.c_void_p()
         with torch.cuda.device(dev):
             _native.check(L.cfr_solver_create(game._h, ctypes.byref(self.cfg), ctypes.c_void_p(aligned),
@@ -174,7 +182,7 @@ class Solver:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            self._L.cfr_solver_destroy(h)
+            self._L.cfr_solver_destroy(h)   # synchronises the solver stream first
             self._h = None
 
     # -- iteration
@@ -221,6 +229,8 @@ class Solver:
         return dict(regret=r, snum=sn, sden=sd)
 
     def expected_values(self, which: str = "average") -> np.ndarray:
+        if which not in ("average", "current"):
+            raise ValueError(f"which must be 'average' or 'current', not {which!r}")
         out = np.zeros(self.P)
         w = 0 if which == "average" else 1
         _native.check(self._L.cfr_solver_expected_values(self._h, w, _ptr(out)))
@@ -231,6 +241,25 @@ class Solver:
         br = np.zeros(self.P)
         _native.check(self._L.cfr_solver_exploitability(self._h, ctypes.byref(nc), ctypes.byref(ex), _ptr(br)))
         return dict(nash_conv=nc.value, exploitability=ex.value, br=br)
+
+    def run_tracked(self, iterations: int, every: int) -> dict:
+        """PAPER.md Fig 3 curve: run `iterations` iterations and evaluate NashConv of
+        sigma_bar on the device every `every` of them (one CUDA graph per
+        evaluation, no host sync in between).  Returns arrays T, nash_conv, ev [.., P],
+        br [.., P]."""
+        rows_cap = max(1, int(iterations) // int(every))
+        out = np.zeros((rows_cap, 2 + 2 * self.P))
+        rows = ctypes.c_int64()
+        _native.check(self._L.cfr_solver_run_tracked(self._h, int(iterations), int(every), _ptr(out),
+                                                     ctypes.byref(rows)))
+        out = out[:rows.value]
+        return dict(T=out[:, 0].astype(np.int64), nash_conv=out[:, 1], ev=out[:, 2:2 + self.P],
+                    br=out[:, 2 + self.P:])
+
+    def br_passes(self) -> int:
+        n = ctypes.c_int32()
+        _native.check(self._L.cfr_solver_br_passes(self._h, ctypes.byref(n)))
+        return int(n.value)
 
     # -- instrumentation
     def launches_per_iteration(self) -> int:
@@ -245,11 +274,17 @@ class Solver:
 
     # -- multi-GPU (external mode drives the phases; see include/cfr_b200.h)
     PHASE_LOWER, PHASE_UPPER, PHASE_UPDATE, PHASE_EV_LOWER, PHASE_EV_UPPER = 0, 1, 2, 3, 4
+    BR_SETUP, BR_LOWER, BR_UPPER, BR_DECIDE = 0, 1, 2, 3
     XCHG_CUT, XCHG_ACC = 0, 1
 
     def phase(self, ph: int):
         out = np.zeros(self.P)
         _native.check(self._L.cfr_solver_phase(self._h, int(ph), _ptr(out)))
+        return out
+
+    def br_phase(self, ph: int, player: int = 1):
+        out = np.zeros(self.P)
+        _native.check(self._L.cfr_solver_br_phase(self._h, int(ph), int(player), _ptr(out)))
         return out
 
     def exchange_get(self, which: int) -> np.ndarray:
@@ -274,28 +309,31 @@ class Solver:
 
     def level_kernels(self) -> list:
         """Backward kernel of each parent level (include/cfr_b200.h cfr_solver_level_kernels)."""
-        out = np.zeros(64, dtype=np.int32)
+        D = max(1, self.game.D)
+        out = np.zeros(D, dtype=np.int32)
         nl = ctypes.c_int32()
-        _native.check(self._L.cfr_solver_level_kernels(self._h, _ptr(out), 64, ctypes.byref(nl)))
-        return [self.KERNEL_NAMES[int(x)] for x in out[:min(nl.value, 64)]]
+        _native.check(self._L.cfr_solver_level_kernels(self._h, _ptr(out), D, ctypes.byref(nl)))
+        return [self.KERNEL_NAMES[int(x)] for x in out[:min(nl.value, D)]]
 
     def counters(self) -> dict:
         """Cumulative streaming-level work counters (include/cfr_b200.h cfr_solver_counters),
         summed over levels, plus the per-level table."""
-        out = np.zeros(4 * 64, dtype=np.int64)
+        D = max(1, self.game.D)
+        out = np.zeros(4 * D, dtype=np.int64)
         nl = ctypes.c_int32()
-        _native.check(self._L.cfr_solver_counters(self._h, _ptr(out), 64, ctypes.byref(nl)))
-        per = out[:4 * min(nl.value, 64)].reshape(-1, 4)
+        _native.check(self._L.cfr_solver_counters(self._h, _ptr(out), D, ctypes.byref(nl)))
+        per = out[:4 * min(nl.value, D)].reshape(-1, 4)
         tot = per.sum(0)
         return dict(live_infosets=int(tot[0]), live_pairs=int(tot[1]), infosets=int(tot[2]), pairs=int(tot[3]),
                     per_level=per.tolist())
 
     def level_profile(self) -> list:
         """Per level of the last profile(): forward / backward ms and model bytes."""
-        out = np.zeros(4 * 64)
+        D = max(1, self.game.D)
+        out = np.zeros(4 * D)
         nl = ctypes.c_int32()
-        _native.check(self._L.cfr_solver_level_profile(self._h, _ptr(out), 64, ctypes.byref(nl)))
-        per = out[:4 * min(nl.value, 64)].reshape(-1, 4)
+        _native.check(self._L.cfr_solver_level_profile(self._h, _ptr(out), D, ctypes.byref(nl)))
+        per = out[:4 * min(nl.value, D)].reshape(-1, 4)
         kern = self.level_kernels()
         return [dict(level=L, fwd_ms=float(r[0]), bwd_ms=float(r[1]), fwd_bytes=float(r[2]), bwd_bytes=float(r[3]),
                      bwd_kernel=kern[L] if L < len(kern) else None) for L, r in enumerate(per)]

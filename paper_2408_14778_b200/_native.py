@@ -132,6 +132,9 @@ SIGNATURES = {
     "cfr_solver_level_profile": (ctypes.c_int, [_P, _P, _I32, _P]),
     "cfr_nccl_unique_id": (ctypes.c_int, [_P]),
     "cfr_solver_phase": (ctypes.c_int, [_P, _I32, _P]),
+    "cfr_solver_br_phase": (ctypes.c_int, [_P, _I32, _I32, _P]),
+    "cfr_solver_br_passes": (ctypes.c_int, [_P, _P]),
+    "cfr_solver_run_tracked": (ctypes.c_int, [_P, _I64, _I64, _P, _P]),
     "cfr_solver_exchange_size": (ctypes.c_int, [_P, _I32, _P]),
     "cfr_solver_exchange": (ctypes.c_int, [_P, _I32, _I32, _P, ctypes.c_size_t]),
     "cfr_solver_shard_info": (ctypes.c_int, [_P, _P]),

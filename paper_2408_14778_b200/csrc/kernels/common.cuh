@@ -56,6 +56,7 @@ struct DG {
     const TileD* tiles;
     const SegD* segs;
     const I* deferred;            // [ndef]
+    int* br_best;                 // [ndef] best-response action of each deferred infoset (MODE_BR passes)
     long long* ctrl;              // [0] iterations done, [1] first bad iteration, [2] done counter
     unsigned long long* lcnt;     // [D][4] streaming-level work counters (updated / visited infosets, pairs)
     long long ndef;

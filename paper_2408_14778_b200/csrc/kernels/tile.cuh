@@ -291,7 +291,7 @@ __device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict_
             c2 += __shfl_xor_sync(0xffffffffu, c2, o);
         }
         if (active && part == 0) {
-            const bool keep = (MODE == MODE_BR) || sm.seg[k].fused;
+            const bool keep = sm.seg[k].fused;
             if (keep) {
                 const double x = is_pair ? xdec(c0, c1, c2, g.rc) : xdec(c0, c1, c2, g.rcp);
                 if (rd == 0) kr0 = x;
@@ -299,7 +299,10 @@ __device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict_
                 else if (rd == 2) kr2 = x;
                 else if (rd == 3) kr3 = x;
                 else kr4 = x;
-            } else if (MODE == MODE_CFR && T.contrib) {
+            } else if (T.contrib) {
+                // deferred infoset (spans tiles, depths or ranks): exact partial sums
+                // into its global slices (CFR: r~ and pi_bar; BR: the best-response
+                // sums of the BR player's infosets, decided by k_br_decide)
                 if (is_pair) {
                     const long long q = sm.seg[k].dq + a;
                     atomicAdd(&g.acc_r[q * 3 + 0], (unsigned long long)(long long)c0);
@@ -330,9 +333,16 @@ __device__ __forceinline__ void bwd_tile(const DG<R, I>& g, const R* __restrict_
 
     if (MODE == MODE_BR) {
         // argmax per segment (ties to the lowest action); for u2 = -u1 storage the
-        // stored sums are negated, so player 2 takes the argmin.
+        // stored sums are negated, so player 2 takes the argmin.  A deferred
+        // infoset (not complete in this tile) takes the action k_br_decide chose
+        // after the previous pass (reading Q17: the BR passes repeat until every
+        // deferred decision below is final; see Solver::best_response).
         for (int k = tid; k < nseg; k += nth) {
             if (sm.seg[k].owner != br_player) continue;
+            if (!sm.seg[k].fused) {
+                sm.best[k] = g.br_best[sm.seg[k].dh];
+                continue;
+            }
             const int n = sm.seg[k].n;
             const bool neg = (PC == 1) && (br_player == 2);
             int best = 0;

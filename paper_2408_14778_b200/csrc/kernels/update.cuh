@@ -78,6 +78,58 @@ __global__ void __launch_bounds__(256) k_deferred(DG<R, I> g, int last) {
 }
 
 
+// Best response (reading Q11 / Q17): after a MODE_BR backward pass, every
+// deferred infoset of the BR player (spanning tiles, depths or ranks) decodes its
+// exact sums sum_{d in h} pi_check(d, i) V(child(d, a)) and takes the argmax
+// (ties to the lowest action; with u2 = -u1 storage player 2 takes the argmin of
+// the stored sums), compared in the working precision like the in-tile argmax.
+// The accumulators of every deferred infoset are zeroed for the next pass.
+template <class R, class I>
+__global__ void __launch_bounds__(256) k_br_decide(DG<R, I> g, int br_player, int neg) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < g.ndef; idx += stride) {
+        const long long h = (long long)g.deferred[idx];
+        const long long qb = (long long)g.qbase[h];
+        const int n = (int)((long long)g.qbase[h + 1] - qb);
+        const long long dq = g.dqbase[idx];
+        const bool mine = g.owner[h] == br_player;
+        int best = 0;
+        R bv = (R)0;
+        for (int a = 0; a < n; ++a) {
+            const long long cq = dq + a;
+            const long long c0 = (long long)g.acc_r[cq * 3 + 0], c1 = (long long)g.acc_r[cq * 3 + 1],
+                            c2 = (long long)g.acc_r[cq * 3 + 2];
+            g.acc_r[cq * 3 + 0] = 0;
+            g.acc_r[cq * 3 + 1] = 0;
+            g.acc_r[cq * 3 + 2] = 0;
+            const R x = (R)xdec_ll(c0, c1, c2, g.rc);
+            if (a == 0 || (neg ? (x < bv) : (x > bv))) {
+                bv = x;
+                best = a;
+            }
+        }
+        if (mine) g.br_best[idx] = best;
+    }
+}
+
+// Root row of U (values of the last backward pass) into slot `slot` of the
+// exploitability record `rec` (in-graph exploitability, cfr_solver_run_tracked):
+// rec[row * width + slot + j] = U[j], row = ctrl[4]; `advance` closes the row
+// (writes the iteration count into its last entry and moves to the next row).
+template <class R>
+__global__ void k_root_store(const R* __restrict__ U, double* __restrict__ rec, long long* ctrl, int Pc, int slot,
+                             int width, int advance, long long cap) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const long long row = ctrl[4];
+        if (row < cap) {
+            double* r = rec + row * width;
+            for (int j = 0; j < Pc; ++j) r[slot + j] = (double)U[j];
+            if (advance) r[width - 1] = (double)ctrl[0];
+        }
+        if (advance) ctrl[4] = row + 1;
+    }
+}
+
 // sigma_bar (Eq 10, reading Q5) into an evaluation strategy buffer: S_num/S_den,
 // uniform where S_den = 0.  Chance part copied.
 template <class R, class I>

@@ -91,6 +91,9 @@ struct SolverBase {
     virtual cfr_status exchange_size(int which, size_t* bytes) = 0;
     virtual cfr_status exchange(int which, int put, void* host, size_t bytes) = 0;
     virtual cfr_status shard_info(int64_t* out) = 0;
+    virtual cfr_status br_phase(int ph, int player, double* out) = 0;
+    virtual cfr_status br_passes_out(int32_t* n) = 0;
+    virtual cfr_status run_tracked(int64_t iters, int64_t every, double* out, int64_t* rows) = 0;
 };
 
 struct Layout {
@@ -404,12 +407,18 @@ static size_t fast_pool_bytes(const Game& g, const ShardInfo* sh) {
     return pool;
 }
 
+// In-graph exploitability record (cfr_solver_run_tracked): per evaluation one
+// row of root values -- EV (Pc columns), then each player's best-response root
+// row (Pc columns each), then the iteration count.
+constexpr int kRecRows = 1024;
+static int rec_width(const Game& g) { return g.Pc + g.P * g.Pc + 1; }
+
 template <class R, class I>
 struct Plan {
     size_t U, reach, sig, sig_eval, regret, snum, sden, acc_r, acc_p, dqbase;
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
-    size_t qbase, owner, tiles, segs, deferred, ctrl, lcnt, out;
+    size_t qbase, owner, tiles, segs, deferred, br_best, ctrl, lcnt, out, rec;
     size_t cutbuf, cutrow, cutown, report, pool, spool, plev, gbar, tlev, tmem_of;
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
@@ -441,6 +450,7 @@ struct Plan {
         tiles = L.take<TileD>(g.tiles.size());
         segs = L.take<SegD>(g.segs.size());
         deferred = L.take<I>(g.deferred_list.size());
+        br_best = L.take<int>(g.deferred_list.size() + 1);
         ctrl = L.take<long long>(8);
         lcnt = L.take<unsigned long long>(4 * (size_t)g.D + 4);
         out = L.take<R>(std::max<size_t>(Q + C, (size_t)g.P * 2 + 8));
@@ -455,6 +465,7 @@ struct Plan {
         gbar = L.take<unsigned>(4);
         tlev = L.take<TinyLevel>((size_t)g.D + 1);
         tmem_of = L.take<I>(g.V <= (int64_t(1) << 20) ? 2 * H + 2 : 2);
+        rec = L.take<double>((size_t)kRecRows * rec_width(g));
         total = L.off + 256;
     }
 };
@@ -501,8 +512,12 @@ struct Solver final : SolverBase {
     }
 
     ~Solver() override {
+        // the workspace belongs to the caller: no kernel may still run on it once
+        // the handle is gone (the caller frees it after cfr_solver_destroy)
+        cudaStreamSynchronize(stream);
         if (pinned_) cudaFreeHost(pinned_);
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (eval_exec_) cudaGraphExecDestroy(eval_exec_);
         if (cap_stream) cudaStreamDestroy(cap_stream);
         if (comm) ncclCommDestroy(comm);
     }
@@ -651,6 +666,7 @@ struct Solver final : SolverBase {
         dg.tiles = at<TileD>(plan.tiles);
         dg.segs = at<SegD>(plan.segs);
         dg.deferred = at<I>(plan.deferred);
+        dg.br_best = at<int>(plan.br_best);
         dg.ctrl = at<long long>(plan.ctrl);
         dg.lcnt = at<unsigned long long>(plan.lcnt);
         dg.ndef = (long long)g.deferred_list.size();
@@ -840,6 +856,7 @@ struct Solver final : SolverBase {
         CU(cudaMemsetAsync(ws + plan.snum, 0, g.Q * sizeof(R), stream));
         CU(cudaMemsetAsync(ws + plan.sden, 0, g.H * sizeof(R), stream));
         CU(cudaMemsetAsync(ws + plan.acc_r, 0, acc_bytes(), stream));
+        CU(cudaMemsetAsync(ws + plan.br_best, 0, (g.deferred_list.size() + 1) * sizeof(int), stream));
         CU(cudaMemsetAsync(ws + plan.lcnt, 0, (4 * (size_t)g.D + 4) * sizeof(unsigned long long), stream));
         CU(cudaMemsetAsync(ws + plan.reach, 0, 2 * (size_t)g.P * g.ND * sizeof(R), stream));
         {
@@ -1204,7 +1221,9 @@ struct Solver final : SolverBase {
     // forward level l runs inside the streaming backward kernel of level l
     bool fwd_fused(int l) const { return use_stream_ && l < (int)stream_.size() && stream_[l].ntiles > 0 && stream_[l].fused; }
 
-    void launch_lower(cudaStream_t st, int mode, const R* sig, std::vector<Mark>* ev) {
+    // mode MODE_CFR (forward + backward), MODE_VALUES (values under sig) or
+    // MODE_BR (best-response values of player br_player; reach of sig computed before)
+    void launch_lower(cudaStream_t st, int mode, const R* sig, std::vector<Mark>* ev, int br_player = 0) {
         const Game& g = *gp;
         if (mode == MODE_CFR)
             for (int l = 1; l < g.D; ++l) {
@@ -1216,7 +1235,8 @@ struct Solver final : SolverBase {
         for (int L = g.D - 1; L >= stop; --L) {
             const int last = (mode == MODE_CFR && L == 0 && !has_def() && pass_final_) ? 1 : 0;
             if (mode == MODE_CFR) bwd_level<MODE_CFR>(st, sig, L, 0, last);
-            else bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
+            else if (mode == MODE_VALUES) bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
+            else bwd_level<MODE_BR>(st, sig, L, br_player, 0);
             mark(st, ev, 1, L);
         }
         if (sharded()) {
@@ -1226,7 +1246,7 @@ struct Solver final : SolverBase {
                                               at<R>(plan.cutbuf), n, g.Pc);
         }
     }
-    void launch_upper(cudaStream_t st, int mode, const R* sig, std::vector<Mark>* ev) {
+    void launch_upper(cudaStream_t st, int mode, const R* sig, std::vector<Mark>* ev, int br_player = 0) {
         const Game& g = *gp;
         if (!sharded()) return;
         const long long n = ncut();
@@ -1235,7 +1255,8 @@ struct Solver final : SolverBase {
         for (int L = sh->cut - 1; L >= 0; --L) {
             const int last = (mode == MODE_CFR && L == 0 && !has_def() && pass_final_) ? 1 : 0;
             if (mode == MODE_CFR) bwd_level<MODE_CFR>(st, sig, L, 0, last);
-            else bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
+            else if (mode == MODE_VALUES) bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
+            else bwd_level<MODE_BR>(st, sig, L, br_player, 0);
             mark(st, ev, 1, L);
         }
     }
@@ -1386,11 +1407,11 @@ struct Solver final : SolverBase {
         return CFR_OK;
     }
 
-    cfr_status compute_average() {
+    cfr_status compute_average(cudaStream_t st = nullptr) {
         const Game& g = *gp;
         const long long n = std::max<long long>(g.H, g.C);
         const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 8));
-        k_average<R, I><<<blocks, 256, 0, stream>>>(dg, at<R>(plan.sig_eval), g.H, g.Q, g.C);
+        k_average<R, I><<<blocks, 256, 0, st ? st : stream>>>(dg, at<R>(plan.sig_eval), g.H, g.Q, g.C);
         CU(cudaGetLastError());
         return CFR_OK;
     }
@@ -1464,42 +1485,248 @@ struct Solver final : SolverBase {
         return root_values(sig, out);
     }
 
+    // ---- best response (reading Q11 / Q17) ------------------------------------
+    // BR_i under sig: MODE_BR backward passes (+ the cut exchange when sharded).
+    // Infosets complete in one tile decide in-tile, bottom-up, in the same pass.
+    // A deferred infoset (its members span tiles, depths or ranks) sums its
+    // exact BR terms globally; k_br_decide (after the int64 exchange when
+    // sharded) sets its action, which its members use from the next pass on.
+    // Under perfect recall the deferred infosets below a member of h have
+    // strictly longer own-action sequences than h, so after pass k every
+    // deferred infoset whose chain of deferred infosets below is shorter than k
+    // has its final action; sequences are at most D long, so D passes decide all
+    // and one more pass leaves BR_i at the root (1 pass without deferred infosets).
+    int br_passes() const { return (world > 1 || has_def()) ? full->D + 1 : 1; }
+    cfr_status br_decide(cudaStream_t st, int i) {
+        const long long n = dg.ndef;
+        if (n == 0) return CFR_OK;
+        if (world > 1) {
+            cfr_status s = nccl_sum(st, dg.acc_r, acc_bytes() / 8, ncclInt64);
+            if (s) return s;
+        }
+        const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 8));
+        k_br_decide<R, I><<<blocks, 256, 0, st>>>(dg, i, (gp->Pc == 1 && i == 2) ? 1 : 0);
+        CU(cudaGetLastError());
+        return CFR_OK;
+    }
+    cfr_status br_pass(cudaStream_t st, const R* sig, int i) {
+        const Game& g = *gp;
+        launch_lower(st, MODE_BR, sig, nullptr, i);
+        if (sharded()) {
+            cfr_status s = nccl_sum(st, at<R>(plan.cutbuf), (size_t)ncut() * g.Pc, rtype());
+            if (s) return s;
+            launch_upper(st, MODE_BR, sig, nullptr, i);
+        }
+        return br_decide(st, i);
+    }
+    // sigma_bar into sig_eval and its forward pass (reach of every level)
+    cfr_status eval_setup(cudaStream_t st) {
+        const Game& g = *gp;
+        cfr_status s = compute_average(st);
+        if (s) return s;
+        const R* sig = at<R>(plan.sig_eval);
+        for (int l = 1; l < g.D; ++l) fwd_level(st, sig, l);
+        CU(cudaGetLastError());
+        return CFR_OK;
+    }
+    // root row -> per-player values (u2 = -u1 storage for two-player zero-sum)
+    void root_to_players(const R* r, double* out) const {
+        const Game& g = *gp;
+        if (g.zero_sum_2p) {
+            out[0] = (double)r[0];
+            out[1] = (double)(-r[0]);
+        } else {
+            for (int j = 0; j < g.P; ++j) out[j] = (double)r[j];
+        }
+    }
+
     cfr_status exploitability(double* nc, double* ex, double* br) override {
         const Game& g = *gp;
-        if (world > 1) {
-            cfrb_set_error("device best response is single-GPU in this version (DESIGN.md §9)");
-            return CFR_ERR_UNSUPPORTED;
-        }
-        if (!g.depth_homogeneous || !g.deferred_list.empty()) {
-            cfrb_set_error("device best response needs every infoset on one depth and inside one tile (reading Q17)");
+        if (external) {
+            cfrb_set_error("world_size > 1 without an NCCL id: drive the best response with cfr_solver_br_phase");
             return CFR_ERR_UNSUPPORTED;
         }
         CU(cudaStreamSynchronize(stream));
-        cfr_status s = compute_average();
-        if (s) return s;
-        const R* sig = at<R>(plan.sig_eval);
+        cfr_status s;
         double ev[16];
-        if ((s = root_values(sig, ev))) return s;
-        // forward pass under sigma_bar: pi_check(., i) for every player
-        for (int l = 1; l < g.D; ++l) fwd_level(stream, sig, l);
+        {
+            if ((s = compute_average())) return s;
+            if ((s = root_values(at<R>(plan.sig_eval), ev))) return s;
+        }
+        if ((s = eval_setup(stream))) return s;
+        const R* sig = at<R>(plan.sig_eval);
         double total = 0.0;
+        const int passes = br_passes();
         for (int i = 1; i <= g.P; ++i) {
-            for (int L = g.D - 1; L >= 0; --L) bwd_level<MODE_BR>(stream, sig, L, i, 0);
-            CU(cudaGetLastError());
+            for (int k = 0; k < passes; ++k)
+                if ((s = br_pass(stream, sig, i))) return s;
             std::vector<R> r(g.Pc);
             CU(cudaMemcpyAsync(r.data(), dg.U, g.Pc * sizeof(R), cudaMemcpyDeviceToHost, stream));
             CU(cudaStreamSynchronize(stream));
-            double b;
-            if (g.zero_sum_2p) b = (i == 1) ? (double)r[0] : (double)(-r[0]);
-            else b = (double)r[i - 1];
+            double v[16];
+            root_to_players(r.data(), v);
+            const double b = v[i - 1];
             if (br) br[i - 1] = b;
             total = total + (b - ev[i - 1]);
         }
-        // restore the reach arrays of the current strategy is unnecessary: every
-        // iteration recomputes them.  Root reach stays 1.
+        // the reach arrays of the current strategy need no restoring: every
+        // iteration recomputes them (root reach stays 1)
         *nc = total;
         *ex = total / (double)g.P;
         return CFR_OK;
+    }
+
+    // externally driven sharded best response (tests; world > 1 without NCCL):
+    // 0 setup (sigma_bar + its forward pass), 1 lower pass, 2 upper pass (caller
+    // exchanged the cut values), 3 decide (caller exchanged the int64 sums; `out`
+    // receives the root values of this pass)
+    cfr_status br_phase(int ph, int i, double* out) override {
+        const Game& g = *gp;
+        if (i < 1 || i > g.P) {
+            cfrb_set_error("bad best-response player");
+            return CFR_ERR_INVALID_ARG;
+        }
+        const R* sig = at<R>(plan.sig_eval);
+        cfr_status s = CFR_OK;
+        switch (ph) {
+            case 0: s = eval_setup(stream); break;
+            case 1: launch_lower(stream, MODE_BR, sig, nullptr, i); break;
+            case 2: launch_upper(stream, MODE_BR, sig, nullptr, i); break;
+            case 3: {
+                if (dg.ndef > 0) {
+                    const unsigned blocks = (unsigned)std::max<long long>(
+                        1, std::min<long long>((dg.ndef + 255) / 256, 148LL * 8));
+                    k_br_decide<R, I><<<blocks, 256, 0, stream>>>(dg, i, (g.Pc == 1 && i == 2) ? 1 : 0);
+                }
+                if (out) {
+                    CU(cudaGetLastError());
+                    std::vector<R> r(g.Pc);
+                    CU(cudaMemcpyAsync(r.data(), dg.U, g.Pc * sizeof(R), cudaMemcpyDeviceToHost, stream));
+                    CU(cudaStreamSynchronize(stream));
+                    root_to_players(r.data(), out);
+                }
+                break;
+            }
+            default:
+                cfrb_set_error("bad best-response phase");
+                return CFR_ERR_INVALID_ARG;
+        }
+        if (s) return s;
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(stream));
+        return CFR_OK;
+    }
+    cfr_status br_passes_out(int32_t* n) override {
+        *n = br_passes();
+        return CFR_OK;
+    }
+
+    // ---- in-graph exploitability (Fig 3) -------------------
+    // One evaluation = sigma_bar, its forward pass, the values pass (EV) and every
+    // player's best-response passes, each root row stored on the device into the
+    // record (k_root_store): captured once as a CUDA graph and replayed every
+    // `every` iterations with no host synchronisation; rows are read back when
+    // the record fills up and at the end.
+    cudaGraphExec_t eval_exec_ = nullptr;
+    cfr_status eval_enqueue(cudaStream_t st) {
+        const Game& g = *gp;
+        const int width = rec_width(g);
+        double* rec = at<double>(plan.rec);
+        const R* sig = at<R>(plan.sig_eval);
+        cfr_status s;
+        if ((s = compute_average(st))) return s;
+        launch_lower(st, MODE_VALUES, sig, nullptr);
+        if (sharded()) {
+            if ((s = nccl_sum(st, at<R>(plan.cutbuf), (size_t)ncut() * g.Pc, rtype()))) return s;
+            launch_upper(st, MODE_VALUES, sig, nullptr);
+        }
+        k_root_store<R><<<1, 32, 0, st>>>(dg.U, rec, dg.ctrl, g.Pc, 0, width, 0, kRecRows);
+        for (int l = 1; l < g.D; ++l) fwd_level(st, sig, l);
+        const int passes = br_passes();
+        for (int i = 1; i <= g.P; ++i) {
+            for (int k = 0; k < passes; ++k)
+                if ((s = br_pass(st, sig, i))) return s;
+            k_root_store<R><<<1, 32, 0, st>>>(dg.U, rec, dg.ctrl, g.Pc, g.Pc * i, width, i == g.P ? 1 : 0, kRecRows);
+        }
+        CU(cudaGetLastError());
+        return CFR_OK;
+    }
+    cfr_status flush_record(int64_t rows, double* out, int64_t* written) {
+        const Game& g = *gp;
+        const int width = rec_width(g);
+        std::vector<double> buf((size_t)rows * width);
+        CU(cudaStreamSynchronize(stream));
+        if (rows) CU(cudaMemcpy(buf.data(), at<double>(plan.rec), buf.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        long long zero = 0;
+        CU(cudaMemcpy(dg.ctrl + 4, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+        const int ow = 2 + 2 * g.P;   // out row: T, NashConv, EV_1..P, BR_1..P
+        for (int64_t r = 0; r < rows; ++r) {
+            const double* row = buf.data() + (size_t)r * width;
+            double* o = out + (size_t)(*written + r) * ow;
+            std::vector<R> tmp(g.Pc);
+            for (int j = 0; j < g.Pc; ++j) tmp[j] = (R)row[j];
+            root_to_players(tmp.data(), o + 2);
+            double nc = 0.0;
+            for (int i = 1; i <= g.P; ++i) {
+                for (int j = 0; j < g.Pc; ++j) tmp[j] = (R)row[g.Pc * i + j];
+                double v[16];
+                root_to_players(tmp.data(), v);
+                o[2 + g.P + (i - 1)] = v[i - 1];
+                nc = nc + (v[i - 1] - o[2 + (i - 1)]);
+            }
+            o[0] = row[width - 1];
+            o[1] = nc;
+        }
+        *written += rows;
+        return CFR_OK;
+    }
+    cfr_status run_tracked(int64_t iters, int64_t every, double* out, int64_t* rows_out) override {
+        if (external) {
+            cfrb_set_error("world_size > 1 without an NCCL id: tracked runs need the in-graph exchanges");
+            return CFR_ERR_UNSUPPORTED;
+        }
+        if (every <= 0 || iters < 0) {
+            cfrb_set_error("run_tracked: every must be > 0 and iterations >= 0");
+            return CFR_ERR_INVALID_ARG;
+        }
+        CU(cudaStreamSynchronize(stream));
+        if (!eval_exec_ && use_graph) {
+            cudaStream_t cs = cap_stream;
+            if (!cs) CU(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+            cudaGraph_t graph;
+            CU(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+            cfr_status ls = eval_enqueue(cap_stream);
+            cudaError_t ce = cudaStreamEndCapture(cap_stream, &graph);
+            if (ls != CFR_OK) return ls;
+            if (ce != cudaSuccess) {
+                cfrb_set_error(std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
+                return CFR_ERR_CUDA;
+            }
+            CU(cudaGraphInstantiate(&eval_exec_, graph, 0));
+            cudaGraphDestroy(graph);
+        }
+        long long zero = 0;
+        CU(cudaMemcpy(dg.ctrl + 4, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+        int64_t written = 0, pending = 0;
+        for (int64_t done = 0; done + every <= iters; done += every) {
+            cfr_status s = enqueue(every);
+            if (s) return s;
+            if (eval_exec_) CU(cudaGraphLaunch(eval_exec_, stream));
+            else if ((s = eval_enqueue(stream))) return s;
+            if (++pending == kRecRows) {
+                if ((s = flush_record(pending, out, &written))) return s;
+                pending = 0;
+            }
+        }
+        const int64_t tail = iters % every;
+        if (tail) {
+            cfr_status s = enqueue(tail);
+            if (s) return s;
+        }
+        cfr_status s = flush_record(pending, out, &written);
+        if (s) return s;
+        *rows_out = written;
+        return sync();
     }
 
     cfr_status launches(int64_t* n) override {
@@ -1978,6 +2205,20 @@ cfr_status cfr_game_shard_info(const cfr_game* g, int32_t rank, int32_t world, i
 cfr_status cfr_solver_phase(cfr_solver* s, int32_t phase, double* out) {
     CHK_S(s);
     return s->impl->phase(phase, out);
+}
+cfr_status cfr_solver_br_phase(cfr_solver* s, int32_t phase, int32_t player, double* out) {
+    CHK_S(s);
+    return s->impl->br_phase(phase, player, out);
+}
+cfr_status cfr_solver_br_passes(cfr_solver* s, int32_t* passes) {
+    CHK_S(s);
+    if (!passes) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->br_passes_out(passes);
+}
+cfr_status cfr_solver_run_tracked(cfr_solver* s, int64_t iterations, int64_t every, double* out, int64_t* rows) {
+    CHK_S(s);
+    if (!out || !rows) { cfrb_set_error("NULL out"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->run_tracked(iterations, every, out, rows);
 }
 cfr_status cfr_solver_exchange_size(cfr_solver* s, int32_t which, size_t* bytes) {
     CHK_S(s);

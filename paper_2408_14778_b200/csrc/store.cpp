@@ -66,7 +66,15 @@ void info_fields(IO& io, S& s) {
     io.pod(s.owned_nodes);
 }
 
-const char kMagic[8] = {'C', 'F', 'R', 'S', 'H', 'R', 'D', '1'};
+const char kMagic[8] = {'C', 'F', 'R', 'S', 'H', 'R', 'D', '2'};
+// The file stores raw TileH / SegH records: their sizes are part of the format, so
+// a layout change is rejected on load instead of being read as corrupt data.
+struct FormatTag {
+    uint32_t version = 2;
+    uint32_t tile_bytes = (uint32_t)sizeof(TileH);
+    uint32_t seg_bytes = (uint32_t)sizeof(SegH);
+    uint32_t pad = 0;
+};
 
 }  // namespace
 
@@ -79,6 +87,8 @@ bool save_shard(const std::string& path, const Game& full, const Game& local, co
     if (!f) { err = "cannot open " + path + " for writing"; return false; }
     Writer w{f};
     w.ok = std::fwrite(kMagic, 1, 8, f) == 8;
+    const FormatTag tag;
+    w.ok = w.ok && std::fwrite(&tag, sizeof(tag), 1, f) == 1;
     // header of the full game (info / caller-order readbacks)
     Game head;
     head.V = full.V; head.P = full.P; head.Pc = full.Pc; head.zero_sum_2p = full.zero_sum_2p; head.D = full.D;
@@ -90,8 +100,12 @@ bool save_shard(const std::string& path, const Game& full, const Game& local, co
     game_fields(w, head);
     game_fields(w, const_cast<Game&>(local));
     info_fields(w, const_cast<ShardInfo&>(info));
-    const bool ok = w.ok && std::fclose(f) == 0;
-    if (!ok) err = "write failed: " + path;
+    const bool closed = std::fclose(f) == 0;   // always close, then combine
+    const bool ok = w.ok && closed;
+    if (!ok) {
+        err = "write failed: " + path;
+        std::remove(path.c_str());   // no partial shard file left behind
+    }
     return ok;
 }
 
@@ -101,7 +115,11 @@ bool load_shard(const std::string& path, Game& head, Game& local, ShardInfo& inf
     Reader r{f};
     char magic[8];
     r.ok = std::fread(magic, 1, 8, f) == 8 && std::memcmp(magic, kMagic, 8) == 0;
-    if (!r.ok) { std::fclose(f); err = "bad magic in " + path; return false; }
+    if (!r.ok) { std::fclose(f); err = "bad magic (or an older shard format) in " + path; return false; }
+    FormatTag tag, want;
+    r.ok = std::fread(&tag, sizeof(tag), 1, f) == 1 && tag.version == want.version &&
+           tag.tile_bytes == want.tile_bytes && tag.seg_bytes == want.seg_bytes;
+    if (!r.ok) { std::fclose(f); err = "shard format version / record layout mismatch in " + path; return false; }
     game_fields(r, head);
     game_fields(r, local);
     info_fields(r, info);
@@ -138,6 +156,12 @@ cfr_status cfr_game_load_shard(const char* prefix, int32_t rank, int32_t world, 
     if (!cfrb::load_shard(cfrb::shard_path(prefix, rank, world), G->g, sh->local, sh->info, err)) {
         delete G;
         cfrb_set_error(err);
+        return CFR_ERR_INVALID_ARG;
+    }
+    if (sh->info.rank != rank || sh->info.world != world) {
+        delete G;
+        cfrb_set_error("shard file " + cfrb::shard_path(prefix, rank, world) + " holds rank " +
+                       std::to_string(sh->info.rank) + " of " + std::to_string(sh->info.world));
         return CFR_ERR_INVALID_ARG;
     }
     G->shard_only = true;

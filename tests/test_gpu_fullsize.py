@@ -6,13 +6,15 @@ size, so the checks are:
     kernels (k_bwd, FLAG_NO_STREAM: a separately written backward kernel) reach
     bit-identical state after T iterations -- the exact accumulation (reading
     Q8) makes the result independent of how members are grouped and summed;
-  * sampled outputs against the oracle: after one iteration, the regrets of
-    randomly drawn deepest-level infosets equal oracle/sampled.py (Eq 6/7 from
-    the definitions, pinned against the full oracle in test_oracle_pins.py)
-    within the north-star tolerance (1e-10 relative, f64);
+  * sampled outputs against the oracle: after one iteration, the regrets R^1
+    of randomly drawn deepest-level infosets (Eq 6/7), their S_den = pi_bar
+    (Eq 5 / Eq 10), their sigma^2 = RM(R^1) (Eq 9), and the expected value of
+    sigma_bar^1 = sigma^1 (the uniform profile: a plain sum over all 917M
+    terminals of pi(z) u(z)) equal oracle/sampled.py (the definitions, pinned
+    against the full oracle in test_oracle_pins.py) within the north-star
+    tolerance (1e-10 relative, f64);
   * properties that hold at any size: sigma and sigma_bar are distributions per
-    infoset, CFR+ regrets are non-negative, the game is zero-sum so the two
-    expected values cancel."""
+    infoset, CFR+ regrets are non-negative."""
 import gc
 
 import numpy as np
@@ -21,7 +23,7 @@ import pytest
 import gamegen
 from gamegen.synthetic_tree import synthetic_counts
 import paper_2408_14778_b200 as pb
-from oracle.sampled import first_iteration_regrets, qbase
+from oracle.sampled import first_iteration_pibar, first_iteration_regrets, qbase, regret_matching, uniform_ev
 
 pytestmark = pytest.mark.gpu
 
@@ -48,6 +50,8 @@ def test_full_size_stream_vs_tile_and_invariants(cuda):
     dec = np.flatnonzero(desc.player > 0)
     rng = np.random.default_rng(2408)
     hs = np.unique(desc.infoset[rng.choice(dec[-len(dec) // 10:], 8, replace=False)])
+    pib = first_iteration_pibar(desc, hs)
+    ev_u, mag = uniform_ev(desc)
     for variant, plus in (("cfr+", True), ("cfr", False)):   # CFR: signed regrets
         one = _run(game, 0, 1, variant)
         assert "k_bwd_stream" in one["kernels"], one["kernels"]
@@ -57,8 +61,15 @@ def test_full_size_stream_vs_tile_and_invariants(cuda):
             tol = 1e-10 * np.abs(ref[h]).max()
             assert np.abs(ref[h]).max() > 0
             assert np.all(np.abs(got - ref[h]) <= tol), (variant, h, got, ref[h])
+            assert abs(one["sden"][h] - pib[h]) <= 1e-10 * pib[h], (h, one["sden"][h], pib[h])
+            want = regret_matching(ref[h])
+            assert np.all(np.abs(one["cur"][q[h]:q[h + 1]] - want) <= 1e-10 * want.max()), (h, want)
         if not plus:
             assert any((ref[h] < 0).any() for h in hs)
+        # EV of sigma_bar^1 = sigma^1: rounding of the device's Eq 1 tree sums is
+        # bounded by (depth + 1) * 2^-53 * sum_z pi(z)|u(z)| (depth 11)
+        assert np.all(np.abs(one["ev"] - ev_u) <= 12 * 2.0 ** -53 * mag), (one["ev"], ev_u, mag)
+        assert np.all(np.abs(one["ev"] - ev_u) <= 1e-10 * np.abs(ev_u)), (one["ev"], ev_u)
         del one
     del desc, dec
     gc.collect()
@@ -76,5 +87,3 @@ def test_full_size_stream_vs_tile_and_invariants(cuda):
         assert np.all(np.abs(sums - 1.0) <= 1e-12), (k, np.abs(sums - 1.0).max())
         assert np.all(a[k] >= 0.0)
     assert np.all(a["regret"] >= 0.0)
-    ev = a["ev"]
-    assert abs(ev[0] + ev[1]) <= 1e-9 * max(1.0, abs(ev[0])), ev

@@ -1,0 +1,100 @@
+"""GPU parity at each BASELINE.json config's stated iteration count, and on a
+bench-shaped synthetic tree against the FULL oracle.
+
+CFR's trajectory is chaotic in floating point (Leduc diverges O(1)
+by T = 10k under a reordered sum), so a rare divergence (the z = 0 branch of
+Eq 9, a -0, an unrounded input) shows up only at long T.  Every comparison is
+IEEE equality of the whole state (sigma, R, S_num, S_den), sigma_bar, EV and
+best response (tests/parity.py), i.e. strictly inside the north-star bar of
+1e-10 relative (f64) / 1e-4 (f32)."""
+import numpy as np
+import pytest
+
+import gamegen
+import oracle
+import paper_2408_14778_b200 as pb
+from tests.parity import assert_same, run_pair
+from tests.test_gpu_sharded import run_world
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_leduc_10k(cuda, variant, precision):
+    """configs[1]: Leduc poker, CFR and CFR+, 10k iterations, fp64 and fp32."""
+    out, s, o = run_pair(gamegen.leduc(), variant, precision, 10_000)
+    ev = s.expected_values()
+    nc = s.exploitability()["nash_conv"]
+    # literature value ~ -0.0856 (not in PAPER.md): within the 2-eps bound
+    assert abs(ev[0] + 0.0856) <= nc + 1e-3
+
+
+@pytest.mark.parametrize("precision,T", [(64, 1000), (32, 200)])
+def test_liars_dice_cfr_plus(cuda, precision, T):
+    """configs[2]: liar's dice 1x6, CFR+ on one B200."""
+    run_pair(gamegen.liars_dice(), 1, precision, T)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_goofspiel_cfr_plus_2000(cuda, precision):
+    """configs[3] on one GPU: Goofspiel-5, CFR+, T = 2000 (value 0 by symmetry)."""
+    out, s, o = run_pair(gamegen.goofspiel(), 1, precision, 2000)
+    ev = s.expected_values()
+    assert abs(ev[0]) <= s.exploitability()["nash_conv"]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_goofspiel_cfr_plus_2000_sharded(cuda, world):
+    """configs[3] at 2/4/8 ranks (level-sharded; ranks driven in one
+    process with exact host exchanges): bit-identical to the oracle at T = 2000."""
+    desc = gamegen.goofspiel()
+    T = 2000
+    o = oracle.Oracle(desc, precision=64).run(T, 1)
+    r = run_world(desc, 1, 64, T, world)
+    os_ = o.state()
+    assert_same("average strategy", r["avg"], os_["avg"], 64)
+    assert_same("current strategy", r["cur"], os_["sigma"], 64)
+    assert_same("regret", r["regret"], os_["regret"], 64)
+    assert_same("S_den", r["sden"], os_["sden"], 64)
+    for ev in r["ev"]:
+        assert_same("EV(avg)", ev, o.expected_values(), 64)
+    oe = o.exploitability()
+    for b in r["br"]:
+        assert_same("BR", b, oe["br"], 64)
+
+
+# ------------------------------------------------- bench-shaped synthetic
+def _bench_shaped(c, seed):
+    """configs[4]'s shape (n = 40 types: 40 members per infoset, |A| = 20, the
+    multiply-shift member->infoset map umem = 40, compact reach rows of the deepest
+    level) with a truncated public tree so the full oracle finishes in seconds."""
+    return gamegen.synthetic(n_types=40, c=c, seed=seed)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_bench_shaped_synthetic_vs_full_oracle(cuda, variant, precision):
+    desc = _bench_shaped((4, 3), seed=11)
+    T = 50
+    out, s, o = run_pair(desc, variant, precision, T, flags=pb.FLAG_FORCE_STREAM)
+    kern = s.level_kernels()
+    # every player level with whole infosets streams, like the bench's levels 5-10
+    assert kern[-1] == "k_bwd_stream" and kern.count("k_bwd_stream") >= 3, kern
+    c = s.counters()
+    assert c["infosets"] > 0 and 0 < c["live_infosets"] <= c["infosets"]
+
+
+@pytest.mark.parametrize("variant,precision", [(1, 64), (0, 32)])
+def test_bench_shaped_deeper_synthetic_vs_full_oracle(cuda, variant, precision):
+    """Four public levels below the deal (V = 6.7M): the bench's alternation of
+    player-1 / player-2 streaming levels, T = 10."""
+    desc = _bench_shaped((4, 3, 4, 3), seed=5)
+    out, s, o = run_pair(desc, variant, precision, 10, flags=pb.FLAG_FORCE_STREAM)
+    assert s.level_kernels().count("k_bwd_stream") >= 5, s.level_kernels()
+
+
+def test_bench_shaped_default_flags(cuda):
+    """The same tree in the default configuration (the planner's own kernel choice)."""
+    desc = _bench_shaped((4, 3, 4), seed=2)
+    run_pair(desc, 1, 64, 20)

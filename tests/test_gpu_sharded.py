@@ -13,7 +13,7 @@ from tests.parity import assert_same
 pytestmark = pytest.mark.gpu
 
 
-def run_world(desc, variant, precision, T, world, shard_prefix=None):
+def run_world(desc, variant, precision, T, world, shard_prefix=None, br=True):
     g = pb.Game(desc)
     games = [g] * world
     if shard_prefix is not None:      # ranks load their own view from shard files
@@ -52,7 +52,34 @@ def run_world(desc, variant, precision, T, world, shard_prefix=None):
         s.phase(pb.Solver.PHASE_EV_LOWER)
     allreduce(pb.Solver.XCHG_CUT)
     evs = [s.phase(pb.Solver.PHASE_EV_UPPER) for s in ss]
-    return dict(avg=avg, cur=cur, regret=reg, sden=sden, ev=evs, info=[s.shard_info() for s in ss])
+    out = dict(avg=avg, cur=cur, regret=reg, sden=sden, ev=evs, info=[s.shard_info() for s in ss])
+    if br:
+        out["br"] = world_best_response(ss, allreduce)
+    return out
+
+
+def world_best_response(ss, allreduce):
+    """Best response to sigma_bar of every player through the sharded BR passes
+    (include/cfr_b200.h CFR_BR_*): per pass lower -> cut sum -> upper -> int64 sum
+    of the deferred infosets' exact BR sums -> decide.  Returns [rank][player]."""
+    P = ss[0].P
+    for s in ss:
+        s.br_phase(pb.Solver.BR_SETUP)
+    passes = ss[0].br_passes()
+    assert all(s.br_passes() == passes for s in ss)
+    res = [[0.0] * P for _ in ss]
+    for i in range(1, P + 1):
+        for _ in range(passes):
+            for s in ss:
+                s.br_phase(pb.Solver.BR_LOWER, i)
+            allreduce(pb.Solver.XCHG_CUT)
+            for s in ss:
+                s.br_phase(pb.Solver.BR_UPPER, i)
+            allreduce(pb.Solver.XCHG_ACC)
+            outs = [s.br_phase(pb.Solver.BR_DECIDE, i) for s in ss]
+        for r, o in enumerate(outs):
+            res[r][i - 1] = o[i - 1]
+    return res
 
 
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
@@ -70,6 +97,9 @@ def test_sharded_bit_identical_to_oracle(cuda, name, variant, precision, T, worl
     assert_same("S_den", r["sden"], os_["sden"], precision)
     for ev in r["ev"]:
         assert_same("EV(avg)", ev, o.expected_values(), precision)
+    oe = o.exploitability()
+    for b in r["br"]:   # every rank holds the same best-response values
+        assert_same("BR", b, oe["br"], precision)
     if name != "kuhn3":
         assert r["info"][0]["cut"] >= 1
 
@@ -84,6 +114,8 @@ def test_sharded_liars_dice_and_random(cuda):
         o = oracle.Oracle(d).run(8, seed % 2)
         r = run_world(d, seed % 2, 64, 8, 2 + seed % 3)
         assert_same("avg", r["avg"], o.state()["avg"], 64)
+        for b in r["br"]:
+            assert_same("BR", b, o.exploitability()["br"], 64)
         assert_same("regret", r["regret"], o.state()["regret"], 64)
 
 

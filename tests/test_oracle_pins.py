@@ -447,3 +447,227 @@ def test_sampled_first_iteration_regrets_match_full_oracle(n_types, seed):
             ref = reg[q[h]:q[h + 1]]
             assert np.allclose(res[h], ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max()), h
             assert np.abs(ref).max() > 0
+
+
+# ------------------------------------------------------------- f32 mode (Q14)
+# Reading Q14 ("both 64-bit and 32-bit floating-point data types"): in f32
+# mode the utilities and sigma_0 are rounded to binary32 ONCE at load, all state
+# is binary32, and every exact slice sum is decoded to binary64 and rounded ONCE
+# to binary32.  The two games below are built so that each of those two rules
+# changes a result macroscopically (a strategy or an ulp-exact regret).
+
+def _one_decision(payoffs):
+    b = gamegen.Builder("one_decision", 1)
+    r = b.node(-1, -1)
+    b.set_player(r, 1, "root", len(payoffs))
+    for a, u in enumerate(payoffs):
+        b.set_terminal(b.node(r, a), [u])
+    return b.build(zero_sum=False)
+
+
+def test_f32_rounds_utilities_once_at_load():
+    """Payoffs (1 + 2^-30, 1): in binary64 action 0 is strictly better by 2^-30,
+    so r~ = (+2^-31, -2^-31) (Eq 7, sigma^1 uniform) and sigma^2 = (1, 0) (Eq 9).
+    Rounded to binary32 first, both payoffs are 1: r~ = (0, 0), sigma^2 uniform
+    (Eq 9, z = 0).  An f32 mode that kept binary64 inputs would give (1, 0)."""
+    d = _one_decision([1.0 + 2.0 ** -30, 1.0])
+    s64 = oracle.Oracle(d, 64).run(1, 0).state()
+    assert np.array_equal(s64["regret"], [2.0 ** -31, -(2.0 ** -31)])
+    assert np.array_equal(s64["sigma"], [1.0, 0.0])
+    s32 = oracle.Oracle(d, 32).run(1, 0).state()
+    assert np.array_equal(s32["regret"], [0.0, 0.0])
+    assert np.array_equal(s32["sigma"], [0.5, 0.5])
+
+
+def _hidden_chance_decision():
+    """Chance (1/2, 1/4, 1/4) -> one player-1 infoset (the outcome is hidden) with
+    two actions; payoffs (2, -2), (3*2^-24, -3*2^-24) twice (all exact in binary32).
+    Under sigma^1 every u(d) = 0, so the Eq 7 terms of action 0 are
+    1/2 * 2 = 1 and 1/4 * 3*2^-24 = 0.75*2^-24 (twice)."""
+    b = gamegen.Builder("hidden_chance", 1)
+    r = b.node(-1, -1)
+    b.set_chance(r)
+    small = 3.0 * 2.0 ** -24
+    for k, (p, u) in enumerate(((0.5, 2.0), (0.25, small), (0.25, small))):
+        v = b.node(r, k, p)
+        b.set_player(v, 1, "hidden", 2)
+        b.set_terminal(b.node(v, 0), [u])
+        b.set_terminal(b.node(v, 1), [-u])
+    return b.build(zero_sum=False)
+
+
+def test_f32_exact_sum_decoded_then_rounded_once():
+    """r~(h, 0) = 1 + 1.5*2^-24 exactly (binary64 holds it).  Rounded once to
+    binary32 that is 1 + 2^-23 (0.75 ulp rounds up); a running binary32 sum in
+    node order gives 1 (each 0.375-ulp term rounds away).  The result may not
+    depend on the node order (reading Q8)."""
+    d = _hidden_chance_decision()
+    r64 = oracle.Oracle(d, 64).run(1, 0).state()["regret"]
+    assert r64[0] == 1.0 + 1.5 * 2.0 ** -24 and r64[1] == -r64[0]
+    for desc in (d, d.shuffled(1), d.shuffled(2)):
+        r32 = oracle.Oracle(desc, 32).run(1, 0).state()["regret"]
+        assert r32[0] == 1.0 + 2.0 ** -23 and r32[1] == -r32[0], r32
+    naive = np.float32(0)
+    for t in (1.0, 0.75 * 2.0 ** -24, 0.75 * 2.0 ** -24):
+        naive = np.float32(naive + np.float32(t))
+    assert naive == np.float32(1.0)   # the order-dependent answer the rule excludes
+
+
+def test_f32_kuhn_uniform_closed_forms():
+    """Kuhn under sigma^1 in binary32: EV = (1/8, -1/8), BR = (1/2, 5/12),
+    NashConv = 11/12, each within a few binary32 ulps (payoffs are
+    small integers; only 1/3 and 1/2 are rounded)."""
+    o = oracle.Oracle(gamegen.kuhn(2), 32)
+    ulp = 2.0 ** -24
+    ev = o.expected_values("current")
+    assert abs(ev[0] - 0.125) <= 8 * ulp and abs(ev[1] + 0.125) <= 8 * ulp
+    ex = o.exploitability("current")
+    assert abs(ex["br"][0] - 0.5) <= 16 * ulp and abs(ex["br"][1] - 5.0 / 12.0) <= 16 * ulp
+    assert abs(ex["nash_conv"] - 11.0 / 12.0) <= 32 * ulp
+    # every readback is a binary32 number
+    for x in list(ev) + list(ex["br"]):
+        assert float(np.float32(x)) == x
+
+
+def _eq7_bruteforce_f32(d, o, sigma):
+    """_eq7_bruteforce in binary32 arithmetic: inputs rounded once (Q14), every
+    product and sum a binary32 operation (plain Python over np.float32 scalars)."""
+    f = np.float32
+    ch, root = _tree(d)
+    P = d.num_players
+    qb = o.qbase
+    util = d.utility.astype(np.float32)
+    cp = d.chance_prob.astype(np.float32)
+    sig = np.asarray(sigma, dtype=np.float32)
+
+    def prob(v, a, prof):
+        c = ch[v][a]
+        return cp[c] if d.player[v] == 0 else prof[qb[d.infoset[v]] + a]
+
+    def value(v, prof):
+        if d.player[v] < 0:
+            return util[v].copy()
+        out = np.zeros(P, dtype=np.float32)
+        for a, c in enumerate(ch[v]):
+            out = (out + prob(v, a, prof) * value(c, prof)).astype(np.float32)
+        return out
+
+    pc, ph = {}, {}
+
+    def reach(v, rc, rh):
+        pc[v], ph[v] = rc, rh
+        if d.player[v] < 0:
+            return
+        pl = d.player[v]
+        for a, c in enumerate(ch[v]):
+            s = prob(v, a, sig)
+            reach(c, [f(rc[j] * (s if pl != j + 1 else f(1))) for j in range(P)],
+                  [f(rh[j] * (s if pl == j + 1 else f(1))) for j in range(P)])
+
+    reach(root, [f(1)] * P, [f(1)] * P)
+    rt = np.zeros(o.Q)
+    for h in range(o.H):
+        members = [int(v) for v in np.nonzero((d.infoset == h) & (d.player >= 1))[0]]
+        i = int(d.player[members[0]])
+        n = int(qb[h + 1] - qb[h])
+        # the literal Eq 6/7 (P:109-125): sum_d pi_check(d) u(sigma|h->a, d) - sum_d pi_check(d) u(sigma, d)
+        base = f(0)
+        for m in members:
+            base = f(base + f(pc[m][i - 1] * value(m, sig)[i - 1]))
+        for a in range(n):
+            over = sig.copy()
+            over[qb[h]:qb[h + 1]] = 0
+            over[qb[h] + a] = 1
+            tot = f(0)
+            for m in members:
+                tot = f(tot + f(pc[m][i - 1] * value(m, over)[i - 1]))
+            rt[qb[h] + a] = float(f(tot - base))
+    return rt
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 5])
+def test_f32_iteration_one_matches_literal_eq7_in_binary32(seed):
+    """The f32 oracle's first-iteration regrets against the LITERAL Eq 6/7 evaluated
+    in binary32 (a different formula: override profiles, no cancellation).  The two
+    differ only by binary32 rounding: |d| <= 64 ulp(1) * max|u| (depth <= 6 sums of
+    <= 4 terms on each side).  Every regret is a binary32 number, and it is within
+    the same scale of the binary64 oracle's."""
+    d = gamegen.random_game(seed, num_players=2 + seed % 2, max_nodes=300)
+    o32 = oracle.Oracle(d, 32)
+    sigma1 = o32.current_strategy()
+    lit = _eq7_bruteforce_f32(d, o32, sigma1)
+    got = o32.run(1, 0).state()["regret"]
+    umax = float(np.abs(d.utility).max())
+    assert np.all(np.abs(got - lit) <= 64 * 2.0 ** -24 * umax), np.abs(got - lit).max()
+    for x in got:
+        assert float(np.float32(x)) == x
+    r64 = oracle.Oracle(d, 64).run(1, 0).state()["regret"]
+    assert np.all(np.abs(got - r64) <= 64 * 2.0 ** -24 * umax)
+
+
+@pytest.mark.parametrize("n_types,seed", [(2, 1), (3, 4)])
+def test_sampled_pibar_rm_and_uniform_ev_match_full_oracle(n_types, seed):
+    """oracle/sampled.py's pi_bar (Eq 5), regret matching (Eq 9) of the sampled R^1
+    and the uniform-profile EV against the full oracle after one iteration."""
+    from oracle.sampled import first_iteration_pibar, first_iteration_regrets, qbase, regret_matching, uniform_ev
+    d = gamegen.synthetic(n_types=n_types, seed=seed)
+    q = qbase(d)
+    dec = np.flatnonzero(d.player > 0)
+    rng = np.random.default_rng(seed)
+    hs = np.unique(d.infoset[rng.choice(dec[-len(dec) // 10:], 30, replace=False)])
+    for plus in (False, True):
+        o = oracle.Oracle(d).run(1, int(plus))
+        st = o.state()
+        pib = first_iteration_pibar(d, hs)
+        r1 = first_iteration_regrets(d, hs, plus)
+        for h in hs:
+            assert abs(st["sden"][h] - pib[h]) <= 1e-15 * pib[h] and pib[h] > 0
+            assert np.allclose(st["sigma"][q[h]:q[h + 1]], regret_matching(r1[h]), rtol=1e-12, atol=1e-13)
+        ev, mag = uniform_ev(d)
+        assert np.all(np.abs(o.expected_values() - ev) <= 1e-14 * mag), (o.expected_values(), ev)
+        assert np.all(mag > 0) and abs(ev[0] + ev[1]) <= 1e-15 * mag[0]
+
+
+def _depths(d):
+    dep = np.full(d.num_nodes, -1)
+    order = []
+    root = int(np.nonzero(d.parent < 0)[0][0])
+    dep[root] = 0
+    ch = [[] for _ in range(d.num_nodes)]
+    for v in range(d.num_nodes):
+        if d.parent[v] >= 0:
+            ch[d.parent[v]].append(v)
+    stack = [root]
+    while stack:
+        v = stack.pop()
+        for c in ch[v]:
+            dep[c] = dep[v] + 1
+            stack.append(c)
+    return dep
+
+
+@pytest.mark.parametrize("seed", [5, 11, 33, 34])
+def test_best_response_on_depth_spanning_infosets_equals_enumeration(seed):
+    """Reading Q17: on perfect-recall games whose infosets pool nodes of different
+    depths, the oracle's memoised recursive BR equals the max over every pure
+    strategy of the player (max over Sigma_j; pure strategies suffice)."""
+    d = gamegen.random_game(seed, num_players=2, span_depths=True, max_depth=5, max_nodes=80)
+    dep = _depths(d)
+    spans = [h for h in range(d.num_infosets) if len(set(dep[d.infoset == h])) > 1]
+    assert spans, "fixture must pool nodes of several depths"
+    o = oracle.Oracle(d)
+    rng = np.random.default_rng(seed)
+    base = np.zeros(o.Q)
+    for h in range(o.H):
+        w = rng.uniform(0.05, 1, size=o.qbase[h + 1] - o.qbase[h])
+        base[o.qbase[h]:o.qbase[h + 1]] = w / w.sum()
+    for pl in (1, 2):
+        best = -math.inf
+        for hs, choice in _pure_strategies(d, o, pl):
+            s = base.copy()
+            for h, a in zip(hs, choice):
+                s[o.qbase[h]:o.qbase[h + 1]] = 0.0
+                s[o.qbase[h] + a] = 1.0
+            best = max(best, o.expected_values(s)[pl - 1])
+        val, _ = o.best_response(pl, base)
+        assert abs(val - best) <= 1e-12, (pl, val, best)
