@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-games", action="store_true", help="skip the per-game (Kuhn/Leduc/...) lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--no-variants", action="store_true", help="skip the configs[4] variant / precision lines")
+    ap.add_argument("--variant-steps", type=int, default=50)
     ap.add_argument("--cpu-sample-types", type=int, default=4)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -128,33 +130,88 @@ def cpu_baseline(n_types: int, variant: int, precision: int, seconds: float, V_f
     d = gamegen.synthetic(n_types=n_types)
     o = oracle.Oracle(d, precision=precision)
     del d
-    t0 = time.perf_counter()
-    it = 0
-    while True:
-        o.run(1, variant)
-        it += 1
-        if time.perf_counter() - t0 >= seconds:
-            break
-    dt = time.perf_counter() - t0
+    with pinned_core() as pc:
+        t0 = time.perf_counter()
+        it = 0
+        while True:
+            o.run(1, variant)
+            it += 1
+            if time.perf_counter() - t0 >= seconds:
+                break
+        dt = time.perf_counter() - t0
     node_s = o.V * it / dt
     return {
         "value": node_s / V_full,
         "unit": UNIT,
         "cores": 1,
         "kind": "oracle",
+        "pinned_core": pc.core,
         "node_updates_per_s": node_s,
         "sample": (f"synthetic n_types={n_types} ({o.V:,} nodes = {100.0 * o.V / V_full:.2f}% of the "
-                   f"workload), {it} oracle iteration(s) in {dt:.1f} s; value = node-updates/s / V_workload"),
+                   f"workload), {it} oracle iteration(s) in {dt:.1f} s; value = node-updates/s / V_workload "
+                   f"(extrapolated by node count)"),
     }
 
 
-def per_game(pb, torch, variant: str, precision: int):
-    """Secondary lines of the metric: it/s and node-updates/s per small game."""
-    out = {}
-    for name, iters in (("kuhn", 2000), ("leduc", 1000), ("goofspiel", 500), ("liars_dice", 500), ("goofspiel6", 200)):
-        d = gamegen.goofspiel(6) if name == "goofspiel6" else gamegen.by_name(name)
+# BASELINE.json configs[0-3] (+ Goofspiel-6, a paper-scale second real game) as
+# secondary lines: (name, variant, precision, GPU iterations timed, oracle
+# iterations timed).  The oracle (test infrastructure, as it stands, 1 pinned core)
+# runs beside each line on this box's host.
+GAME_LINES = (
+    ("kuhn", "cfr", 64, 1000, 1000),          # configs[0]
+    ("leduc", "cfr", 64, 10000, 2000),        # configs[1]
+    ("leduc", "cfr", 32, 10000, 2000),
+    ("leduc", "cfr+", 64, 10000, 2000),
+    ("leduc", "cfr+", 32, 10000, 2000),
+    ("liars_dice", "cfr+", 64, 1000, 100),    # configs[2]
+    ("liars_dice", "cfr+", 32, 1000, 100),
+    ("goofspiel", "cfr+", 64, 2000, 500),     # configs[3]
+    ("goofspiel", "cfr+", 32, 2000, 500),
+    ("goofspiel6", "cfr+", 64, 300, 10),
+)
+# PAPER.md Table 2, vanilla CFR, RTX 4090 + CuPy, mean ms per iteration
+PAPER_MS = {("kuhn", 64): 3.319, ("kuhn", 32): 3.362, ("leduc", 64): 6.269, ("leduc", 32): 6.178,
+            ("liars_dice", 64): 10.766, ("liars_dice", 32): 8.443}
+
+
+def host_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model,
+            "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None}
+
+
+class pinned_core:
+    """Run the oracle on one host core (restores the affinity afterwards)."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = min(self.old)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.old)
+
+
+def game_desc(name: str):
+    return gamegen.goofspiel(6) if name == "goofspiel6" else gamegen.by_name(name)
+
+
+def per_game(pb, torch, with_oracle: bool):
+    """Secondary lines of the metric: it/s and node-updates/s per BASELINE config
+    (latency-bound, L2-resident games: no HBM fraction), the oracle beside each."""
+    out = []
+    for name, variant, prec, iters, oiters in GAME_LINES:
+        d = game_desc(name)
         g = pb.Game(d)
-        s = pb.Solver(g, variant=variant, precision=precision)
+        s = pb.Solver(g, variant=variant, precision=prec)
         s.run(5)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s.stream)
@@ -162,13 +219,82 @@ def per_game(pb, torch, variant: str, precision: int):
         e1.record(s.stream)
         s.sync()
         ms = e0.elapsed_time(e1) / iters
-        out[name] = {"it_per_s": round(1e3 / ms, 1), "node_updates_per_s": float(f"{g.V * 1e3 / ms:.4g}"),
-                     "V": g.V, "launches_per_iter": s.launches_per_iteration()}
-        del s, g
+        e = {"game": name, "variant": variant, "dtype": f"f{prec}", "iterations": iters,
+             "it_per_s": round(1e3 / ms, 1), "node_updates_per_s": float(f"{g.V * 1e3 / ms:.4g}"), "V": g.V,
+             "launches_per_iter": s.launches_per_iteration(), "kernels": sorted({k for k in s.level_kernels() if k})
+             if s.launches_per_iteration() > 1 else ["k_tiny"]}
+        del s
+        if with_oracle:
+            import oracle
+
+            o = oracle.Oracle(d, precision=prec)
+            with pinned_core() as pc:
+                t0 = time.perf_counter()
+                o.run(oiters, 1 if variant == "cfr+" else 0)
+                dt = time.perf_counter() - t0
+            e["oracle"] = {"it_per_s": round(oiters / dt, 1), "node_updates_per_s": float(f"{g.V * oiters / dt:.4g}"),
+                           "iterations": oiters, "cores": 1, "pinned_core": pc.core}
+            e["gpu_over_oracle"] = round(e["it_per_s"] / e["oracle"]["it_per_s"], 2)
+            del o
+        pm = PAPER_MS.get((name, prec))
+        if pm is not None:
+            e["paper_context"] = {"it_per_s": round(1e3 / pm, 1), "variant": "cfr",
+                                  "hardware": "RTX 4090 + CuPy (PAPER.md Table 2, P:426)"}
+        out.append(e)
+        del g
     return out
 
 
+def synthetic_variants(pb, torch, game, dev, lines, steps: int):
+    """configs[4] under the other variant / precision combinations (each its own
+    solver on the same flattened game; CUDA events around `steps` graph replays)."""
+    out = []
+    for variant, prec in lines:
+        s = pb.Solver(game, variant=variant, precision=prec, device=dev)
+        s.run(3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s.stream)
+        s.enqueue(steps)
+        e1.record(s.stream)
+        s.sync()
+        ms = e0.elapsed_time(e1) / steps
+        prof = s.profile(3)
+        mb = s.model_bytes()
+        out.append({"variant": variant, "dtype": f"f{prec}", "steps": steps, "it_per_s": round(1e3 / ms, 2),
+                    "ms_per_step": round(ms, 4), "node_updates_per_s": float(f"{game.V * 1e3 / ms:.4g}"),
+                    "dominant_ms": round(prof["dominant_ms"], 4),
+                    "dominant_GBps": round(mb["dominant"] / (prof["dominant_ms"] * 1e-3) / 1e9, 1),
+                    "whole_step_model_GBps": round(mb["total"] / (ms * 1e-3) / 1e9, 1)})
+        del s
+        torch.cuda.empty_cache()
+    return out
+
+
+PAPER_CONTEXT = {
+    "max_speedup_vs_openspiel_python": 401.2, "max_speedup_vs_openspiel_cpp": 203.6,
+    "games": "tic_tac_toe f32 (P:487); Battleship-7 f32 (P:632)",
+    "largest_game_node_updates_per_s": 1.30e8,
+    "largest_game": "Battleship-11, 57.9M nodes, f32, 446.4 ms/it (P:602)",
+    "hardware": "NVIDIA RTX 4090 (CuPy/cuSPARSE) vs AMD Ryzen 9 3900X (PAPER.md P:345)",
+    "note": "context only: another machine, vanilla CFR, OpenSpiel baselines (P:7)",
+}
+
+
+def config_of(args, V=None, D=None, H=None, Q=None):
+    """The `config` object: identical for both arms (same workload)."""
+    w = f"synthetic_n{args.n_types}"
+    if V is None:
+        c = gamegen.synthetic_counts(args.n_types)
+        V, D, H, Q = c["V"], c["D"], c["H"], c["Q"]
+    return {"workload": f"{w}: {V:,} nodes, D={D}, {H:,} infosets, {Q:,} (h,a) pairs (BASELINE.json configs[4])",
+            "variant": args.variant, "precision": f"f{args.precision}"}
+
+
 def run_reference(args):
+    """The oracle (as it stands, one pinned host core) on a bounded sample of the
+    workload: each step = one oracle iteration over the n = cpu_sample_types
+    synthetic; `value` is extrapolated to the full workload by node count (the
+    oracle's cost per iteration is linear in V)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -179,26 +305,33 @@ def run_reference(args):
     d = gamegen.synthetic(n_types=args.cpu_sample_types)
     o = oracle.Oracle(d, precision=args.precision)
     del d
-    for _ in range(args.warmup):
-        o.run(1, variant)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        o.run(1, variant)
-    dt = time.perf_counter() - t0
+    with pinned_core() as pc:
+        for _ in range(args.warmup):
+            o.run(1, variant)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            o.run(1, variant)
+        dt = time.perf_counter() - t0
     node_s = o.V * args.steps / dt
     value = node_s / V_full
+    sample = (f"synthetic n_types={args.cpu_sample_types} ({o.V:,} nodes = {100.0 * o.V / V_full:.2f}% of the "
+              f"workload), {args.steps} oracle iterations in {dt:.1f} s on 1 pinned core; value = node-updates/s / V_workload")
     line = {
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup,
+        # the measured time of one sample step (what the timed region holds); the
+        # full-workload time per iteration is 1e3 / value (extrapolated)
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": f"f{args.precision}", "data": "synthetic",
-        "config": {"workload": f"synthetic_n{args.n_types}", "variant": args.variant,
-                   "sample": f"synthetic n_types={args.cpu_sample_types} ({o.V:,} nodes)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"synthetic n_types={args.cpu_sample_types} ({o.V:,} nodes), "
-                                   f"{args.steps} oracle iterations; value = node-updates/s / V_workload"},
+        "config": config_of(args),
+        "extrapolated": {"from_nodes": o.V, "to_nodes": V_full, "factor": V_full / o.V,
+                         "full_workload_ms_per_iteration": 1e3 / value,
+                         "note": "value = sample node-updates/s / V_workload (oracle cost linear in V)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "node_updates_per_s": node_s,
+        "host": host_info(),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -283,6 +416,7 @@ def main():
         ms = float(t.item())
         dist.barrier()
     launches = solver.launches_per_iteration()
+    shard_cut = solver.shard_info()["cut"] if world > 1 else None
 
     # ---- roofline of the dominant kernel (live CUDA events, un-graphed launches)
     prof = solver.profile(5)
@@ -335,9 +469,18 @@ def main():
            "note": "per step: cfr_solver_run(1) (status read back); sigma_bar read back once per window"}
     assert np.isfinite(avg).all()
 
+    # ---- configs[4] under the other variants / precisions (the headline solver
+    # is released first: each solver holds the full device state)
+    del solver
+    torch.cuda.empty_cache()
+    variants = None
+    if rank == 0 and world == 1 and not args.no_variants:
+        others = [(v, p) for v in ("cfr+", "cfr") for p in (64, 32) if (v, p) != (args.variant, args.precision)]
+        variants = synthetic_variants(pb, torch, game, dev, others, args.variant_steps)
+
     games = None
     if rank == 0 and not args.no_games:
-        games = per_game(pb, torch, args.variant, args.precision)
+        games = per_game(pb, torch, with_oracle=not args.no_cpu)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.cpu_sample_types, variant, args.precision, args.cpu_seconds, game.V)
@@ -349,14 +492,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None, "dtype": f"f{args.precision}", "data": "synthetic",
-            "config": {"workload": f"synthetic_n{args.n_types}: {game.V:,} nodes, D={game.D}, {game.H:,} infosets, "
-                                   f"{game.Q:,} (h,a) pairs (BASELINE.json configs[4], single GPU)",
-                       "variant": args.variant, "precision": f"f{args.precision}",
-                       "parallelism": "single GPU" if world == 1 else
-                       f"level-sharded x{world} (cut depth {solver.shard_info()['cut']}, NCCL exchanges)",
-                       "l2": "no flush: per-iteration working set ~13 GB >> 126 MB L2",
-                       "setup_s": {"generate": round(t_gen, 1), "flatten": round(t_flat, 1),
-                                   "upload": round(t_up, 1)}},
+            "config": config_of(args, game.V, game.D, game.H, game.Q),
+            "parallelism": "single GPU" if world == 1 else
+            f"level-sharded x{world} (cut depth {shard_cut}, NCCL exchanges)",
+            "l2": "no flush: per-iteration working set ~12 GB >> 126 MB L2",
+            "setup_s": {"generate": round(t_gen, 1), "flatten": round(t_flat, 1), "upload": round(t_up, 1),
+                        "note": "one-time setup (PAPER.md P:397, Table 9), outside the timed region"},
             "node_updates_per_s": float(f"{game.V * value:.4g}"),
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -364,7 +505,10 @@ def main():
             "gpu_launches": int(launches * args.steps),
             "launches_per_step": launches,
             "clocks": clk,
+            "synthetic_variants": variants,
             "per_game": games,
+            "host": host_info(),
+            "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -55,3 +55,19 @@ def test_zero_sum_fixtures():
         d = gamegen.by_name(name)
         t = d.player < 0
         assert np.array_equal(d.utility[t, 1], -d.utility[t, 0])
+
+
+@pytest.mark.parametrize("name", ["battleship0", "battleship1", "battleship2", "battleship3", "battleship4",
+                                  "battleship5", "battleship6", "battleship7", "battleship8", "battleship11"])
+def test_battleship_table7_counts(name):
+    """PAPER.md Table 7: nodes, terminals and infosets of the
+    Experiment 2 battleship games, exactly (generator rules: DESIGN.md Q20)."""
+    from gamegen.battleship import PAPER_CONFIGS, paper_battleship
+
+    want = PAPER_CONFIGS[name][1]
+    d = paper_battleship(name)
+    assert (d.num_nodes, int((d.player == -1).sum()), d.num_infosets) == want[:3]
+    assert d.utility.shape == (d.num_nodes, 2)
+    # sanity of the general-sum payoffs (ship values 1, loss multiplier 2)
+    term = d.player == -1
+    assert set(np.unique(d.utility[term, 0])) <= {1.0, 0.0, -2.0, -1.0, 2.0, -4.0, -3.0, -5.0, -6.0, 3.0}
