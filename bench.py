@@ -168,10 +168,17 @@ GAME_LINES = (
     ("goofspiel", "cfr+", 64, 2000, 500),     # configs[3]
     ("goofspiel", "cfr+", 32, 2000, 500),
     ("goofspiel6", "cfr+", 64, 300, 10),
+    ("battleship7", "cfr", 64, 300, 10),      # PAPER.md Experiment 2
+    ("battleship7", "cfr", 32, 300, 10),
+    ("battleship11", "cfr", 64, 100, 2),      # the paper's largest game
+    ("battleship11", "cfr", 32, 100, 2),
 )
 # PAPER.md Table 2, vanilla CFR, RTX 4090 + CuPy, mean ms per iteration
 PAPER_MS = {("kuhn", 64): 3.319, ("kuhn", 32): 3.362, ("leduc", 64): 6.269, ("leduc", 32): 6.178,
-            ("liars_dice", 64): 10.766, ("liars_dice", 32): 8.443}
+            ("liars_dice", 64): 10.766, ("liars_dice", 32): 8.443,
+            # Table 5, 10 iterations
+            ("battleship7", 64): 38.554, ("battleship7", 32): 20.437,
+            ("battleship11", 64): 856.541, ("battleship11", 32): 446.369}
 
 
 def host_info():
@@ -201,6 +208,10 @@ class pinned_core:
 
 
 def game_desc(name: str):
+    if name.startswith("battleship"):
+        from gamegen.battleship import paper_battleship
+
+        return paper_battleship(name)
     return gamegen.goofspiel(6) if name == "goofspiel6" else gamegen.by_name(name)
 
 
@@ -238,8 +249,9 @@ def per_game(pb, torch, with_oracle: bool):
             del o
         pm = PAPER_MS.get((name, prec))
         if pm is not None:
-            e["paper_context"] = {"it_per_s": round(1e3 / pm, 1), "variant": "cfr",
-                                  "hardware": "RTX 4090 + CuPy (PAPER.md Table 2, P:426)"}
+            e["paper_context"] = {"it_per_s": round(1e3 / pm, 2), "variant": "cfr",
+                                  "hardware": "RTX 4090 + CuPy (PAPER.md Table 2 P:426 / Table 5 P:570)",
+                                  "ratio": round(e["it_per_s"] * pm / 1e3, 1)}
         out.append(e)
         del g
     return out

@@ -125,10 +125,10 @@ typedef struct {
                          /* DCFR, CFR+ with alternating updates                    */
     int32_t precision;   /* 64 (binary64) or 32 (binary32) working precision      */
     int32_t flags;       /* bit 0: disable CUDA-Graph capture (debug);            */
-                         /* bit 1: run small games (<= 2^22 nodes) as ONE         */
-                         /* cooperative launch per enqueue (k_persist, grid      */
-                         /* barriers between levels; measured slower than the    */
-                         /* PDL graph on B200); bit 2: disable the pipelined     */
+                         /* bit 1: reserved -- the cooperative single-launch     */
+                         /* kernel it selected was removed (slower than the PDL  */
+                         /* graph on B200): CFR_ERR_UNSUPPORTED; bit 2: disable  */
+                         /* the pipelined                                        */
                          /* (persistent) backward kernel; bit 3: disable          */
                          /* programmatic dependent launch; bit 4: disable the     */
                          /* streaming (TMA) backward kernel (A/B comparisons);    */
@@ -144,7 +144,7 @@ typedef struct {
 } cfr_solver_config;
 
 #define CFR_FLAG_NO_GRAPH 1
-#define CFR_FLAG_PERSISTENT 2
+#define CFR_FLAG_PERSISTENT 2   /* reserved: rejected with CFR_ERR_UNSUPPORTED */
 #define CFR_FLAG_NO_PIPELINE 4
 #define CFR_FLAG_NO_PDL 8
 #define CFR_FLAG_NO_STREAM 16

@@ -433,10 +433,11 @@ int compute_E(const Game& g) {
         if (g.player[v] < 0)
             for (int j = 0; j < g.P; ++j) m = std::max(m, std::fabs((double)(R)g.util[v * g.P + j]));
     if (m == 0.0) return 1;
+    // ceil(log2(2m)) = 1 + ceil(log2 m), taken on m (2m overflows above DBL_MAX / 2)
     int e;
-    const double f = std::frexp(2.0 * m, &e);   // 2m = f * 2^e, f in [0.5, 1)
+    const double f = std::frexp(m, &e);   // m = f * 2^e, f in [0.5, 1)
     const int ceil_log2 = (f == 0.5) ? e - 1 : e;
-    return 1 + ceil_log2;
+    return 2 + ceil_log2;
 }
 
 }  // namespace

@@ -34,13 +34,13 @@ bool fail(std::string& err, const std::string& m) {
     return false;
 }
 
-// E = 1 + ceil(log2(2*m)) for m > 0, else 1.  ilogb-based.
+// E = 1 + ceil(log2(2*m)) = 2 + ceil(log2 m) for m > 0, else 1,
+// evaluated on m itself: 2*m overflows for m > DBL_MAX / 2.  ilogb-based.
 int exponent_for(double m) {
     if (!(m > 0.0)) return 1;
-    const double x = 2.0 * m;
-    int k = std::ilogb(x);                 // floor(log2 x) for normal x
-    if (std::ldexp(1.0, k) < x) k += 1;    // ceil
-    return 1 + k;
+    int k = std::ilogb(m);                 // floor(log2 m) for normal m
+    if (std::ldexp(1.0, k) < m) k += 1;    // ceil
+    return 2 + k;
 }
 
 }  // namespace

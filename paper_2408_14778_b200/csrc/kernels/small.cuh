@@ -1,72 +1,8 @@
-// Small-game kernels: k_persist (cooperative, opt-in) and k_tiny (one CTA, shared memory).
+// Small-game kernel: k_tiny (one CTA, shared memory, T iterations per launch).
 // Part of the single translation unit solver.cu (included from it only).
 #pragma once
 
 namespace cfrb {
-
-// --------------------------------------------------- persistent iteration
-// Small games are launch-latency bound (2D kernels per iteration).  k_persist runs
-// T whole iterations in ONE cooperative launch: every CTA is resident; the levels
-// of an iteration are separated by grid-wide barriers (the same forward, tile and
-// deferred bodies as the per-level kernels, so the arithmetic is identical).
-struct PLevel {
-    long long s0, s1;   // slots of depth l (forward pass of level l)
-    long long t0, t1;   // tiles of parent depth L (backward pass)
-    SmemLayout lay;     // tile shared-memory layout of depth L
-};
-
-// Sense-free grid barrier: bar[0] arrivals, bar[1] generation.  Thread 0 arrives
-// after a gpu-scope fence (the block's writes are visible) and leaves after one
-// (other blocks' writes are visible to the block, L1 included).
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* gen = bar + 1;
-        const unsigned g0 = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g0) __nanosleep(32);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-template <class R, class I, int PC, int PT>
-__global__ void __launch_bounds__(kTileSlots) k_persist(DG<R, I> g, const PLevel* __restrict__ lv, int D, int has_def,
-                                                         long long T, unsigned* bar) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    long long t_done = g.ctrl[0];
-    for (long long it = 0; it < T; ++it) {
-        for (int l = 1; l < D; ++l) {   // forward pass, depth 1 .. D-1
-            const long long s0 = lv[l].s0, s1 = lv[l].s1;
-            if (s1 <= s0) continue;
-            fwd_body<R, I, PT>(g, g.sig, s0, s1, 0);
-            grid_sync(bar);
-        }
-        for (int L = D - 1; L >= 0; --L) {   // backward pass, parent depth D-1 .. 0
-            const long long t0 = lv[L].t0, t1 = lv[L].t1;
-            if (t1 <= t0) continue;
-            const SmemLayout lay = lv[L].lay;
-            for (long long t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
-                __syncthreads();   // the previous tile's shared-memory reads are done
-                bwd_tile<R, I, PC, MODE_CFR>(g, g.sig, t, 0, 0, lay, smem_raw);
-            }
-            grid_sync(bar);
-        }
-        if (has_def) {
-            deferred_body<R, I>(g, 0);
-            grid_sync(bar);
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) g.ctrl[0] = ++t_done;   // the iteration is complete
-        else ++t_done;
-        grid_sync(bar);
-    }
-}
 
 // ------------------------------------------------------------- tiny games
 // Games whose whole mutable state fits in one CTA's shared memory (Kuhn; Leduc in
@@ -114,7 +50,7 @@ __global__ void __launch_bounds__(1024) k_tiny(DG<R, I> g, const TinyLevel* __re
     for (long long k = tid; k < tp.H; k += nth) sden[k] = g.sden[k];
     __syncthreads();
     long long t_iter = g.ctrl[0];
-    bool bad = false;
+    long long bad = LLONG_MAX;   // first iteration of this launch with a non-finite value
     for (long long it = 0; it < T; ++it) {
         ++t_iter;
         const Upd<R> up = make_upd<R>(g.variant, t_iter);
@@ -210,7 +146,7 @@ __global__ void __launch_bounds__(1024) k_tiny(DG<R, I> g, const TinyLevel* __re
                             const R pos = (r > (R)0) ? r : (R)0;
                             const R nsig = (z > (R)0) ? pos / z : (R)1 / (R)n;
                             sig[q] = nsig;
-                            if (!finite_(rtb[q]) || !finite_(nsig) || !finite_(z)) bad = true;
+                            if (!finite_(rtb[q]) || !finite_(nsig) || !finite_(z)) bad = min(bad, t_iter);
                         }
                     }
                 }
@@ -228,7 +164,7 @@ __global__ void __launch_bounds__(1024) k_tiny(DG<R, I> g, const TinyLevel* __re
         g.snum[k] = snum[k];
     }
     for (long long k = tid; k < tp.H; k += nth) g.sden[k] = sden[k];
-    if (bad) atomicMin(&g.ctrl[1], t_iter);
+    if (bad != LLONG_MAX) atomicMin(&g.ctrl[1], bad);
     if (tid == 0) g.ctrl[0] = t_iter;
 }
 

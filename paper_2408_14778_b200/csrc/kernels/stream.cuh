@@ -36,10 +36,22 @@ struct StreamLevel {
     int o_sv, o_cm, o_rt, o_pos, o_pib, o_zs, o_ccnt, o_bar;          // work arrays / barriers
     int bytes;              // dynamic shared memory
     int last;
-    int debug;              // timing experiments only: 1 consumers skip compute, 2 producer skips loads
+    int debug;              // timing experiments only (CFR_STREAM_EXPERIMENTS builds): 1 consumers skip
+                            // compute, 2 producer skips loads, 4/8/16/32 skip value writes / updates /
+                            // value loop / compaction
     int level;              // parent level (work counters)
     int compact;            // 1: reach rows of this level are compact (pi_check, pi_hat of the actor; k_fwd compact)
+    int defer;              // 1: every infoset of the level is deferred (spans ranks): exact partial sums are
+                            //    added to the exchange block acc_r / acc_p; the update runs after the all-reduce
+    long long dh0, dq0;     // defer: deferred index of the level's first infoset, its compact pair base
 };
+// The timing-experiment knobs (StreamLevel::debug) exist only in experiment
+// builds (-DCFR_STREAM_EXPERIMENTS); the product build compiles them out.
+#ifdef CFR_STREAM_EXPERIMENTS
+#define STREAM_DEBUG(L) ((L).debug)
+#else
+#define STREAM_DEBUG(L) 0
+#endif
 constexpr int kStreamConsumers = 256;   // 8 consumer warps
 constexpr int kStreamThreads = kStreamConsumers + 32;   // + 1 producer warp
 
@@ -200,7 +212,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 hd->rro = o_reach;
                 (void)po2; (void)po3;   // sigma / R / S_num share the pair window offset (same base alignment)
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                if (L.debug == 2) {   // timing experiment: no loads (consumers compute on stale data)
+                if (STREAM_DEBUG(L) == 2) {   // timing experiment: no loads (consumers compute on stale data)
                     mbar_expect_tx(&full[st], 0);
                 } else {
                     mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs + b_node + b_pact);
@@ -305,7 +317,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         const R* gsig = reinterpret_cast<const R*>(S + L.o_gsig);                                  // fused only
         const int nseg = hd.nseg, M = hd.M, m0 = hd.m0;
 
-        if (L.debug == 1) {   // timing experiment: data movement only
+        if (STREAM_DEBUG(L) == 1) {   // timing experiment: data movement only
             consumers_sync();
             if (tid == 0) mbar_arrive(&empty[st]);
             if (++st == L.stages) { st = 0; ++ph; }
@@ -339,7 +351,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 for (int j = 0; j < PC; ++j) v[j] = (R)0;
                 const R* row = rows + (long long)m * L.rowlen;
                 const R* sg = ssig + k * n;
-                if (L.debug & 16) {   // timing experiment: no value loop
+                if (STREAM_DEBUG(L) & 16) {   // timing experiment: no value loop
                 } else if (PC == 1 && vec_rows) {
                     // 16-byte row reads (vec_rows: rows 16-byte aligned in the stage)
                     using V = typename std::conditional<sizeof(R) == 8, double2, float4>::type;
@@ -395,7 +407,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 SPROF(2);
 #pragma unroll
                 for (int j = 0; j < PC; ++j) {
-                    if (!(L.debug & 4)) g.U[node * PC + j] = v[j];   // (debug bit 4: timing experiment)
+                    if (!(STREAM_DEBUG(L) & 4)) g.U[node * PC + j] = v[j];   // (debug bit 4: timing experiment)
                     sv[m * PC + j] = v[j];
                 }
                 const int i = own[k];
@@ -417,7 +429,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 }
             }
             SPROF(3);
-            if (L.debug & 32) continue;   // timing experiment: no compaction
+            if (STREAM_DEBUG(L) & 32) continue;   // timing experiment: no compaction
             // a warp whose members all have zero reach has nothing to compact
             if (__ballot_sync(0xffffffffu, active && (pc != (R)0 || ph != (R)0)) == 0u) continue;
             const int key = active ? k : -1;
@@ -449,9 +461,12 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         const long long ht = L.h0 + hd.k0;
         {
             const int warp = tid >> 5;
+            // (a deferred infoset contributes only nonzero partial sums; its update
+            // runs after the exchange)
             const unsigned live = __ballot_sync(
-                0xffffffffu, lane < nseg && (g.upd_player == 0 || own[lane] == g.upd_player) &&
-                                 (all_live || ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0));
+                0xffffffffu, lane < nseg && (L.defer ? (ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0)
+                                                     : (g.upd_player == 0 || own[lane] == g.upd_player) &&
+                                                           (all_live || ccnt[lane] != 0 || ccnt[L.maxseg + lane] != 0)));
             if (tid == 0) {
                 live_h += __popc(live);
                 all_h += nseg;
@@ -509,12 +524,22 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                         c1 += __shfl_xor_sync(0xffffffffu, c1, o);
                         c2 += __shfl_xor_sync(0xffffffffu, c2, o);
                     }
-                    if (part == 0) {
+                    if (L.defer) {
+                        // exact partial sums of this rank's members (int64 slices, any order)
+                        if (part == 0 && itm <= n && (c0 != 0.0 || c1 != 0.0 || c2 != 0.0)) {
+                            unsigned long long* acc = (itm < n) ? g.acc_r + (L.dq0 + (long long)(hd.k0 + k) * n + itm) * 3
+                                                                : g.acc_p + (L.dh0 + hd.k0 + k) * 3;
+                            atomicAdd(acc + 0, (unsigned long long)(long long)c0);
+                            atomicAdd(acc + 1, (unsigned long long)(long long)c1);
+                            atomicAdd(acc + 2, (unsigned long long)(long long)c2);
+                        }
+                    } else if (part == 0) {
                         if (itm < n) rt[k * n + itm] = (R)xdec(c0, c1, c2, g.rc);
                         else if (itm == n) pib[k] = (R)xdec(c0, c1, c2, g.rcp);
                     }
                 }
                 __syncwarp();
+                if (L.defer) continue;   // updated by k_deferred after the exchange
                 // ---- phase C: Eq 8/15 or CFR+, Eq 10, then Eq 9 (z ascending)
                 const R wp = w * pib[k];
                 for (int c = 0; c < n; c += 32) {
@@ -523,7 +548,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                         const int p = k * n + a;
                         const R r_t = rt[p];
                         const R r = upd_regret(up, sreg[p], r_t);   // Eq 8/15 (Q4) / CFR+ (Q6) / Q18
-                        if (!(L.debug & 8)) {   // (debug bit 8: timing experiment)
+                        if (!(STREAM_DEBUG(L) & 8)) {   // (debug bit 8: timing experiment)
                             g.regret[qt + p] = r;
                             g.snum[qt + p] = upd_sum(up, ssn[p], wp * ssig[p]);  // Eq 10 numerator
                         }
@@ -535,13 +560,13 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 const R* pk = pos + k * n;
 #pragma unroll 4
                 for (int b = 0; b < n; ++b) z = z + pk[b];   // broadcast reads, ascending
-                if (lane == 0 && !(L.debug & 8)) g.sden[ht + k] = upd_sum(up, sden[k], wp);   // Eq 10 denominator
+                if (lane == 0 && !(STREAM_DEBUG(L) & 8)) g.sden[ht + k] = upd_sum(up, sden[k], wp);   // Eq 10 denominator
                 for (int c = 0; c < n; c += 32) {
                     const int a = c + lane;
                     if (a < n) {
                         const int p = k * n + a;
                         const R nsig = (z > (R)0) ? pos[p] / z : inv_n;   // Eq 9
-                        if (!(L.debug & 8)) g.sig[qt + p] = nsig;
+                        if (!(STREAM_DEBUG(L) & 8)) g.sig[qt + p] = nsig;
                         if (!finite_(rt[p]) || !finite_(nsig) || !finite_(z)) bad = true;
                     }
                 }

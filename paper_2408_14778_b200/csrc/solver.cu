@@ -285,7 +285,7 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int ix, int stages
 template <class R, class I>
 static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<int64_t>& cb_u, std::vector<int>* pool,
                                               int min_tiles, int stages, int tile_target, bool fuse_forward,
-                                              bool compact_reach) {
+                                              bool compact_reach, const std::vector<uint8_t>& contrib) {
     const int w = (int)sizeof(R), P = g.P, Pc = g.Pc, ix = (int)sizeof(I);
     std::vector<StreamLevel> out(g.D, StreamLevel{});
     for (int L = 0; L < g.D; ++L) {
@@ -296,13 +296,22 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         std::vector<int> hs;
         int64_t h_prev = -1, next = s0;
         int n = -1;
+        // every infoset of the level fused (updated here), or every one deferred
+        // (spanning ranks: exact partial sums into the exchange block, updated
+        // after the all-reduce) with consecutive deferred indices; a deferred
+        // level must lie below the cut (every tile contributes)
+        int mode = -1;   // 0 fused, 1 deferred
         for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1] && ok; ++t)
             for (int k = g.tiles[t].seg0; k < g.tiles[t].seg1 && ok; ++k) {
                 const SegH& sg = g.segs[k];
                 const int nn = (int)(g.qbase_int[sg.h + 1] - g.qbase_int[sg.h]);
-                if (!sg.fused || sg.sb != next || (h_prev >= 0 && sg.h != h_prev + 1) || (n >= 0 && nn != n) ||
-                    sg.se - sg.sb > tile_target)
+                const int m = sg.fused ? 0 : (g.deferred[sg.h] ? 1 : 2);
+                if (m == 2 || (mode >= 0 && m != mode) || sg.sb != next || (h_prev >= 0 && sg.h != h_prev + 1) ||
+                    (n >= 0 && nn != n) || sg.se - sg.sb > tile_target)
                     ok = false;
+                if (m == 1 && h_prev >= 0 && g.dpos[sg.h] != g.dpos[h_prev] + 1) ok = false;
+                if (m == 1 && !contrib.empty() && !contrib[t]) ok = false;
+                mode = m;
                 n = nn;
                 hs.push_back((int)(sg.sb - s0));
                 h_prev = sg.h;
@@ -331,6 +340,11 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         f.s0 = s0;
         f.h0 = g.segs[g.tiles[g.tile_ptr[L]].seg0].h;
         f.q0 = g.qbase_int[f.h0];
+        f.defer = mode == 1 ? 1 : 0;
+        if (f.defer) {
+            f.dh0 = g.dpos[f.h0];
+            f.dq0 = g.dqbase[f.dh0];
+        }
         f.row0 = row0;
         f.n = n;
         f.rowlen = n * Pc;
@@ -419,7 +433,7 @@ struct Plan {
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, br_best, ctrl, lcnt, out, rec;
-    size_t cutbuf, cutrow, cutown, report, pool, spool, plev, gbar, tlev, tmem_of;
+    size_t cutbuf, cutrow, cutown, report, pool, spool, tlev, tmem_of;
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
         Layout L;
@@ -461,8 +475,6 @@ struct Plan {
         report = L.take<unsigned char>(H + 1);
         pool = L.take<unsigned char>(fast_pool_bytes<R, I>(g, sh) + 16);
         spool = L.take<int>(stream_pool_bound(g));
-        plev = L.take<PLevel>((size_t)g.D + 1);
-        gbar = L.take<unsigned>(4);
         tlev = L.take<TinyLevel>((size_t)g.D + 1);
         tmem_of = L.take<I>(g.V <= (int64_t(1) << 20) ? 2 * H + 2 : 2);
         rec = L.take<double>((size_t)kRecRows * rec_width(g));
@@ -492,10 +504,8 @@ struct Solver final : SolverBase {
     int E = 1;
     int64_t launches_per_iter = 0;
     bool use_graph = true;
-    bool persist_ = false;        // small game: whole iterations in one cooperative launch (k_persist)
     bool tiny_ = false;           // tiny game: whole iterations in one CTA, state in shared memory (k_tiny)
     TinyPlan tiny_plan_{};
-    int persist_grid_ = 0, persist_smem_ = 0;
     bool use_fast_ = true;
     bool use_stream_ = true;
     int stream_debug_ = 0;   // CFR_STREAM_DEBUG (timing experiments; results are garbage when set)
@@ -511,10 +521,23 @@ struct Solver final : SolverBase {
         rank = sh->rank;
     }
 
+    // NCCL mode: exchange 2 per level, overlapped with the shallower levels.  A
+    // deferred infoset's sums are complete once its shallowest level is done
+    // (levels run deep -> shallow); internal ids are assigned level by level, so
+    // the deferred infosets first seen at level L are one contiguous range of
+    // deferred indices [xr_[L].first, xr_[L].second).
+    std::vector<std::pair<int64_t, int64_t>> xr_;
+    cudaStream_t xstream_ = nullptr;          // the communication stream
+    std::vector<cudaEvent_t> xev_;            // fork / join events (2 per level + 1)
+
     ~Solver() override {
         // the workspace belongs to the caller: no kernel may still run on it once
         // the handle is gone (the caller frees it after cfr_solver_destroy)
         cudaStreamSynchronize(stream);
+        if (xstream_) cudaStreamSynchronize(xstream_);
+        for (cudaEvent_t e : xev_) cudaEventDestroy(e);
+        if (xstream_) cudaStreamDestroy(xstream_);
+
         if (pinned_) cudaFreeHost(pinned_);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (eval_exec_) cudaGraphExecDestroy(eval_exec_);
@@ -619,6 +642,42 @@ struct Solver final : SolverBase {
             } else {
                 external = true;   // the caller performs the two exchanges (cfr_solver_phase)
             }
+        }
+        if (comm) {
+            // deferred-index range of the infosets first seen at each level
+            xr_.assign(g.D, std::make_pair((int64_t)0, (int64_t)0));
+            std::vector<int> first(g.H, INT32_MAX);
+            for (int L = 0; L < g.D; ++L)
+                for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1]; ++t)
+                    for (int k = g.tiles[t].seg0; k < g.tiles[t].seg1; ++k)
+                        first[g.segs[k].h] = std::min(first[g.segs[k].h], L);
+            std::vector<int64_t> lo(g.D, INT64_MAX), hi(g.D, -1);
+            for (size_t d = 0; d < g.deferred_list.size(); ++d) {
+                const int L = first[g.deferred_list[d]];
+                if (L == INT32_MAX) continue;
+                lo[L] = std::min(lo[L], (int64_t)d);
+                hi[L] = std::max(hi[L], (int64_t)d + 1);
+            }
+            int64_t next = 0;
+            bool contiguous = true;
+            for (int L = 0; L < g.D; ++L) {   // shallow -> deep: ranges must tile [0, ndef) in order
+                if (hi[L] < 0) continue;
+                if (lo[L] != next || hi[L] - lo[L] <= 0) contiguous = false;
+                xr_[L] = std::make_pair(lo[L], hi[L]);
+                next = hi[L];
+            }
+            if (!contiguous || next != (int64_t)g.deferred_list.size()) xr_.clear();   // one exchange after the pass
+            if (!xr_.empty()) {
+                CU(cudaStreamCreateWithFlags(&xstream_, cudaStreamNonBlocking));
+                xev_.resize(2 * g.D + 2);
+                for (cudaEvent_t& e : xev_) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+        }
+
+        if (cfg.flags & CFR_FLAG_PERSISTENT) {
+            cfrb_set_error("CFR_FLAG_PERSISTENT (the cooperative single-launch kernel) was removed: measured slower "
+                           "than the CUDA-graph iteration on B200; tiny games use k_tiny (DESIGN.md 6.1)");
+            return CFR_ERR_UNSUPPORTED;
         }
         if (g.Pc > 4) {
             cfrb_set_error("non-zero-sum games with more than 4 players are not supported by the device kernels");
@@ -767,13 +826,16 @@ struct Solver final : SolverBase {
             std::vector<int> sp;
             int stages = 2;
             if (const char* e = std::getenv("CFR_STREAM_STAGES")) stages = std::max(2, std::min(8, std::atoi(e)));
+#ifdef CFR_STREAM_EXPERIMENTS
             if (const char* e = std::getenv("CFR_STREAM_DEBUG")) stream_debug_ = std::atoi(e);
+#endif
             // members per tile: ~240 f64 / ~480 f32 keeps two CTAs (2-stage rings of
             // ~50 KB) resident per SM (measured best, tools/stream_sweep.py)
             int tile = (sizeof(R) == 4 && !(cfg.flags & CFR_FLAG_FUSED_FORWARD)) ? 2 * kStreamConsumers : kStreamConsumers;
             if (const char* e = std::getenv("CFR_STREAM_TILE")) tile = std::max(32, std::min(1024, std::atoi(e)));
             stream_ = stream_levels<R, I>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages, tile,
-                                          (cfg.flags & CFR_FLAG_FUSED_FORWARD) != 0, std::getenv("CFR_NO_COMPACT") == nullptr);
+                                          (cfg.flags & CFR_FLAG_FUSED_FORWARD) != 0, std::getenv("CFR_NO_COMPACT") == nullptr,
+                                          tile_contrib_);
             if (sp.size() > stream_pool_bound(g)) {
                 cfrb_set_error("internal: stream table bound");
                 return CFR_ERR_INVALID_ARG;
@@ -888,9 +950,8 @@ struct Solver final : SolverBase {
         }
         launches_per_iter = count_launches();
         {
-            cfr_status ps = setup_persistent();
+            cfr_status ps = setup_tiny();
             if (ps) return ps;
-            if ((ps = setup_tiny())) return ps;
         }
         if (use_graph && g.NS > 0 && !external) {
             CU(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
@@ -934,68 +995,6 @@ struct Solver final : SolverBase {
         return e;
     }
 
-    // Persistent mode for small games (opt-in, CFR_FLAG_PERSISTENT): one cooperative
-    // launch runs T iterations (k_persist).  Measured slower than the PDL graph on
-    // B200 (Kuhn 36.6 vs 24.6 us/it, Leduc 134 vs 108): each level's dependent
-    // global-memory chain, not the launch, dominates.  Off for sharded solvers.
-    static constexpr int64_t kPersistMaxNodes = int64_t(1) << 22;
-    cfr_status setup_persistent() {
-        const Game& g = *gp;
-        persist_ = false;
-        if (world > 1 || external || !(cfg.flags & CFR_FLAG_PERSISTENT) || g.NS == 0 || g.V > kPersistMaxNodes ||
-            cfg.variant == CFR_PLUS_ALT)
-            return CFR_OK;
-        int dev = 0, coop = 0;
-        CU(cudaGetDevice(&dev));
-        CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-        if (!coop) return CFR_OK;
-        std::vector<PLevel> lv(g.D + 1);
-        long long max_units = 1;
-        for (int l = 0; l < g.D; ++l) {
-            lv[l].s0 = g.slot_ptr[l];
-            lv[l].s1 = g.slot_ptr[l + 1];
-            lv[l].t0 = g.tile_ptr[l];
-            lv[l].t1 = g.tile_ptr[l + 1];
-            lv[l].lay = lay_[l];
-            max_units = std::max<long long>(max_units, lv[l].t1 - lv[l].t0);
-            max_units = std::max<long long>(max_units, (lv[l].s1 - lv[l].s0 + 1023) / 1024);
-        }
-        persist_smem_ = std::max(16, max_smem_);
-        void* fn = persist_fn();
-        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, persist_smem_));
-        int per_sm = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kTileSlots, persist_smem_));
-        if (per_sm < 1) return CFR_OK;
-        persist_grid_ = (int)std::min<long long>((long long)num_sms_ * per_sm, max_units);
-        cfr_status st = up(plan.plev, lv);
-        if (st) return st;
-        CU(cudaMemsetAsync(ws + plan.gbar, 0, 4 * sizeof(unsigned), stream));
-        CU(cudaStreamSynchronize(stream));
-        persist_ = true;
-        return CFR_OK;
-    }
-    void* persist_fn() const {
-        const int Pc = gp->Pc;
-        const bool p2 = gp->P == 2;
-        switch (Pc) {
-            case 1: return p2 ? (void*)k_persist<R, I, 1, 2> : (void*)k_persist<R, I, 1, 0>;
-            case 2: return p2 ? (void*)k_persist<R, I, 2, 2> : (void*)k_persist<R, I, 2, 0>;
-            case 3: return p2 ? (void*)k_persist<R, I, 3, 2> : (void*)k_persist<R, I, 3, 0>;
-            default: return p2 ? (void*)k_persist<R, I, 4, 2> : (void*)k_persist<R, I, 4, 0>;
-        }
-    }
-    cfr_status launch_persistent(int64_t iters) {
-        const Game& g = *gp;
-        const PLevel* lv = at<PLevel>(plan.plev);
-        int D = g.D;
-        int has_def = has_def_() ? 1 : 0;
-        long long T = (long long)iters;
-        unsigned* bar = at<unsigned>(plan.gbar);
-        void* args[] = {(void*)&dg, (void*)&lv, (void*)&D, (void*)&has_def, (void*)&T, (void*)&bar};
-        CU(cudaLaunchCooperativeKernel(persist_fn(), dim3(persist_grid_), dim3(kTileSlots), args, (size_t)persist_smem_,
-                                       stream));
-        return CFR_OK;
-    }
     bool has_def_() const { return !gp->deferred_list.empty(); }
 
     void* tiny_fn() const {
@@ -1011,7 +1010,7 @@ struct Solver final : SolverBase {
     cfr_status setup_tiny() {
         const Game& g = *gp;
         tiny_ = false;
-        if (world > 1 || external || persist_ || (cfg.flags & CFR_FLAG_NO_TINY) || !g.depth_homogeneous || g.NS == 0)
+        if (world > 1 || external || (cfg.flags & CFR_FLAG_NO_TINY) || !g.depth_homogeneous || g.NS == 0)
             return CFR_OK;
         const long long nU = (long long)(plan_u_rows()) * g.Pc, nreach = 2LL * g.P * g.NS, nsig = g.Q + g.C;
         int dev = 0, optin = 0;
@@ -1238,6 +1237,7 @@ struct Solver final : SolverBase {
             else if (mode == MODE_VALUES) bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
             else bwd_level<MODE_BR>(st, sig, L, br_player, 0);
             mark(st, ev, 1, L);
+            if (mode == MODE_CFR && overlap_exchange()) xchg_level(st, L);
         }
         if (sharded()) {
             const long long n = ncut();
@@ -1245,6 +1245,30 @@ struct Solver final : SolverBase {
             k_cut_pack<R><<<nb, 256, 0, st>>>(dg.U, at<long long>(plan.cutrow), at<unsigned char>(plan.cutown),
                                               at<R>(plan.cutbuf), n, g.Pc);
         }
+    }
+    // exchange 2 of the infosets first seen at level L on the communication
+    // stream, forked from `st` after level L's backward kernel (NCCL issues the
+    // per-level calls in the same order on every rank: the level schedule is
+    // identical).  Returns the NCCL status through xstatus_.
+    cfr_status xstatus_ = CFR_OK;
+    int xforks_ = 0;
+    bool overlap_exchange() const { return comm && xstream_ && world > 1 && has_def(); }
+    void xchg_level(cudaStream_t st, int L) {
+        const int64_t d0 = xr_[L].first, d1 = xr_[L].second;
+        if (d1 <= d0) return;
+        cudaEvent_t e = xev_[xforks_++ % xev_.size()];
+        cudaEventRecord(e, st);
+        cudaStreamWaitEvent(xstream_, e, 0);
+        const int64_t q0 = gp->dqbase[d0], q1 = gp->dqbase[d1];
+        cfr_status s = nccl_sum(xstream_, dg.acc_r + 3 * q0, (size_t)(3 * (q1 - q0)), ncclInt64);
+        if (!s) s = nccl_sum(xstream_, dg.acc_p + 3 * d0, (size_t)(3 * (d1 - d0)), ncclInt64);
+        if (s && !xstatus_) xstatus_ = s;
+    }
+    // join: `st` waits for every exchange issued on the communication stream
+    void xchg_join(cudaStream_t st) {
+        cudaEvent_t e = xev_.back();
+        cudaEventRecord(e, xstream_);
+        cudaStreamWaitEvent(st, e, 0);
     }
     void launch_upper(cudaStream_t st, int mode, const R* sig, std::vector<Mark>* ev, int br_player = 0) {
         const Game& g = *gp;
@@ -1258,6 +1282,7 @@ struct Solver final : SolverBase {
             else if (mode == MODE_VALUES) bwd_level<MODE_VALUES>(st, sig, L, 0, 0);
             else bwd_level<MODE_BR>(st, sig, L, br_player, 0);
             mark(st, ev, 1, L);
+            if (mode == MODE_CFR && overlap_exchange()) xchg_level(st, L);
         }
     }
     void launch_update(cudaStream_t st, std::vector<Mark>* ev) {
@@ -1286,18 +1311,36 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         cfr_status s = CFR_OK;
         const int passes = (cfg.variant == CFR_PLUS_ALT) ? g.P : 1;
+        xstatus_ = CFR_OK;
         mark(st, ev, -1, 0);
         for (int pass = 1; pass <= passes && !s; ++pass) {
             dg.upd_player = (passes > 1) ? pass : 0;
             pass_final_ = (pass == passes) ? 1 : 0;
             launch_lower(st, MODE_CFR, dg.sig, ev);
             if (sharded()) {
-                if ((s = nccl_sum(st, at<R>(plan.cutbuf), (size_t)ncut() * g.Pc, rtype()))) break;
+                if (overlap_exchange()) {
+                    // every NCCL call of the iteration goes through the one
+                    // communication stream, in issue order (no two collectives of
+                    // the communicator in flight on different streams)
+                    cudaEvent_t e = xev_[xforks_++ % xev_.size()];
+                    cudaEventRecord(e, st);
+                    cudaStreamWaitEvent(xstream_, e, 0);
+                    if ((s = nccl_sum(xstream_, at<R>(plan.cutbuf), (size_t)ncut() * g.Pc, rtype()))) break;
+                    xchg_join(st);
+                } else if ((s = nccl_sum(st, at<R>(plan.cutbuf), (size_t)ncut() * g.Pc, rtype()))) {
+                    break;
+                }
                 mark(st, ev, 3, -1);
                 launch_upper(st, MODE_CFR, dg.sig, ev);
             }
             if (world > 1 && has_def()) {
-                if ((s = nccl_sum(st, dg.acc_r, acc_bytes() / 8, ncclInt64))) break;
+                if (overlap_exchange()) {
+                    // the per-level exchanges ran on the communication stream
+                    if ((s = xstatus_)) break;
+                    xchg_join(st);
+                } else if ((s = nccl_sum(st, dg.acc_r, acc_bytes() / 8, ncclInt64))) {
+                    break;
+                }
                 mark(st, ev, 3, -1);
             }
             launch_update(st, ev);
@@ -1315,7 +1358,6 @@ struct Solver final : SolverBase {
             cfrb_set_error("world_size > 1 without an NCCL id: drive the iteration with cfr_solver_phase");
             return CFR_ERR_UNSUPPORTED;
         }
-        if (persist_ && iters > 0) return launch_persistent(iters);
         if (tiny_ && iters > 0) return launch_tiny(iters);
         for (int64_t k = 0; k < iters; ++k) {
             if (gexec) CU(cudaGraphLaunch(gexec, stream));
@@ -1730,7 +1772,7 @@ struct Solver final : SolverBase {
     }
 
     cfr_status launches(int64_t* n) override {
-        *n = (persist_ || tiny_) ? 1 : launches_per_iter;   // one launch per enqueue of T iterations
+        *n = tiny_ ? 1 : launches_per_iter;   // k_tiny: one launch per enqueue of T iterations
         return CFR_OK;
     }
 

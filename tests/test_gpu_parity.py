@@ -76,24 +76,13 @@ def test_synthetic_small(cuda):
     run_pair(desc, 0, 32, 2, checks=("state",))
 
 
-@pytest.mark.parametrize("name", ["kuhn", "leduc", "goofspiel", "liars_dice"])
-def test_persistent_matches_per_level_launches(cuda, name):
-    """The persistent single-launch iteration (k_persist, grid barriers between
-    levels) and the per-level kernel launches give the same bits."""
+def test_removed_persistent_flag_is_rejected(cuda):
+    """CFR_FLAG_PERSISTENT selected the cooperative single-launch kernel, removed
+    (slower than the graph): creation fails loudly."""
     import paper_2408_14778_b200 as pb
-    desc = gamegen.by_name(name)
-    g = pb.Game(desc)
-    T = 7 if name == "liars_dice" else 40
-    a = pb.Solver(g, variant="cfr+", precision=64, flags=pb.FLAG_PERSISTENT)
-    b = pb.Solver(g, variant="cfr+", precision=64, flags=pb.FLAG_NO_TINY)
-    assert a.launches_per_iteration() == 1 and b.launches_per_iteration() > 1
-    a.run(T)
-    b.run(T)
-    assert a.iteration == b.iteration == T
-    sa, sb = a.state(), b.state()
-    for k in ("regret", "snum", "sden"):
-        assert np.array_equal(sa[k], sb[k]), k
-    assert np.array_equal(a.average_strategy(), b.average_strategy())
+    with pytest.raises(pb.NativeError) as ei:
+        pb.Solver(pb.Game(gamegen.kuhn()), variant="cfr", precision=64, flags=pb.FLAG_PERSISTENT)
+    assert ei.value.name == "CFR_ERR_UNSUPPORTED"
 
 
 @pytest.mark.parametrize("precision", [64, 32])

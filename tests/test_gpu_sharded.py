@@ -13,13 +13,13 @@ from tests.parity import assert_same
 pytestmark = pytest.mark.gpu
 
 
-def run_world(desc, variant, precision, T, world, shard_prefix=None, br=True):
+def run_world(desc, variant, precision, T, world, shard_prefix=None, br=True, flags=0):
     g = pb.Game(desc)
     games = [g] * world
     if shard_prefix is not None:      # ranks load their own view from shard files
         g.save_shards(world, shard_prefix)
         games = [pb.Game.load_shard(shard_prefix, r, world) for r in range(world)]
-    ss = [pb.Solver(games[r], variant=int(variant), precision=precision, rank=r, world_size=world)
+    ss = [pb.Solver(games[r], variant=int(variant), precision=precision, rank=r, world_size=world, flags=flags)
           for r in range(world)]
 
     def allreduce(which):
@@ -52,7 +52,8 @@ def run_world(desc, variant, precision, T, world, shard_prefix=None, br=True):
         s.phase(pb.Solver.PHASE_EV_LOWER)
     allreduce(pb.Solver.XCHG_CUT)
     evs = [s.phase(pb.Solver.PHASE_EV_UPPER) for s in ss]
-    out = dict(avg=avg, cur=cur, regret=reg, sden=sden, ev=evs, info=[s.shard_info() for s in ss])
+    out = dict(avg=avg, cur=cur, regret=reg, sden=sden, ev=evs, info=[s.shard_info() for s in ss],
+               kernels=[s.level_kernels() for s in ss])
     if br:
         out["br"] = world_best_response(ss, allreduce)
     return out
@@ -126,3 +127,28 @@ def test_sharded_from_shard_files(cuda, tmp_path):
     assert_same("average strategy", r["avg"], o.state()["avg"], 64)
     for ev in r["ev"]:
         assert_same("EV(avg)", ev, o.expected_values(), 64)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("variant,precision", [(1, 64), (0, 32), (2, 64)])
+def test_sharded_synthetic_streaming_deferred_levels(cuda, world, variant, precision):
+    """The synthetic tree sharded by player 1's type: player 2's infosets span the
+    ranks, so player 2's levels run k_bwd_stream in deferred mode (exact partial
+    sums into the exchange block, updated after the all-reduce) -- bit-identical
+    to the oracle, like the fused levels."""
+    desc = gamegen.synthetic(n_types=2 * world, c=(3, 2, 3, 2), seed=2)   # cut at player 1's type
+    T = 4
+    o = oracle.Oracle(desc, precision=precision).run(T, variant)
+    r = run_world(desc, variant, precision, T, world, br=False, flags=pb.FLAG_FORCE_STREAM)
+    os_ = o.state()
+    assert_same("average strategy", r["avg"], os_["avg"], precision)
+    assert_same("current strategy", r["cur"], os_["sigma"], precision)
+    assert_same("regret", r["regret"], os_["regret"], precision)
+    assert_same("S_den", r["sden"], os_["sden"], precision)
+    for ev in r["ev"]:
+        assert_same("EV(avg)", ev, o.expected_values(), precision)
+    info = r["info"][0]
+    assert info["deferred"] > 0
+    # player 2's deepest decision level (depth D - 2) streams although its infosets span ranks
+    for ks in r["kernels"]:
+        assert ks.count("k_bwd_stream") >= 2, ks

@@ -671,3 +671,24 @@ def test_best_response_on_depth_spanning_infosets_equals_enumeration(seed):
             best = max(best, o.expected_values(s)[pl - 1])
         val, _ = o.best_response(pl, base)
         assert abs(val - best) <= 1e-12, (pl, val, best)
+
+
+def test_exact_sums_near_the_largest_double():
+    """Appendix B-4's exponent E = 1 + ceil(log2(2 max|u|)) evaluated without
+    overflow: with payoffs (B, -B), B = 1.5e308 (2B is not finite), iteration 1 of
+    vanilla CFR gives v = 0, r~ = (B, -B) exactly (S:529's closed form scaled), and
+    sigma^(2) = (1, 0); iteration 2's term -B - B overflows (Eq 7)."""
+    from gamegen.desc import Builder
+
+    B = 1.5e308
+    b = Builder("big", 1)
+    r = b.node(-1, -1)
+    b.set_player(r, 1, "root", 2)
+    for a, u in enumerate((B, -B)):
+        c = b.node(r, a)
+        b.set_terminal(c, [u])
+    o = oracle.Oracle(b.build(zero_sum=False)).run(1, 0)
+    st = o.state()
+    assert st["regret"].tolist() == [B, -B]
+    assert st["sigma"].tolist() == [1.0, 0.0]
+    assert o.expected_values("current").tolist() == [B]
