@@ -433,7 +433,7 @@ struct Plan {
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, br_best, ctrl, lcnt, out, rec;
-    size_t cutbuf, cutrow, cutown, report, pool, spool, tlev, tmem_of;
+    size_t cutbuf, cutrow, cutown, report, pool, spool, tmeta;
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
         Layout L;
@@ -475,8 +475,8 @@ struct Plan {
         report = L.take<unsigned char>(H + 1);
         pool = L.take<unsigned char>(fast_pool_bytes<R, I>(g, sh) + 16);
         spool = L.take<int>(stream_pool_bound(g));
-        tlev = L.take<TinyLevel>((size_t)g.D + 1);
-        tmem_of = L.take<I>(g.V <= (int64_t(1) << 20) ? 2 * H + 2 : 2);
+        // k_tiny's int32 game tables (TinyMeta), tiny-game candidates only
+        tmeta = L.take<int>(g.V <= (int64_t(1) << 20) ? (size_t)(4 * (g.D + 1) + 7 * NS + 4 * H + Q + 16) : 2);
         rec = L.take<double>((size_t)kRecRows * rec_width(g));
         total = L.off + 256;
     }
@@ -997,12 +997,14 @@ struct Solver final : SolverBase {
 
     bool has_def_() const { return !gp->deferred_list.empty(); }
 
+    bool tiny_meta_smem_ = false;   // k_tiny's game tables are in shared memory
     void* tiny_fn() const {
+        const bool m = tiny_meta_smem_;
         switch (gp->Pc) {
-            case 1: return (void*)k_tiny<R, I, 1>;
-            case 2: return (void*)k_tiny<R, I, 2>;
-            case 3: return (void*)k_tiny<R, I, 3>;
-            default: return (void*)k_tiny<R, I, 4>;
+            case 1: return m ? (void*)k_tiny<R, I, 1, true> : (void*)k_tiny<R, I, 1, false>;
+            case 2: return m ? (void*)k_tiny<R, I, 2, true> : (void*)k_tiny<R, I, 2, false>;
+            case 3: return m ? (void*)k_tiny<R, I, 3, true> : (void*)k_tiny<R, I, 3, false>;
+            default: return m ? (void*)k_tiny<R, I, 4, true> : (void*)k_tiny<R, I, 4, false>;
         }
     }
     // Tiny-game mode (k_tiny): single-GPU, depth-homogeneous games whose mutable
@@ -1041,13 +1043,12 @@ struct Solver final : SolverBase {
             if (bytes <= optin - 1024) break;
         }
         if (bytes > optin - 1024) return CFR_OK;
-        tp.bytes = (int)bytes;
         // per level: slots and its (consecutive) infosets; members of each infoset
-        std::vector<TinyLevel> lv(g.D + 1, TinyLevel{0, 0, 0, 0});
+        std::vector<int64_t> lvv(4 * (size_t)(g.D + 1), 0);
         std::vector<int64_t> mem(2 * (size_t)g.H + 2, -1);
         for (int L = 0; L < g.D; ++L) {
-            lv[L].s0 = g.slot_ptr[L];
-            lv[L].s1 = g.slot_ptr[L + 1];
+            lvv[4 * L] = g.slot_ptr[L];
+            lvv[4 * L + 1] = g.slot_ptr[L + 1];
             long long h0 = LLONG_MAX, h1 = -1;
             for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1]; ++t)
                 for (int k = g.tiles[t].seg0; k < g.tiles[t].seg1; ++k) {
@@ -1059,38 +1060,97 @@ struct Solver final : SolverBase {
                     h1 = std::max<long long>(h1, h + 1);
                 }
             if (h1 > h0) {
-                lv[L].h0 = h0;
-                lv[L].h1 = h1;
+                lvv[4 * L + 2] = h0;
+                lvv[4 * L + 3] = h1;
             }
         }
         for (int64_t h = 0; h < g.H; ++h)
             if (mem[2 * h] < 0) return CFR_OK;
         for (int L = 0; L < g.D; ++L)   // each level's infosets must be a consecutive id range
-            for (long long h = lv[L].h0; h < lv[L].h1; ++h)
+            for (long long h = lvv[4 * L + 2]; h < lvv[4 * L + 3]; ++h)
                 if (mem[2 * h] < g.slot_ptr[L] || mem[2 * h + 1] > g.slot_ptr[L + 1]) return CFR_OK;
+        // TinyMeta: int32 tables (the slot tables come back from the device
+        // arrays the per-level kernels use, so both paths read the same numbers)
+        const int64_t NS = g.NS;
+        tp.m_lv = 0;
+        tp.m_slot = 4 * (g.D + 1);
+        tp.m_qb = (int)(tp.m_slot + 7 * NS);
+        tp.m_own = (int)(tp.m_qb + g.H + 1);
+        tp.m_mem = (int)(tp.m_own + g.H);
+        tp.m_ph = (int)(tp.m_mem + 2 * g.H);
+        tp.meta_ints = (int)(tp.m_ph + g.Q);
+        std::vector<int> meta((size_t)tp.meta_ints, 0);
+        for (size_t k = 0; k < lvv.size(); ++k) meta[tp.m_lv + k] = (int)lvv[k];
+        {
+            std::vector<I> fp(NS), fe(NS), cb(NS), eb(NS), nd(NS);
+            std::vector<unsigned char> pa(NS);
+            std::vector<int> nn(NS);
+            CU(cudaStreamSynchronize(stream));   // the uploads of the device tables are done
+            CU(cudaMemcpy(fp.data(), ws + plan.f_parent, NS * sizeof(I), cudaMemcpyDeviceToHost));
+            CU(cudaMemcpy(fe.data(), ws + plan.f_e, NS * sizeof(I), cudaMemcpyDeviceToHost));
+            CU(cudaMemcpy(pa.data(), ws + plan.f_pact, NS, cudaMemcpyDeviceToHost));
+            CU(cudaMemcpy(cb.data(), ws + plan.s_cb, NS * sizeof(I), cudaMemcpyDeviceToHost));
+            CU(cudaMemcpy(eb.data(), ws + plan.s_ebase, NS * sizeof(I), cudaMemcpyDeviceToHost));
+            CU(cudaMemcpy(nn.data(), ws + plan.s_n, NS * sizeof(int), cudaMemcpyDeviceToHost));
+            CU(cudaMemcpy(nd.data(), ws + plan.s_node, NS * sizeof(I), cudaMemcpyDeviceToHost));
+            for (int64_t k = 0; k < NS; ++k) {
+                int* e = &meta[tp.m_slot + 7 * k];
+                e[0] = (int)fp[k];
+                e[1] = (int)fe[k];
+                e[2] = (int)pa[k];
+                e[3] = (int)cb[k];
+                e[4] = (int)eb[k];
+                e[5] = nn[k];
+                e[6] = (int)nd[k];
+            }
+        }
+        for (int64_t h = 0; h <= g.H; ++h) meta[tp.m_qb + h] = (int)g.qbase_int[h];
+        for (int64_t h = 0; h < g.H; ++h) {
+            meta[tp.m_own + h] = (int)g.owner_int[h];
+            meta[tp.m_mem + 2 * h] = (int)mem[2 * h];
+            meta[tp.m_mem + 2 * h + 1] = (int)mem[2 * h + 1];
+            for (int64_t q = g.qbase_int[h]; q < g.qbase_int[h + 1]; ++q) meta[tp.m_ph + q] = (int)h;
+        }
+        // the tables join the state in shared memory when both fit (Kuhn)
+        const long long meta_bytes = 4LL * tp.meta_ints;
+        tp.meta_off = (int)((bytes + 15) & ~15LL);
+        tiny_meta_smem_ = tp.meta_off + meta_bytes <= optin - 1024;
+        tp.bytes = tiny_meta_smem_ ? (int)(tp.meta_off + meta_bytes) : (int)bytes;
         CU(cudaFuncSetAttribute(tiny_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, tp.bytes));
-        cfr_status st = up(plan.tlev, lv);
+        cfr_status st = up(plan.tmeta, meta);
         if (st) return st;
-        if ((st = up(plan.tmem_of, narrow<I>(mem)))) return st;
         CU(cudaStreamSynchronize(stream));
+        // one thread per slot / item of the widest level (fewer warps = cheaper
+        // barriers on games like Kuhn), at most 1024
+        int64_t widest = 32;
+        for (int L = 0; L < g.D; ++L) {
+            widest = std::max<int64_t>(widest, lvv[4 * L + 1] - lvv[4 * L]);
+            const int64_t h0 = lvv[4 * L + 2], h1 = lvv[4 * L + 3];
+            if (h1 > h0) widest = std::max<int64_t>(widest, (g.qbase_int[h1] - g.qbase_int[h0]) + (h1 - h0));
+        }
+        tiny_threads_ = (int)std::min<int64_t>(1024, (widest + 31) / 32 * 32);
         tiny_plan_ = tp;
         tiny_ = true;
         return CFR_OK;
     }
+    int tiny_threads_ = 1024;
     long long plan_u_rows() const { return (long long)u_layout(*gp, sizeof(R)).back(); }
     cfr_status launch_tiny(int64_t iters) {
         const Game& g = *gp;
-        const TinyLevel* lv = reinterpret_cast<const TinyLevel*>(ws + plan.tlev);
-        const I* mem = reinterpret_cast<const I*>(ws + plan.tmem_of);
+        const int* meta = reinterpret_cast<const int*>(ws + plan.tmeta);
         const int D = g.D;
         const long long T = (long long)iters;
         const TinyPlan tp = tiny_plan_;
+#define CFRB_TINY(PC)                                                                                              \
+    (tiny_meta_smem_ ? launch(pdl_, k_tiny<R, I, PC, true>, dim3(1), dim3(tiny_threads_), (size_t)tp.bytes, stream, dg, meta, D, T, tp) \
+                     : launch(pdl_, k_tiny<R, I, PC, false>, dim3(1), dim3(tiny_threads_), (size_t)tp.bytes, stream, dg, meta, D, T, tp))
         switch (g.Pc) {
-            case 1: launch(pdl_, k_tiny<R, I, 1>, dim3(1), dim3(1024), (size_t)tp.bytes, stream, dg, lv, mem, D, T, tp); break;
-            case 2: launch(pdl_, k_tiny<R, I, 2>, dim3(1), dim3(1024), (size_t)tp.bytes, stream, dg, lv, mem, D, T, tp); break;
-            case 3: launch(pdl_, k_tiny<R, I, 3>, dim3(1), dim3(1024), (size_t)tp.bytes, stream, dg, lv, mem, D, T, tp); break;
-            default: launch(pdl_, k_tiny<R, I, 4>, dim3(1), dim3(1024), (size_t)tp.bytes, stream, dg, lv, mem, D, T, tp); break;
+            case 1: CFRB_TINY(1); break;
+            case 2: CFRB_TINY(2); break;
+            case 3: CFRB_TINY(3); break;
+            default: CFRB_TINY(4); break;
         }
+#undef CFRB_TINY
         CU(cudaGetLastError());
         return CFR_OK;
     }
