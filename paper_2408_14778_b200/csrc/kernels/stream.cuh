@@ -66,15 +66,22 @@ __device__ __forceinline__ void mbar_expect_tx(void* bar, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive(void* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait suspend-time hint: a waiting warp is parked by the hardware until the
+// phase completes (or the hint elapses) instead of re-issuing the test, so
+// waiting warps do not take issue slots from working ones
+#ifndef CFR_WAIT_HINT_NS
+#define CFR_WAIT_HINT_NS 1000000
+#endif
+constexpr unsigned kWaitHintNs = CFR_WAIT_HINT_NS;
 __device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "n"(kWaitHintNs)
         : "memory");
 }
 // global -> shared bulk copy of a 16-byte-aligned window; completes on `bar`

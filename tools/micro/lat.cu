@@ -43,11 +43,16 @@ int main() {
     double* out; long long* cyc;
     cudaMalloc(&out, 1024 * 8); cudaMallocManaged(&cyc, 64);
     const int n = 1000;
-    k<<<1, 32>>>(out, cyc, 1.25, n, 3);
-    cudaDeviceSynchronize();
-    k<<<1, 32>>>(out, cyc, 1.25, n, 3);
-    cudaDeviceSynchronize();
     const char* nm[] = {"DADD", "DMUL", "FADD", "LDS.64+F2I", "SHFL.64", "IDIV(rt)", "DDIV"};
-    for (int i = 0; i < 7; ++i) printf("%-12s %6.1f cycles\n", nm[i], (double)cyc[i] / (i == 6 ? n : 4 * n));
+    // one warp, then 18 warps on one SM (the streaming kernel's residency): cycles
+    // per dependent operation as seen by warp 0
+    for (int threads : {32, 576}) {
+        k<<<1, threads>>>(out, cyc, 1.25, n, 3);
+        cudaDeviceSynchronize();
+        k<<<1, threads>>>(out, cyc, 1.25, n, 3);
+        cudaDeviceSynchronize();
+        printf("-- %d warps on one SM\n", threads / 32);
+        for (int i = 0; i < 7; ++i) printf("%-12s %6.1f cycles\n", nm[i], (double)cyc[i] / (i == 6 ? n : 4 * n));
+    }
     return 0;
 }
