@@ -404,6 +404,52 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                             for (int e = 0; e < E; ++e) v[0] = v[0] + sg[a + e] * ue[e];
                         }
                     }
+                } else if (PC == 2 && vec_rows) {
+                    // two value columns (general-sum two-player games): 16-byte row
+                    // reads, four chunks in flight per step; the two columns' sums
+                    // are independent chains, each in ascending action order
+                    using V = typename std::conditional<sizeof(R) == 8, double2, float4>::type;
+                    constexpr int E = 16 / (2 * (int)sizeof(R));   // actions per 16-byte chunk
+                    const V* row4 = reinterpret_cast<const V*>(row);
+                    const int nc = n / E;
+                    int c = 0;
+                    for (; c + 4 <= nc; c += 4) {
+                        const V p0 = row4[c], p1 = row4[c + 1], p2 = row4[c + 2], p3 = row4[c + 3];
+                        const R* u0 = reinterpret_cast<const R*>(&p0);
+                        const R* u1 = reinterpret_cast<const R*>(&p1);
+                        const R* u2 = reinterpret_cast<const R*>(&p2);
+                        const R* u3 = reinterpret_cast<const R*>(&p3);
+                        const int a0 = c * E;
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const R x = sg[a0 + e];
+                            v[0] = v[0] + x * u0[2 * e];
+                            v[1] = v[1] + x * u0[2 * e + 1];
+                        }
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const R x = sg[a0 + E + e];
+                            v[0] = v[0] + x * u1[2 * e];
+                            v[1] = v[1] + x * u1[2 * e + 1];
+                        }
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const R x = sg[a0 + 2 * E + e];
+                            v[0] = v[0] + x * u2[2 * e];
+                            v[1] = v[1] + x * u2[2 * e + 1];
+                        }
+#pragma unroll
+                        for (int e = 0; e < E; ++e) {
+                            const R x = sg[a0 + 3 * E + e];
+                            v[0] = v[0] + x * u3[2 * e];
+                            v[1] = v[1] + x * u3[2 * e + 1];
+                        }
+                    }
+                    for (int a = c * E; a < n; ++a) {
+                        const R x = sg[a];
+                        v[0] = v[0] + x * row[2 * a];
+                        v[1] = v[1] + x * row[2 * a + 1];
+                    }
                 } else {
                     for (int a = 0; a < n; ++a) {
                         const R x = sg[a];
@@ -501,7 +547,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                     double c0 = 0, c1 = 0, c2 = 0;
                     if (itm < n) {
                         const int a = itm;
-                        double e0 = 0, e1 = 0, e2 = 0;   // second independent slice chain (ILP)
+                        double e0 = 0, e1 = 0, e2 = 0;   // second independent slice chain (ILP; a 4-chain variant measured slower)
                         int jj = part;
                         for (; jj + ns < cntc; jj += 2 * ns) {
                             const int la = memc[jj], lb = memc[jj + ns];

@@ -247,6 +247,9 @@ static std::vector<FastLevel> fast_levels(const Game& g, const std::vector<TileD
     return out;
 }
 
+// child-row bytes per streaming tile (the n = 40 synthetic's f64 tiles: 240 x 160 B)
+constexpr int kStreamRowBytes = 40960;
+
 // Shared-memory plan of k_bwd_stream for one level (stage ring + work arrays +
 // barriers).  Every block is 16-byte aligned; windows get 16 bytes of slack.
 static void stream_plan(StreamLevel& f, int P, int Pc, int w, int ix, int stages) {
@@ -328,11 +331,18 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         if (!ok) { out[L] = f; continue; }
         const int nh = (int)hs.size();
         hs.push_back((int)(s1 - s0));
-        // tiles: greedy runs of whole infosets, <= kStreamConsumers members, <= 32 infosets
+        // tiles: greedy runs of whole infosets, <= 32 infosets, at most tile_target
+        // members and about kStreamRowBytes of child rows per stage (wide rows --
+        // e.g. two value columns of a general-sum game -- get fewer members, so two
+        // CTAs with two-stage rings stay resident per SM), never fewer members
+        // than the level's largest infoset
+        int maxmem = 1;
+        for (int k = 0; k < nh; ++k) maxmem = std::max(maxmem, hs[k + 1] - hs[k]);
+        const int tt = std::max(maxmem, std::min(tile_target, kStreamRowBytes / std::max(1, n * Pc * w)));
         std::vector<int> tk = {0};
         for (int k = 0; k < nh; ++k) {
             const int k0 = tk.back();
-            if (k > k0 && (hs[k + 1] - hs[k0] > tile_target || k + 1 - k0 > 32)) tk.push_back(k);
+            if (k > k0 && (hs[k + 1] - hs[k0] > tt || k + 1 - k0 > 32)) tk.push_back(k);
         }
         tk.push_back(nh);
         f.ntiles = (long long)tk.size() - 1;

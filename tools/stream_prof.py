@@ -1,6 +1,6 @@
 """Per-phase cycle split of k_bwd_stream (built with -DCFR_STREAM_PROFILE as the
 'sprof' library variant): cycles per consumer warp per tile, summed over the
-iteration's streaming levels."""
+iteration's streaming levels.  python tools/stream_prof.py [n_types | battleshipK] [variant] [precision]"""
 import ctypes
 import os
 import sys
@@ -13,11 +13,17 @@ import gamegen
 import paper_2408_14778_b200 as pb
 from paper_2408_14778_b200 import _native
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 40
-d = gamegen.synthetic(n_types=n)
+arg = sys.argv[1] if len(sys.argv) > 1 else "40"
+variant = sys.argv[2] if len(sys.argv) > 2 else "cfr+"
+prec = int(sys.argv[3]) if len(sys.argv) > 3 else 64
+if arg.startswith("battleship"):
+    from gamegen.battleship import paper_battleship
+    d = paper_battleship(arg)
+else:
+    d = gamegen.synthetic(n_types=int(arg))
 g = pb.Game(d)
 del d
-s = pb.Solver(g, variant="cfr+", precision=64)
+s = pb.Solver(g, variant=variant, precision=prec)
 s.run(4)
 L = _native.load()
 f = L.cfr_debug_stream_profile
