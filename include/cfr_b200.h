@@ -127,9 +127,10 @@ typedef struct {
     int32_t flags;       /* bit 0: disable CUDA-Graph capture (debug);            */
                          /* bit 1: reserved -- the cooperative single-launch     */
                          /* kernel it selected was removed (slower than the PDL  */
-                         /* graph on B200): CFR_ERR_UNSUPPORTED; bit 2: disable  */
-                         /* the pipelined                                        */
-                         /* (persistent) backward kernel; bit 3: disable          */
+                         /* graph on B200): CFR_ERR_UNSUPPORTED; bit 2: reserved */
+                         /* (ignored: the pipelined cp.async backward kernel it  */
+                         /* disabled was superseded by the streaming kernel and  */
+                         /* removed); bit 3: disable                             */
                          /* programmatic dependent launch; bit 4: disable the     */
                          /* streaming (TMA) backward kernel (A/B comparisons);    */
                          /* bit 5: use the streaming kernel on every eligible     */
@@ -145,7 +146,7 @@ typedef struct {
 
 #define CFR_FLAG_NO_GRAPH 1
 #define CFR_FLAG_PERSISTENT 2   /* reserved: rejected with CFR_ERR_UNSUPPORTED */
-#define CFR_FLAG_NO_PIPELINE 4
+#define CFR_FLAG_NO_PIPELINE 4   /* reserved: ignored */
 #define CFR_FLAG_NO_PDL 8
 #define CFR_FLAG_NO_STREAM 16
 #define CFR_FLAG_FORCE_STREAM 32
@@ -232,8 +233,8 @@ cfr_status cfr_solver_profile(cfr_solver* s, int64_t iterations, double* out_ms 
  * total, [1] forward, [2] backward, [3] update, [4] dominant backward level. */
 cfr_status cfr_solver_model_bytes(cfr_solver* s, double* out /* [5] */);
 /* Which backward kernel serves each parent level L = 0..D-1 of the CFR iteration:
- * out[L] = 0 (no slots), 1 k_bwd (tile per CTA), 2 k_bwd_fast (pipelined
- * cp.async), 3 k_bwd_stream (TMA bulk-copy ring).  `max_levels` bounds out[];
+ * out[L] = 0 (no slots), 1 k_bwd (tile per CTA), 3 k_bwd_stream (TMA bulk-copy
+ * ring); 2 is no longer used (the pipelined cp.async kernel was removed).  `max_levels` bounds out[];
  * *num_levels receives D. */
 cfr_status cfr_solver_level_kernels(cfr_solver* s, int32_t* out, int32_t max_levels, int32_t* num_levels);
 /* Cumulative work counters of the streaming backward kernel per parent level L

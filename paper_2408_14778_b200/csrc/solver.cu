@@ -38,7 +38,6 @@
 #include "kernels/common.cuh"
 #include "kernels/forward.cuh"
 #include "kernels/tile.cuh"
-#include "kernels/pipelined.cuh"
 #include "kernels/stream.cuh"
 #include "kernels/update.cuh"
 #include "kernels/small.cuh"
@@ -194,57 +193,6 @@ static void stage_tiles(const Game& g, const std::vector<int64_t>& cb_u, const s
         }
         tiles[t] = td;
     }
-}
-
-// Levels served by the pipelined k_bwd_fast: every tile chunk-staged, fused,
-// player-only, one row length across the level, and enough tiles to pipeline.
-template <class R, class I>
-static std::vector<FastLevel> fast_levels(const Game& g, const std::vector<TileD>& tiles, size_t* pool_bytes) {
-    std::vector<FastLevel> out(g.D, FastLevel{});
-    size_t pool = 0;
-    for (int L = 0; L < g.D; ++L) {
-        FastLevel f{};
-        f.tile0 = g.tile_ptr[L];
-        f.ntiles = g.tile_ptr[L + 1] - g.tile_ptr[L];
-        f.recsize = 0;
-        bool ok = f.ntiles >= 2 * 148;
-        int rowlen = -1, maxslot = 1, maxseg = 1, maxpairs = 1, maxch = 0;
-        for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1] && ok; ++t) {
-            const TileD& td = tiles[t];
-            if (td.staged != 1 || td.npairs > kTilePairs || td.cpr > 2 * kTileSlots) { ok = false; break; }
-            if (rowlen < 0) rowlen = td.rowlen;
-            if (td.rowlen != rowlen) { ok = false; break; }
-            int64_t members = 0;
-            for (int k = td.seg0; k < td.seg1; ++k) {
-                if (!g.segs[k].fused) ok = false;
-                members += g.segs[k].se - g.segs[k].sb;
-            }
-            if (members != td.s1 - td.s0) ok = false;   // a chance slot
-            const int nslot = (int)(td.s1 - td.s0);
-            maxslot = std::max(maxslot, nslot);
-            maxseg = std::max(maxseg, td.seg1 - td.seg0);
-            maxpairs = std::max(maxpairs, td.npairs);
-            maxch = std::max(maxch, nslot * td.stride);
-        }
-        if (ok && f.ntiles > 0) {
-            const TileD& t0 = tiles[g.tile_ptr[L]];
-            f.maxslot = maxslot;
-            f.maxseg = maxseg;
-            f.maxpairs = maxpairs;
-            f.maxch = maxch;
-            f.rowlen = t0.rowlen;
-            f.cpr = t0.cpr;
-            f.stride = t0.stride;
-            f.inv_cpr = t0.inv_cpr;
-            f.recsize = (int)((32 + (int64_t)maxseg * sizeof(FastSeg) + 3 * sizeof(I) * (int64_t)maxslot + maxslot +
-                               maxpairs + 15) & ~int64_t(15));
-            f.rec = (long long)pool;
-            pool += (size_t)f.recsize * (size_t)f.ntiles;
-        }
-        out[L] = f;
-    }
-    *pool_bytes = pool;
-    return out;
 }
 
 // child-row bytes per streaming tile (the n = 40 synthetic's f64 tiles: 240 x 160 B)
@@ -417,20 +365,6 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
 // + per-level alignment / terminators and the window slack
 static size_t stream_pool_bound(const Game& g) { return (size_t)(5 * g.H + 10 * (int64_t)g.D + 64); }
 
-template <class R, class I>
-static size_t fast_pool_bytes(const Game& g, const ShardInfo* sh) {
-    const std::vector<int64_t> uoff = u_layout(g, sizeof(R));
-    std::vector<int64_t> nu, cu;
-    u_rows(g, uoff, nu, cu);
-    std::vector<TileD> tiles;
-    std::vector<int32_t> coff;
-    static const std::vector<uint8_t> none;
-    stage_tiles<R>(g, cu, sh ? sh->tile_contrib : none, tiles, coff);
-    size_t pool = 0;
-    fast_levels<R, I>(g, tiles, &pool);
-    return pool;
-}
-
 // In-graph exploitability record (cfr_solver_run_tracked): per evaluation one
 // row of root values -- EV (Pc columns), then each player's best-response root
 // row (Pc columns each), then the iteration count.
@@ -443,7 +377,7 @@ struct Plan {
     size_t f_parent, f_e, f_pact;
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, br_best, ctrl, lcnt, out, rec;
-    size_t cutbuf, cutrow, cutown, report, pool, spool, tmeta;
+    size_t cutbuf, cutrow, cutown, report, spool, tmeta;
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
         Layout L;
@@ -483,7 +417,6 @@ struct Plan {
         cutrow = L.take<long long>(ncut + 1);
         cutown = L.take<unsigned char>(ncut + 1);
         report = L.take<unsigned char>(H + 1);
-        pool = L.take<unsigned char>(fast_pool_bytes<R, I>(g, sh) + 16);
         spool = L.take<int>(stream_pool_bound(g));
         // k_tiny's int32 game tables (TinyMeta), tiny-game candidates only
         tmeta = L.take<int>(g.V <= (int64_t(1) << 20) ? (size_t)(4 * (g.D + 1) + 7 * NS + 4 * H + Q + 16) : 2);
@@ -516,7 +449,6 @@ struct Solver final : SolverBase {
     bool use_graph = true;
     bool tiny_ = false;           // tiny game: whole iterations in one CTA, state in shared memory (k_tiny)
     TinyPlan tiny_plan_{};
-    bool use_fast_ = true;
     bool use_stream_ = true;
     int stream_debug_ = 0;   // CFR_STREAM_DEBUG (timing experiments; results are garbage when set)
     bool pdl_ = true;
@@ -575,7 +507,6 @@ struct Solver final : SolverBase {
     std::vector<SmemLayout> lay_;   // per parent level
     int max_smem_ = 0;
     int max_smem_stream_ = 0;
-    std::vector<FastLevel> fast_;   // per parent level: recsize > 0 -> pipelined kernel
     std::vector<StreamLevel> stream_;   // per parent level: ntiles > 0 -> streaming (TMA) kernel
 
     SmemLayout make_layout(int maxch, int maxslot, int maxpairs, int maxseg) const {
@@ -698,7 +629,6 @@ struct Solver final : SolverBase {
             return CFR_ERR_UNSUPPORTED;
         }
         use_graph = !(cfg.flags & CFR_FLAG_NO_GRAPH);
-        use_fast_ = !(cfg.flags & CFR_FLAG_NO_PIPELINE);
         use_stream_ = !(cfg.flags & CFR_FLAG_NO_STREAM);
         pdl_ = !(cfg.flags & CFR_FLAG_NO_PDL);
         {
@@ -784,53 +714,6 @@ struct Solver final : SolverBase {
         std::vector<int32_t> s_coff;
         std::vector<TileD> tiles;
         stage_tiles<R>(g, s_cb_u, tile_contrib_, tiles, s_coff);
-        {
-            // records of the pipelined levels
-            size_t pool = 0;
-            fast_ = fast_levels<R, I>(g, tiles, &pool);
-            std::vector<unsigned char> rec(pool, 0);
-            for (int L = 0; L < g.D; ++L) {
-                const FastLevel& f = fast_[L];
-                if (f.recsize == 0) continue;
-                for (int64_t t = 0; t < f.ntiles; ++t) {
-                    const TileH& th = g.tiles[f.tile0 + t];
-                    unsigned char* r = rec.data() + f.rec + t * f.recsize;
-                    FastHdr hd{th.s0, (int)(th.s1 - th.s0), th.seg1 - th.seg0, th.npairs, 0};
-                    std::memcpy(r, &hd, sizeof(hd));
-                    FastSeg* sg = reinterpret_cast<FastSeg*>(r + 32);
-                    for (int k = th.seg0; k < th.seg1; ++k) {
-                        const SegH& shh = g.segs[k];
-                        FastSeg fs{};
-                        fs.h = shh.h;
-                        fs.qb = g.qbase_int[shh.h];
-                        fs.pair_off = shh.pair_off;
-                        fs.n = (int)(g.qbase_int[shh.h + 1] - g.qbase_int[shh.h]);
-                        fs.owner = g.owner_int[shh.h];
-                        fs.sb = (int)(shh.sb - th.s0);
-                        fs.se = (int)(shh.se - th.s0);
-                        sg[k - th.seg0] = fs;
-                    }
-                    I* node = reinterpret_cast<I*>(r + 32 + (th.seg1 - th.seg0) * sizeof(FastSeg));
-                    I* cb = node + (th.s1 - th.s0);
-                    I* dec = cb + (th.s1 - th.s0);
-                    for (int64_t s = th.s0; s < th.s1; ++s) {
-                        node[s - th.s0] = (I)s_node_u[s];
-                        cb[s - th.s0] = (I)s_cb_u[s];
-                        dec[s - th.s0] = (I)s;   // reach row = slot
-                    }
-                    // segment of every slot and of every pair (no searches on the device)
-                    unsigned char* sseg = reinterpret_cast<unsigned char*>(dec + (th.s1 - th.s0));
-                    unsigned char* pseg = sseg + (th.s1 - th.s0);
-                    for (int k = th.seg0; k < th.seg1; ++k) {
-                        const SegH& shh = g.segs[k];
-                        for (int64_t s = shh.sb; s < shh.se; ++s) sseg[s - th.s0] = (unsigned char)(k - th.seg0);
-                        const int n = (int)(g.qbase_int[shh.h + 1] - g.qbase_int[shh.h]);
-                        for (int a = 0; a < n; ++a) pseg[shh.pair_off + a] = (unsigned char)(k - th.seg0);
-                    }
-                }
-            }
-            if ((st = up(plan.pool, rec))) return st;
-        }
         {
             // tables of the streaming levels
             std::vector<int> sp;
@@ -984,8 +867,6 @@ struct Solver final : SolverBase {
         cudaError_t e = cudaSuccess;
 #define SETA(PC)                                                                                        \
     e = cudaFuncSetAttribute(k_bwd<R, I, PC, MODE_CFR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
-    if (e) return e;                                                                                    \
-    e = cudaFuncSetAttribute(k_bwd_fast<R, I, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);     \
     if (e) return e;                                                                                    \
     e = cudaFuncSetAttribute(k_bwd_stream<R, I, PC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);   \
     if (e) return e;                                                                                    \
@@ -1225,28 +1106,6 @@ struct Solver final : SolverBase {
                 case 2: launch(pdl_, k_bwd_stream<R, I, 2>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
                 case 3: launch(pdl_, k_bwd_stream<R, I, 3>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
                 default: launch(pdl_, k_bwd_stream<R, I, 4>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
-            }
-            return;
-        }
-        // pipelined kernel: measured faster for f64 only (f32 tiles move half the bytes)
-        if (MODE == MODE_CFR && sizeof(R) == 8 && sig == dg.sig && use_fast_ && fast_[L].recsize > 0) {
-            FastLevel f = fast_[L];
-            f.last = last;
-            const int bytes = fast_plan(f, g.Pc, (int)sizeof(R)).bytes;
-            int per_sm = 1;
-            switch (g.Pc) {
-                case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 1>, 2 * kTileSlots, bytes); break;
-                case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 2>, 2 * kTileSlots, bytes); break;
-                case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 3>, 2 * kTileSlots, bytes); break;
-                default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_fast<R, I, 4>, 2 * kTileSlots, bytes); break;
-            }
-            per_sm = std::max(1, per_sm);
-            const unsigned nb = (unsigned)std::min<long long>(f.ntiles, (long long)num_sms_ * per_sm);
-            switch (g.Pc) {
-                case 1: launch(pdl_, k_bwd_fast<R, I, 1>, dim3(nb), dim3(2 * kTileSlots), (size_t)bytes, st, dg, (const unsigned char*)at<unsigned char>(plan.pool), f); break;
-                case 2: launch(pdl_, k_bwd_fast<R, I, 2>, dim3(nb), dim3(2 * kTileSlots), (size_t)bytes, st, dg, (const unsigned char*)at<unsigned char>(plan.pool), f); break;
-                case 3: launch(pdl_, k_bwd_fast<R, I, 3>, dim3(nb), dim3(2 * kTileSlots), (size_t)bytes, st, dg, (const unsigned char*)at<unsigned char>(plan.pool), f); break;
-                default: launch(pdl_, k_bwd_fast<R, I, 4>, dim3(nb), dim3(2 * kTileSlots), (size_t)bytes, st, dg, (const unsigned char*)at<unsigned char>(plan.pool), f); break;
             }
             return;
         }
@@ -1984,7 +1843,6 @@ struct Solver final : SolverBase {
         const Game& g = *gp;
         if (g.tile_ptr[L + 1] <= g.tile_ptr[L]) return 0;
         if (use_stream_ && stream_[L].ntiles > 0) return 3;
-        if (sizeof(R) == 8 && use_fast_ && fast_[L].recsize > 0) return 2;
         return 1;
     }
     cfr_status read_lcnt(std::vector<unsigned long long>& c) {
