@@ -27,7 +27,8 @@ struct StreamLevel {
     int stages, stage_bytes;
     int o_rows, o_reach, o_sig, o_reg, o_snum, o_sden, o_own, o_hs, o_node;   // byte offsets inside a stage
     int fused;              // 1: deepest decision level -- its forward pass (Eq 2 / Eq 4) is fused here
-    int o_pact, o_gsig;     // fused: parent actors, gathered incoming-edge sigma (reach area = parent rows)
+    int o_pact, o_fpar, o_fe;   // fused: parent actors, parent slots, incoming sigma_ext edges (TMA); the
+                                // reach area holds the consumers' (pi_check, pi_hat) of the actor
     unsigned ndiv_m;        // p / n == (p * ndiv_m) >> ndiv_s (64-bit) for p < 2^16 (host-verified)
     int ndiv_s;
     int umem;               // > 0: every infoset of the level has umem members (m / umem by udiv)
@@ -121,6 +122,7 @@ struct StreamHdr {
     int k0, nseg, m0, M;        // first infoset (level-relative), infosets, first member, members
     int po, ho, oo, hso;        // element offsets inside the windows: pairs, S_den, owner, hs
     int no, pao, ro, rro;       // node-row / parent-actor / child-row / reach-row window offsets
+    int fpo, feo;               // fused: parent-slot / edge window offsets
 };
 
 #ifndef CFR_STREAM_MINB
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
     pdl_trigger();
     if (tid == 0) {
         for (int s = 0; s < L.stages; ++s) {
-            mbar_init(&full[s], L.fused ? 33 : 1);   // fused: + the producer lanes' cp.async arrivals
+            mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -154,28 +156,13 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
 
     if (tid >= kStreamConsumers) {
         // ------------------------------------------------------------ producer
-        // Lane 0 arms the stage and issues the TMA bulk copies.  On the fused level
-        // all 32 lanes also gather each member's parent reach row and incoming-edge
-        // sigma (cp.async, completion counted on the same barrier); the parent /
-        // edge indices of the next tile are prefetched into registers meanwhile.
+        // Lane 0 arms the stage and issues the TMA bulk copies.
         const int plane = tid - kStreamConsumers;
-        if (!L.fused && plane != 0) return;   // lane 0 alone issues
+        if (plane != 0) return;   // lane 0 alone issues
         const int4* recs = reinterpret_cast<const int4*>(pool) + L.rec;
         const int* hs = pool + L.hs;
-        constexpr int GMAX = kStreamConsumers / 32;   // members per lane (maxm <= kStreamConsumers)
         long long t = blockIdx.x;
         int4 rec = (t < L.ntiles) ? recs[t] : make_int4(0, 0, 0, 0);
-        long long fp[GMAX], fe[GMAX];
-        auto prefetch = [&](const int4& r) {
-#pragma unroll
-            for (int q = 0; q < GMAX; ++q) {
-                const int m = q * 32 + plane;
-                const long long s = L.s0 + r.z + m;
-                fp[q] = (m < r.w - r.z) ? (long long)g.f_parent[s] : 0;
-                fe[q] = (m < r.w - r.z) ? (long long)g.f_e[s] : 0;
-            }
-        };
-        if (L.fused && t < L.ntiles) prefetch(rec);
         int st = 0;
         unsigned ph = 0;   // ring pass (parity of the empty barrier's phase to wait for)
         for (int it = 0; t < L.ntiles; ++it, t += G) {
@@ -186,15 +173,21 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
             const int k0 = cur.x, k1 = cur.y, m0 = cur.z, m1 = cur.w;
             const int nseg = k1 - k0, M = m1 - m0;
             const long long slot = L.s0 + m0;
-            if (plane == 0) {
+            {
                 const long long q = L.q0 + (long long)k0 * n;
                 const long long h = L.h0 + k0;
-                unsigned b_rows, b_reach = 0, b_sig, b_reg, b_snum, b_sden, b_own, b_hs, b_node, b_pact = 0;
-                int o_rows, o_reach = 0, po, po2, po3, ho, oo, hso, no, pao = 0;
+                unsigned b_rows, b_reach = 0, b_sig, b_reg, b_snum, b_sden, b_own, b_hs, b_node, b_pact = 0, b_fpar = 0, b_fe = 0;
+                int o_rows, o_reach = 0, po, po2, po3, ho, oo, hso, no, pao = 0, fpo = 0, feo = 0;
+                const unsigned char* w_fpar = nullptr;
+                const unsigned char* w_fe = nullptr;
                 const unsigned char* w_rows = window16(g.U + (L.row0 + (long long)m0 * n) * PC, (long long)M * L.rowlen, &b_rows, &o_rows);
                 const unsigned char* w_reach = nullptr;
                 const unsigned char* w_pact = nullptr;
-                if (L.fused) w_pact = window16(g.f_pact + slot, M, &b_pact, &pao);
+                if (L.fused) {
+                    w_pact = window16(g.f_pact + slot, M, &b_pact, &pao);
+                    w_fpar = window16(g.f_parent + slot, M, &b_fpar, &fpo);
+                    w_fe = window16(g.f_e + slot, M, &b_fe, &feo);
+                }
                 else if (L.compact) w_reach = window16(g.reach + L.s0 * 2 * P + (long long)m0 * 2, (long long)M * 2, &b_reach, &o_reach);
                 else w_reach = window16(g.reach + slot * 2 * P, (long long)M * 2 * P, &b_reach, &o_reach);
                 const unsigned char* w_sig = window16(g.sig + q, (long long)nseg * n, &b_sig, &po);
@@ -217,16 +210,24 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 hd->pao = pao;
                 hd->ro = o_rows;
                 hd->rro = o_reach;
+                hd->fpo = fpo;
+                hd->feo = feo;
                 (void)po2; (void)po3;   // sigma / R / S_num share the pair window offset (same base alignment)
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 if (STREAM_DEBUG(L) == 2) {   // timing experiment: no loads (consumers compute on stale data)
                     mbar_expect_tx(&full[st], 0);
                 } else {
-                    mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs + b_node + b_pact);
+                    mbar_expect_tx(&full[st], b_rows + b_reach + b_sig + b_reg + b_snum + b_sden + b_own + b_hs + b_node +
+                                                  b_pact + b_fpar + b_fe);
                     bulk_g2s(S + L.o_node, w_node, b_node, &full[st]);
                     bulk_g2s(S + L.o_rows, w_rows, b_rows, &full[st]);
-                    if (L.fused) bulk_g2s(S + L.o_pact, w_pact, b_pact, &full[st]);
-                    else bulk_g2s(S + L.o_reach, w_reach, b_reach, &full[st]);
+                    if (L.fused) {
+                        bulk_g2s(S + L.o_pact, w_pact, b_pact, &full[st]);
+                        bulk_g2s(S + L.o_fpar, w_fpar, b_fpar, &full[st]);
+                        bulk_g2s(S + L.o_fe, w_fe, b_fe, &full[st]);
+                    } else {
+                        bulk_g2s(S + L.o_reach, w_reach, b_reach, &full[st]);
+                    }
                     bulk_g2s(S + L.o_sig, w_sig, b_sig, &full[st]);
                     bulk_g2s(S + L.o_reg, w_reg, b_reg, &full[st]);
                     bulk_g2s(S + L.o_snum, w_snum, b_snum, &full[st]);
@@ -234,28 +235,6 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                     bulk_g2s(S + L.o_own, w_own, b_own, &full[st]);
                     bulk_g2s(S + L.o_hs, w_hs, b_hs, &full[st]);
                 }
-            }
-            if (L.fused) {
-                // gathers: parent reach row (2P values, 16-byte pieces) and sigma of
-                // the incoming edge, per member, into the stage
-                constexpr int RB = 2 * 2 * (int)sizeof(R);   // P = 2 fast path is the common case
-                R* prow = reinterpret_cast<R*>(S + L.o_reach);
-                R* gsig = reinterpret_cast<R*>(S + L.o_gsig);
-                const int rowb = 2 * P * (int)sizeof(R);
-                (void)RB;
-#pragma unroll
-                for (int q = 0; q < GMAX; ++q) {
-                    const int m = q * 32 + plane;
-                    if (m < M) {
-                        const unsigned char* src = reinterpret_cast<const unsigned char*>(g.reach + fp[q] * 2 * P);
-                        unsigned char* dst = reinterpret_cast<unsigned char*>(prow + (long long)m * 2 * P);
-                        for (int c = 0; c < rowb; c += 16) cp_async<16>(dst + c, src + c);
-                        cp_async<(int)sizeof(R)>(gsig + m, g.sig + fe[q]);
-                    }
-                }
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[st]))
-                             : "memory");
-                if (t + G < L.ntiles) prefetch(rec);
             }
             if (++st == L.stages) { st = 0; ++ph; }
         }
@@ -297,7 +276,7 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
     bool bad = false;
     const bool all_live = g.variant >= 2;   // discounting changes every infoset: no identity updates
     const R inv_n = (R)1 / (R)n;   // uniform strategy of the level's infosets (Eq 9, z = 0)
-    const int rs = L.compact ? 2 : 2 * P;   // reach row stride in the stage (elements)
+    const int rs = (L.compact || L.fused) ? 2 : 2 * P;   // reach row stride in the stage (elements)
     unsigned long long live_h = 0, all_h = 0;   // updated / visited infosets (thread 0)
     long long t = blockIdx.x;
     int st = 0;
@@ -321,7 +300,8 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
         const int* hs = reinterpret_cast<const int*>(S + L.o_hs) + hd.hso;   // level-relative member starts
         const I* snode = reinterpret_cast<const I*>(S + L.o_node) + hd.no;   // U rows of the members
         const unsigned char* pact = reinterpret_cast<const unsigned char*>(S + L.o_pact) + hd.pao;   // fused only
-        const R* gsig = reinterpret_cast<const R*>(S + L.o_gsig);                                  // fused only
+        const I* fpar = reinterpret_cast<const I*>(S + L.o_fpar) + hd.fpo;                         // fused only
+        const I* fedge = reinterpret_cast<const I*>(S + L.o_fe) + hd.feo;                          // fused only
         const int nseg = hd.nseg, M = hd.M, m0 = hd.m0;
 
         if (STREAM_DEBUG(L) == 1) {   // timing experiment: data movement only
@@ -352,6 +332,19 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                         if (hs[mid] - m0 <= m) lo = mid; else hi = mid - 1;
                     }
                     k = lo;
+                }
+                // fused forward (Eq 2 pi_check, Eq 4 pi_hat with reading Q1, the k_fwd
+                // arithmetic): the actor's two factors of the parent's reach row and
+                // the incoming edge's sigma are loaded now, in flight during the value pass
+                R fpc = (R)0, fph = (R)0, fx = (R)0;
+                int fact = 0;
+                if (L.fused) {
+                    const int ia = own[k];
+                    const R* prow = g.reach + (long long)fpar[m] * 2 * P;
+                    fpc = __ldg(prow + ia - 1);
+                    fph = __ldg(prow + P + ia - 1);
+                    fx = __ldg(g.sig + (long long)fedge[m]);
+                    fact = pact[m];
                 }
                 R v[PC];
 #pragma unroll
@@ -465,17 +458,12 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                 }
                 const int i = own[k];
                 if (L.fused) {
-                    // forward pass of this member (Eq 2 pi_check and Eq 4 pi_hat, reading
-                    // Q1; the k_fwd arithmetic) from its gathered parent row and edge
-                    // sigma; the actor's two factors replace the parent row in place
-                    R* prow = const_cast<R*>(reach) + (long long)m * 2 * P;
-                    const R x = gsig[m];
-                    const int act = pact[m];
-                    const R pcp = prow[i - 1], php = prow[P + i - 1];
-                    pc = (act != i) ? pcp * x : pcp;
-                    ph = (act == i) ? php * x : php;
-                    prow[0] = pc;
-                    prow[1] = ph;
+                    // the member's (pi_check, pi_hat) of the actor, kept for phase B
+                    pc = (fact != i) ? fpc * fx : fpc;
+                    ph = (fact == i) ? fph * fx : fph;
+                    R* rw = const_cast<R*>(reach) + (long long)m * 2;
+                    rw[0] = pc;
+                    rw[1] = ph;
                 } else {
                     pc = reach[(long long)m * rs + (L.compact ? 0 : i - 1)];
                     ph = reach[(long long)m * rs + (L.compact ? 1 : P + i - 1)];

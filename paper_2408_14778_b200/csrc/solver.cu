@@ -205,7 +205,7 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int ix, int stages
     const int maxpairs = f.maxm > 0 ? f.maxseg * f.n : 0;
     int o = al(sizeof(StreamHdr));
     f.o_rows = o; o += al((long long)f.maxm * f.rowlen * w + 16);
-    f.o_reach = o; o += al((long long)f.maxm * 2 * P * w + 16);
+    f.o_reach = o; o += al((long long)f.maxm * (f.fused ? 2 : 2 * P) * w + 16);   // fused: consumer-written (pc, ph)
     f.o_sig = o; o += al((long long)maxpairs * w + 16);
     f.o_reg = o; o += al((long long)maxpairs * w + 16);
     f.o_snum = o; o += al((long long)maxpairs * w + 16);
@@ -214,7 +214,8 @@ static void stream_plan(StreamLevel& f, int P, int Pc, int w, int ix, int stages
     f.o_hs = o; o += al((long long)(f.maxseg + 1) * 4 + 16);
     f.o_node = o; o += al((long long)f.maxm * ix + 16);
     f.o_pact = o; o += f.fused ? al((long long)f.maxm + 16) : 0;
-    f.o_gsig = o; o += f.fused ? al((long long)f.maxm * w) : 0;
+    f.o_fpar = o; o += f.fused ? al((long long)f.maxm * ix + 16) : 0;
+    f.o_fe = o; o += f.fused ? al((long long)f.maxm * ix + 16) : 0;
     f.stages = stages;
     f.stage_bytes = o;
     int x = stages * o;
@@ -351,7 +352,7 @@ static std::vector<StreamLevel> stream_levels(const Game& g, const std::vector<i
         }
         // the deepest decision level: no decision children, so no other forward
         // level reads its reach rows -- its forward pass runs inside this kernel
-        f.fused = (fuse_forward && L == g.D - 1 && f.maxm <= kStreamConsumers && (2 * P * w) % 16 == 0) ? 1 : 0;   // gathers: <= 8 per lane, 16-byte pieces
+        f.fused = (fuse_forward && L == g.D - 1) ? 1 : 0;
         f.level = L;
         f.compact = (!f.fused && P == 2 && L == g.D - 1 && compact_reach) ? 1 : 0;
         stream_plan(f, P, Pc, w, ix, stages);
