@@ -98,3 +98,12 @@ def test_bench_shaped_default_flags(cuda):
     """The same tree in the default configuration (the planner's own kernel choice)."""
     desc = _bench_shaped((4, 3, 4), seed=2)
     run_pair(desc, 1, 64, 20)
+
+
+@pytest.mark.parametrize("precision,T", [(64, 20), (32, 10)])
+def test_goofspiel6_paper_scale(cuda, precision, T):
+    """Goofspiel with 6 cards (2.0M nodes, the second real workload at the scale of
+    the paper's Experiment 2): default kernel choice (streaming levels included),
+    bit-identical to the oracle."""
+    out, s, _ = run_pair(gamegen.goofspiel(6), 1, precision, T)
+    assert "k_bwd_stream" in s.level_kernels()
