@@ -593,9 +593,32 @@ struct Solver final : SolverBase {
                 for (int64_t t = g.tile_ptr[L]; t < g.tile_ptr[L + 1]; ++t)
                     for (int k = g.tiles[t].seg0; k < g.tiles[t].seg1; ++k)
                         first[g.segs[k].h] = std::min(first[g.segs[k].h], L);
+            // a rank sees only its own members: the shallowest level of every
+            // deferred infoset is the minimum over the ranks (one all-reduce at
+            // creation), so every rank derives the same ranges and issues the same
+            // sequence of collectives
+            const size_t ndef = g.deferred_list.size();
+            std::vector<int> fl(ndef + 1, INT32_MAX);
+            for (size_t d = 0; d < ndef; ++d) fl[d] = first[g.deferred_list[d]];
+            {
+                int* dfl = nullptr;
+                CU(cudaMalloc(&dfl, fl.size() * sizeof(int)));
+                cudaError_t ce = cudaMemcpyAsync(dfl, fl.data(), fl.size() * sizeof(int), cudaMemcpyHostToDevice, stream);
+                ncclResult_t nr = ncclSuccess;
+                if (!ce) nr = ncclAllReduce(dfl, dfl, fl.size(), ncclInt32, ncclMin, comm, stream);
+                if (!ce && nr == ncclSuccess)
+                    ce = cudaMemcpyAsync(fl.data(), dfl, fl.size() * sizeof(int), cudaMemcpyDeviceToHost, stream);
+                if (!ce) ce = cudaStreamSynchronize(stream);
+                cudaFree(dfl);
+                if (nr != ncclSuccess) {
+                    cfrb_set_error(std::string("ncclAllReduce: ") + ncclGetErrorString(nr));
+                    return CFR_ERR_NCCL;
+                }
+                CU(ce);
+            }
             std::vector<int64_t> lo(g.D, INT64_MAX), hi(g.D, -1);
-            for (size_t d = 0; d < g.deferred_list.size(); ++d) {
-                const int L = first[g.deferred_list[d]];
+            for (size_t d = 0; d < ndef; ++d) {
+                const int L = fl[d];
                 if (L == INT32_MAX) continue;
                 lo[L] = std::min(lo[L], (int64_t)d);
                 hi[L] = std::max(hi[L], (int64_t)d + 1);
