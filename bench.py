@@ -181,6 +181,22 @@ PAPER_MS = {("kuhn", 64): 3.319, ("kuhn", 32): 3.362, ("leduc", 64): 6.269, ("le
             ("battleship11", 64): 856.541, ("battleship11", 32): 446.369}
 
 
+def shard_dir(V: int) -> str:
+    """Directory for the per-rank shard files (≈ 15.5 bytes per node in total):
+    $CFR_SHARD_DIR, else the first of /dev/shm, /tmp with room for them."""
+    if os.environ.get("CFR_SHARD_DIR"):
+        return os.environ["CFR_SHARD_DIR"]
+    need = int(16 * V * 1.2)
+    for d in ("/dev/shm", "/tmp"):
+        try:
+            st = os.statvfs(d)
+            if st.f_bavail * st.f_frsize >= need:
+                return d
+        except OSError:
+            continue
+    return "/tmp"
+
+
 def host_info():
     model = None
     try:
@@ -382,7 +398,11 @@ def main():
         del desc
         nid = None
     else:
-        prefix = os.path.join(os.environ.get("CFR_SHARD_DIR", "/tmp"), f"cfr_synth_n{args.n_types}")
+        # rank 0 picks the directory (free space) and tells the others
+        pbox = [os.path.join(shard_dir(gamegen.synthetic_counts(args.n_types)["V"]), f"cfr_synth_n{args.n_types}")
+                if rank == 0 else None]
+        dist.broadcast_object_list(pbox, src=0)
+        prefix = pbox[0]
         files = [f"{prefix}.r{r}of{world}.cfrshard" for r in range(world)]
         if rank == 0 and not all(os.path.exists(f) for f in files):
             desc = gamegen.synthetic(n_types=args.n_types, seed=0)
@@ -491,7 +511,7 @@ def main():
         variants = synthetic_variants(pb, torch, game, dev, others, args.variant_steps)
 
     games = None
-    if rank == 0 and not args.no_games:
+    if rank == 0 and world == 1 and not args.no_games:
         games = per_game(pb, torch, with_oracle=not args.no_cpu)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -524,6 +544,13 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
+        if rank == 0 and not os.environ.get("CFR_SHARD_DIR"):
+            for f in files:   # the shard files are scratch (≈ 15 GB for configs[4])
+                try:
+                    os.remove(f)
+                except OSError:
+                    pass
         dist.destroy_process_group()
     return 0
 
