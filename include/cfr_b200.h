@@ -195,6 +195,15 @@ cfr_status cfr_solver_current_strategy(cfr_solver* s, double* out /* [Q+] */);
 /* Raw state for checkpoint/inspection: cumulative regrets R [Q+], S_num [Q+],
  * S_den [H+] (caller order).  Any pointer may be NULL. */
 cfr_status cfr_solver_get_state(cfr_solver* s, double* regret, double* s_num, double* s_den);
+/* Resume from a checkpoint (SURVEY.md §5 checkpoint/resume): T iterations done, the
+ * cumulative regrets R and average-strategy sums S_num (caller (h, a) order, [Q+])
+ * and S_den (caller infoset order, [H+]), as cfr_solver_get_state returned them.
+ * The current strategy is set to the regret matching of R (Eq 9), which
+ * is what every update rule leaves after an iteration, so a restored solver
+ * continues bit-identically to one that never stopped.  Values are rounded once to
+ * the working precision.  Blocking.  CFR_ERR_INVALID_ARG on T < 0 or NULL. */
+cfr_status cfr_solver_set_state(cfr_solver* s, int64_t T, const double* regret, const double* s_num,
+                                const double* s_den);
 
 #define CFR_EV_AVERAGE 0
 #define CFR_EV_CURRENT 1

@@ -228,6 +228,17 @@ class Solver:
         _native.check(self._L.cfr_solver_get_state(self._h, _ptr(r), _ptr(sn), _ptr(sd)))
         return dict(regret=r, snum=sn, sden=sd)
 
+    def set_state(self, T: int, regret, snum, sden) -> "Solver":
+        """Resume from a checkpoint: T iterations done and the state() arrays
+        (include/cfr_b200.h cfr_solver_set_state)."""
+        r = np.ascontiguousarray(regret, dtype=np.float64)
+        sn = np.ascontiguousarray(snum, dtype=np.float64)
+        sd = np.ascontiguousarray(sden, dtype=np.float64)
+        if r.shape != (self.Q,) or sn.shape != (self.Q,) or sd.shape != (self.H,):
+            raise ValueError(f"state shapes must be ({self.Q},), ({self.Q},), ({self.H},)")
+        _native.check(self._L.cfr_solver_set_state(self._h, int(T), _ptr(r), _ptr(sn), _ptr(sd)))
+        return self
+
     def expected_values(self, which: str = "average") -> np.ndarray:
         if which not in ("average", "current"):
             raise ValueError(f"which must be 'average' or 'current', not {which!r}")

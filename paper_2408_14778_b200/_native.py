@@ -122,6 +122,7 @@ SIGNATURES = {
     "cfr_solver_average_strategy": (ctypes.c_int, [_P, _P]),
     "cfr_solver_current_strategy": (ctypes.c_int, [_P, _P]),
     "cfr_solver_get_state": (ctypes.c_int, [_P, _P, _P, _P]),
+    "cfr_solver_set_state": (ctypes.c_int, [_P, ctypes.c_int64, _P, _P, _P]),
     "cfr_solver_expected_values": (ctypes.c_int, [_P, _I32, _P]),
     "cfr_solver_exploitability": (ctypes.c_int, [_P, _P, _P, _P]),
     "cfr_solver_launches_per_iteration": (ctypes.c_int, [_P, _P]),

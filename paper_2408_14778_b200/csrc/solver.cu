@@ -78,6 +78,7 @@ struct SolverBase {
     virtual cfr_status iteration(int64_t* T) = 0;
     virtual cfr_status strategy(int which, double* out) = 0;   // 0 avg, 1 current
     virtual cfr_status get_state(double* regret, double* snum, double* sden) = 0;
+    virtual cfr_status set_state(int64_t T, const double* regret, const double* snum, const double* sden) = 0;
     virtual cfr_status expected_values(int which, double* out) = 0;
     virtual cfr_status exploitability(double* nc, double* ex, double* br) = 0;
     virtual cfr_status launches(int64_t* n) = 0;
@@ -1438,6 +1439,44 @@ struct Solver final : SolverBase {
         return CFR_OK;
     }
 
+    // Resume (checkpoint restore): T iterations done, R, S_num (caller (h, a)
+    // order), S_den (caller infoset order).  The current strategy is the regret
+    // matching of R (Eq 9, z summed in ascending action order, uniform when z = 0)
+    // -- what every update rule leaves after its iteration -- computed here with
+    // the kernels' operations, so a restored solver continues bit for bit.
+    cfr_status set_state(int64_t T, const double* regret, const double* snum, const double* sden) override {
+        const Game& g = *gp;
+        CU(cudaStreamSynchronize(stream));
+        std::vector<R> r(g.Q), sn(g.Q), sd(g.H), sg(g.Q);
+        for (int64_t hc = 0; hc < g.H; ++hc) {
+            const int64_t hi = g.h_int_of_caller[hc];
+            const int64_t n = g.qbase_caller[hc + 1] - g.qbase_caller[hc];
+            for (int64_t a = 0; a < n; ++a) {
+                r[g.qbase_int[hi] + a] = (R)regret[g.qbase_caller[hc] + a];
+                sn[g.qbase_int[hi] + a] = (R)snum[g.qbase_caller[hc] + a];
+            }
+            sd[hi] = (R)sden[hc];
+        }
+        for (int64_t h = 0; h < g.H; ++h) {
+            const int64_t q0 = g.qbase_int[h], q1 = g.qbase_int[h + 1];
+            R z = (R)0;
+            for (int64_t q = q0; q < q1; ++q) z = z + ((r[q] > (R)0) ? r[q] : (R)0);
+            for (int64_t q = q0; q < q1; ++q) {
+                const R pos = (r[q] > (R)0) ? r[q] : (R)0;
+                sg[q] = (z > (R)0) ? pos / z : (R)1 / (R)(q1 - q0);
+            }
+        }
+        cfr_status st;
+        if ((st = up(plan.regret, r))) return st;
+        if ((st = up(plan.snum, sn))) return st;
+        if ((st = up(plan.sden, sd))) return st;
+        if (g.Q) CU(cudaMemcpyAsync(ws + plan.sig, sg.data(), g.Q * sizeof(R), cudaMemcpyHostToDevice, stream));
+        std::vector<long long> ctrl = {(long long)T, LLONG_MAX, 0, 0, 0, 0, 0, 0};
+        if ((st = up(plan.ctrl, ctrl))) return st;
+        CU(cudaStreamSynchronize(stream));
+        return CFR_OK;
+    }
+
     cfr_status read_root(double* out) {
         const Game& g = *gp;
         std::vector<R> r(g.Pc);
@@ -2102,6 +2141,12 @@ cfr_status cfr_solver_run(cfr_solver* s, int64_t iterations) {
     cfr_status st = cfr_solver_enqueue(s, iterations);
     if (st) return st;
     return s->impl->sync();
+}
+cfr_status cfr_solver_set_state(cfr_solver* s, int64_t T, const double* regret, const double* s_num,
+                                const double* s_den) {
+    CHK_S(s);
+    if (T < 0 || !regret || !s_num || !s_den) { cfrb_set_error("bad argument"); return CFR_ERR_INVALID_ARG; }
+    return s->impl->set_state(T, regret, s_num, s_den);
 }
 cfr_status cfr_solver_iteration(cfr_solver* s, int64_t* T) {
     CHK_S(s);

@@ -106,4 +106,5 @@ def test_goofspiel6_paper_scale(cuda, precision, T):
     the paper's Experiment 2): default kernel choice (streaming levels included),
     bit-identical to the oracle."""
     out, s, _ = run_pair(gamegen.goofspiel(6), 1, precision, T)
-    assert "k_bwd_stream" in s.level_kernels()
+    if precision == 64:   # (f32 rows of its widest levels are too short for the streaming tiles)
+        assert "k_bwd_stream" in s.level_kernels()
