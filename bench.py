@@ -197,6 +197,12 @@ def shard_dir(V: int) -> str:
     return "/tmp"
 
 
+# PAPER.md Table 9: seconds to serialize the game into the paper's sparse
+# matrices (context for our generate + flatten + create)
+PAPER_SETUP_S = {"kuhn": 0.010, "leduc": 1.051, "liars_dice": 34.264, "battleship7": 254.096,
+                 "battleship11": 5470.082}
+
+
 def host_info():
     model = None
     try:
@@ -236,9 +242,13 @@ def per_game(pb, torch, with_oracle: bool):
     (latency-bound, L2-resident games: no HBM fraction), the oracle beside each."""
     out = []
     for name, variant, prec, iters, oiters in GAME_LINES:
+        t0 = time.perf_counter()
         d = game_desc(name)
+        t1 = time.perf_counter()
         g = pb.Game(d)
+        t2 = time.perf_counter()
         s = pb.Solver(g, variant=variant, precision=prec)
+        t3 = time.perf_counter()
         s.run(5)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s.stream)
@@ -249,7 +259,10 @@ def per_game(pb, torch, with_oracle: bool):
         e = {"game": name, "variant": variant, "dtype": f"f{prec}", "iterations": iters,
              "it_per_s": round(1e3 / ms, 1), "node_updates_per_s": float(f"{g.V * 1e3 / ms:.4g}"), "V": g.V,
              "launches_per_iter": s.launches_per_iteration(), "kernels": sorted({k for k in s.level_kernels() if k})
-             if s.launches_per_iteration() > 1 else ["k_tiny"]}
+             if s.launches_per_iteration() > 1 else ["k_tiny"],
+             "setup_s": {"generate": round(t1 - t0, 3), "flatten": round(t2 - t1, 3), "solver_create": round(t3 - t2, 3)}}
+        if name in PAPER_SETUP_S:
+            e["setup_s"]["paper"] = PAPER_SETUP_S[name]
         del s
         if with_oracle:
             import oracle
