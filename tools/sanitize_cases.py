@@ -42,6 +42,19 @@ if not FAST:
     o = oracle.Oracle(d, precision=64).run(2, 1)
     assert np.array_equal(out["cur"], o.state()["sigma"])
     print("ok goofspiel sharded world 2", flush=True)
+    # rank-spanning levels on the streaming kernel (deferred mode), world 2
+    d = gamegen.synthetic(n_types=4, c=(3, 2, 3, 2), seed=2)
+    out = run_world(d, pb.CFR_PLUS, 64, 2, 2, br=False, flags=pb.FLAG_FORCE_STREAM)
+    o = oracle.Oracle(d, precision=64).run(2, 1)
+    assert np.array_equal(out["cur"], o.state()["sigma"])
+    print("ok synthetic sharded world 2 (deferred streaming levels)", flush=True)
+    # checkpoint / resume
+    g = pb.Game(gamegen.leduc())
+    a = pb.Solver(g, variant="cfr+", precision=64).run(5)
+    st = a.state()
+    b = pb.Solver(g, variant="cfr+", precision=64)
+    b.set_state(5, st["regret"], st["snum"], st["sden"]).run(2)
+    print("ok resume", flush=True)
 # release every solver and the caching allocator's blocks so memcheck's leak check
 # reports only real leaks
 import gc  # noqa: E402
