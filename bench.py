@@ -391,6 +391,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        # a collective that never completes must fail the run, not hang it: the
+        # library's NCCL communicator has no timeout of its own
+        def _watchdog():
+            time.sleep(float(os.environ.get("CFR_BENCH_TIMEOUT_S", "1500")))
+            print(f"[rank {rank}] bench watchdog: no completion, aborting", file=sys.stderr, flush=True)
+            os._exit(3)
+        threading.Thread(target=_watchdog, daemon=True).start()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
