@@ -141,6 +141,12 @@ typedef struct {
                          /* (k_tiny, default when the state fits one CTA); bit 8: */
                          /* 64-bit device indices even when 32 bits suffice       */
                          /* (they are used automatically for >= 2^31 entries)     */
+                         /* bit 9: disable the subtree kernel (k_sub: the levels  */
+                         /* below a cut in one launch, subtree state in shared    */
+                         /* memory, exact int64 infoset sums; default for         */
+                         /* single-GPU games of <= 2^22 nodes that k_tiny does    */
+                         /* not take); bit 10: the subtree    */
+                         /* kernel even where k_tiny fits                         */
     int32_t reserved;
 } cfr_solver_config;
 
@@ -153,6 +159,8 @@ typedef struct {
 #define CFR_FLAG_FUSED_FORWARD 64
 #define CFR_FLAG_NO_TINY 128
 #define CFR_FLAG_INDEX64 256
+#define CFR_FLAG_NO_SUBTREE 512   /* do not use the subtree kernel (k_sub) */
+#define CFR_FLAG_FORCE_SUBTREE 1024   /* subtree kernel even where k_tiny fits */
 
 /* Multi-GPU level sharding.  NULL or world_size == 1 means a
  * single GPU.  nccl_unique_id points to the 128-byte ncclUniqueId that rank 0

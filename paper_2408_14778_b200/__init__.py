@@ -40,6 +40,8 @@ FLAG_FORCE_STREAM = 32
 FLAG_FUSED_FORWARD = 64
 FLAG_NO_TINY = 128
 FLAG_INDEX64 = 256
+FLAG_NO_SUBTREE = 512
+FLAG_FORCE_SUBTREE = 1024
 
 
 def _ptr(a: np.ndarray) -> ctypes.c_void_p:
@@ -316,7 +318,7 @@ class Solver:
         keys = ("cut", "n_cut", "owned_nodes", "local_nodes", "local_decision", "deferred", "deferred_pairs", "world")
         return {k: int(v) for k, v in zip(keys, out)}
 
-    KERNEL_NAMES = {0: None, 1: "k_bwd", 2: "k_bwd_fast", 3: "k_bwd_stream"}
+    KERNEL_NAMES = {0: None, 1: "k_bwd", 2: "k_bwd_fast", 3: "k_bwd_stream", 4: "k_sub"}
 
     def level_kernels(self) -> list:
         """Backward kernel of each parent level (include/cfr_b200.h cfr_solver_level_kernels)."""

@@ -1,0 +1,212 @@
+// Subtree kernel: forward + backward of the subtrees below a
+// cut level in ONE launch, their state in shared memory; k_sub_update.
+// Part of the single translation unit solver.cu (included from it only).
+#pragma once
+
+namespace cfrb {
+
+// ------------------------------------------------------------ subtree fusion
+// P:401 partitions the root-to-leaf paths into subgraphs processed separately;
+// P:403 chunks the tree into a trunk and subtrees.  Below a cut level c every
+// non-terminal node of depth c roots a subtree; one CTA runs the subtree's whole
+// forward pass (Eq 2 / Eq 4, reading Q1) and backward pass (Eq 1) with the reach
+// factors, node values and terminal utilities of the subtree in shared memory and
+// levels separated by __syncthreads -- instead of 2(D - c) level launches, each a
+// dependent chain through global memory.  Infosets span subtrees (imperfect
+// information), so their regret terms (Eq 7, cancelled form) and pi_hat terms
+// (Eq 5) are added as exact 40-bit slices to int64 accumulators
+// with global atomics: integer sums, so the result does not depend on the order
+// in which subtrees add them.  k_sub_update then decodes the sums and applies the
+// update of every infoset below the cut (Eq 8/15 or CFR+, Eq 10, Eq 9: the
+// operations and order of k_deferred).  The trunk (depths < c) keeps the level
+// kernels; the roots' values are written to their U rows for it.
+//
+// Tables (int32, built once on the host from the device slot tables, so both
+// paths read the same numbers):
+//   per subtree b (kSubMeta ints): node0, nodes, term0, terms, lvl0 (offset of its
+//     per-level node starts), levels, pair_lvl0 (offset of its per-level pair
+//     starts), root slot; the per-level starts are local indices
+//   per local node (kSubRec ints, global index node0 + j): local parent (-1 root),
+//     sigma_ext index of the incoming edge, parent actor, own actor (0 chance),
+//     sigma_ext base of its children's edges, children, first entry in the child
+//     table, internal infoset (-1 chance)
+//   child table: >= 0 local node, < 0 -(1 + k) = the subtree's k-th terminal
+//   pair table (global index pair0 of the subtree + k): local node << 8 | action
+// Terminal utilities in subtree order: tu[(term0 + k) * Pc + j].
+constexpr int kSubMeta = 8;
+constexpr int kSubRec = 8;
+constexpr int kSubThreads = 512;
+
+struct SubPlan {
+    int nsub;          // subtrees (= CTAs)
+    int cut;           // cut level c
+    long long hc, qc;  // first internal infoset / pair below the cut (accumulator bases)
+    long long nh, nq;  // infosets / pairs below the cut
+    int bytes;         // dynamic shared memory
+    int m_sub, m_rec, m_child, m_pair, m_lvl;   // int offsets inside the table block
+};
+
+template <class R, class I, int PC>
+__global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __restrict__ T, const R* __restrict__ tu,
+                                                     unsigned long long* __restrict__ acc, SubPlan sp) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int b = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
+    const int P = g.P;
+    const int* const mb = T + sp.m_sub + kSubMeta * b;
+    const int node0 = mb[0], nn = mb[1], term0 = mb[2], nt = mb[3], lvl0 = mb[4], nlev = mb[5], plv0 = mb[6];
+    const int root_slot = mb[7];
+    const int* const rec = T + sp.m_rec + (long long)kSubRec * node0;
+    const int* const chl = T + sp.m_child;
+    const int* const prs = T + sp.m_pair;
+    const int* const lv = T + sp.m_lvl + lvl0;     // [nlev + 1] local node starts per level
+    const int* const plv = T + sp.m_lvl + plv0;    // [nlev + 1] pair-table starts per level (global)
+    R* const reach = reinterpret_cast<R*>(smem_raw);                       // [nn][2P]
+    R* const val = reach + (((long long)nn * 2 * P + 1) & ~1LL);           // [nn][PC]
+    R* const tv = val + (((long long)nn * PC + 1) & ~1LL);                 // [nt][PC] terminal utilities
+    unsigned long long* const acc_r = acc;                                 // [nq][3]
+    unsigned long long* const acc_p = acc + 3 * sp.nq;                     // [nh][3]
+    pdl_trigger();
+    // terminal utilities are constant: staged before the dependency wait
+    for (long long k = tid; k < (long long)nt * PC; k += nth) tv[k] = tu[(long long)term0 * PC + k];
+    pdl_wait();
+    const long long t_iter = g.ctrl[0] + 1;
+    bool bad = false;
+    if (tid < 2 * P) reach[tid] = g.reach[(long long)root_slot * 2 * P + tid];   // level-c forward kernel's row
+    __syncthreads();
+    // ---- forward (Eq 2 / Eq 4 with reading Q1; k_fwd's operations)
+    for (int l = 1; l < nlev; ++l) {
+        for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
+            const int* e = rec + kSubRec * j;
+            const int p = e[0];
+            const R x = g.sig[e[1]];
+            const int act = e[2];
+            for (int i = 0; i < P; ++i) {
+                const R pc = reach[p * 2 * P + i], ph = reach[p * 2 * P + P + i];
+                reach[j * 2 * P + i] = (act != i + 1) ? pc * x : pc;
+                reach[j * 2 * P + P + i] = (act == i + 1) ? ph * x : ph;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- backward, deepest level first
+    for (int l = nlev - 1; l >= 0; --l) {
+        // values (Eq 1: ascending actions from +0)
+        for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
+            const int* e = rec + kSubRec * j;
+            const int eb = e[4], nch = e[5], cp = e[6];
+            R v[PC];
+#pragma unroll
+            for (int c = 0; c < PC; ++c) v[c] = (R)0;
+            for (int a = 0; a < nch; ++a) {
+                const R x = g.sig[eb + a];
+                const int ch = chl[cp + a];
+                const R* u = (ch >= 0) ? val + (long long)ch * PC : tv + (long long)(-1 - ch) * PC;
+#pragma unroll
+                for (int c = 0; c < PC; ++c) v[c] = v[c] + x * u[c];
+            }
+#pragma unroll
+            for (int c = 0; c < PC; ++c) val[(long long)j * PC + c] = v[c];
+        }
+        __syncthreads();
+        // exact slices of the regret terms pi_check * (u(child) - u(node)) of this
+        // level's (node, action) pairs; zero terms are exact zeros and skipped
+        for (int k = plv[l] + tid; k < plv[l + 1]; k += nth) {
+            const int pr = prs[k];
+            const int j = pr >> 8, a = pr & 255;
+            const int* e = rec + kSubRec * j;
+            const int i = e[3];
+            if (g.upd_player != 0 && i != g.upd_player) continue;
+            const R pc = reach[j * 2 * P + (i - 1)];
+            if (pc == (R)0) continue;
+            const int col = (PC == 1) ? 0 : i - 1;
+            const int ch = chl[e[6] + a];
+            const R u = (ch >= 0) ? val[(long long)ch * PC + col] : tv[(long long)(-1 - ch) * PC + col];
+            const R t = pc * (u - val[(long long)j * PC + col]);
+            if (!finite_(t)) bad = true;
+            double c0 = 0, c1 = 0, c2 = 0;
+            xadd(c0, c1, c2, (double)t, g.sc0);
+            if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
+            unsigned long long* ac = acc_r + ((long long)e[4] + a - sp.qc) * 3;
+            if (c0 != 0.0) atomicAdd(ac + 0, (unsigned long long)(long long)c0);
+            if (c1 != 0.0) atomicAdd(ac + 1, (unsigned long long)(long long)c1);
+            if (c2 != 0.0) atomicAdd(ac + 2, (unsigned long long)(long long)c2);
+        }
+        // exact slices of pi_hat (Eq 5 / Eq 10 weights) of this level's player nodes
+        for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
+            const int* e = rec + kSubRec * j;
+            const int i = e[3];
+            if (i == 0 || (g.upd_player != 0 && i != g.upd_player)) continue;
+            const R ph = reach[j * 2 * P + P + (i - 1)];
+            if (ph == (R)0) continue;
+            double c0 = 0, c1 = 0, c2 = 0;
+            xadd(c0, c1, c2, (double)ph, g.scp0);
+            unsigned long long* ac = acc_p + ((long long)e[7] - sp.hc) * 3;
+            if (c0 != 0.0) atomicAdd(ac + 0, (unsigned long long)(long long)c0);
+            if (c1 != 0.0) atomicAdd(ac + 1, (unsigned long long)(long long)c1);
+            if (c2 != 0.0) atomicAdd(ac + 2, (unsigned long long)(long long)c2);
+        }
+        // (no barrier: the next level reads only values written before the last one)
+    }
+    // the root's value into its U row (read by the trunk's backward pass)
+    if (tid < PC) {
+        const long long row = (long long)g.s_node[root_slot];
+        g.U[row * PC + tid] = val[tid];
+    }
+    if (bad) atomicMin(&g.ctrl[1], t_iter);
+}
+
+// Update of every infoset below the cut: decode the exact sums, then Eq 8/15 or
+// CFR+ (or Q18), Eq 10, Eq 9 (k_deferred's operations and order); zero the sums.
+template <class R, class I>
+__global__ void __launch_bounds__(256) k_sub_update(DG<R, I> g, unsigned long long* __restrict__ acc, SubPlan sp) {
+    pdl_trigger();
+    pdl_wait();
+    const long long t_iter = g.ctrl[0] + 1;
+    const Upd<R> up = make_upd<R>(g.variant, t_iter);
+    const R w = up.w;
+    bool bad = false;
+    unsigned long long* const acc_r = acc;
+    unsigned long long* const acc_p = acc + 3 * sp.nq;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < sp.nh; x += stride) {
+        const long long h = sp.hc + x;
+        const long long qb = (long long)g.qbase[h];
+        const int n = (int)((long long)g.qbase[h + 1] - qb);
+        const long long p0 = (long long)acc_p[x * 3 + 0], p1 = (long long)acc_p[x * 3 + 1], p2 = (long long)acc_p[x * 3 + 2];
+        acc_p[x * 3 + 0] = 0;
+        acc_p[x * 3 + 1] = 0;
+        acc_p[x * 3 + 2] = 0;
+        const long long cq0 = qb - sp.qc;
+        if (g.upd_player != 0 && g.owner[h] != g.upd_player) continue;   // alternating: another player's (sums are 0)
+        const R pib = (R)xdec_ll(p0, p1, p2, g.rcp);
+        const R wp = w * pib;
+        R z = (R)0;
+        for (int a = 0; a < n; ++a) {
+            const long long q = qb + a;
+            unsigned long long* ac = acc_r + (cq0 + a) * 3;
+            const long long c0 = (long long)ac[0], c1 = (long long)ac[1], c2 = (long long)ac[2];
+            ac[0] = 0;
+            ac[1] = 0;
+            ac[2] = 0;
+            const R rt = (R)xdec_ll(c0, c1, c2, g.rc);
+            g.regret[q] = upd_regret(up, g.regret[q], rt);
+            g.snum[q] = upd_sum(up, g.snum[q], wp * g.sig[q]);
+            if (!finite_(rt)) bad = true;
+        }
+        g.sden[h] = upd_sum(up, g.sden[h], wp);
+        for (int a = 0; a < n; ++a) {
+            const R r = g.regret[qb + a];
+            z = z + ((r > (R)0) ? r : (R)0);
+        }
+        for (int a = 0; a < n; ++a) {
+            const R r = g.regret[qb + a];
+            const R pos = (r > (R)0) ? r : (R)0;
+            const R nsig = (z > (R)0) ? pos / z : (R)1 / (R)n;
+            g.sig[qb + a] = nsig;
+            if (!finite_(r) || !finite_(nsig) || !finite_(z)) bad = true;
+        }
+    }
+    if (bad) atomicMin(&g.ctrl[1], t_iter);
+}
+
+}  // namespace cfrb

@@ -41,6 +41,7 @@
 #include "kernels/stream.cuh"
 #include "kernels/update.cuh"
 #include "kernels/small.cuh"
+#include "kernels/subtree.cuh"
 
 namespace cfrb {
 
@@ -373,6 +374,19 @@ static size_t stream_pool_bound(const Game& g) { return (size_t)(5 * g.H + 10 * 
 constexpr int kRecRows = 1024;
 static int rec_width(const Game& g) { return g.Pc + g.P * g.Pc + 1; }
 
+// Subtree mode (k_sub, kernels/subtree.cuh): games up to kSubMaxV nodes reserve
+// its tables; at most kSubMaxSub subtrees (CTAs) per cut.
+constexpr int64_t kSubMaxV = int64_t(1) << 22;
+constexpr int64_t kSubMaxSub = 16384;
+constexpr int64_t kSubMinV = 2048;      // default: below this k_tiny (many iterations per launch) wins (Kuhn)
+constexpr int64_t kSubMinCTAs = 24;     // preferred minimum of subtrees (CTAs) when choosing the cut
+static bool sub_candidate(const Game& g) { return g.V <= kSubMaxV && g.D >= 2 && g.NS > 0; }
+// ints: per-subtree records, node records, child entries (<= V), pair entries
+// (<= V), per-level node and pair starts of every subtree
+static size_t sub_table_bound(const Game& g) {
+    return (size_t)(kSubMeta * kSubMaxSub + kSubRec * g.NS + 2 * g.V + 2 * kSubMaxSub * (g.D + 2) + 64);
+}
+
 template <class R, class I>
 struct Plan {
     size_t U, reach, sig, sig_eval, regret, snum, sden, acc_r, acc_p, dqbase;
@@ -380,6 +394,7 @@ struct Plan {
     size_t s_node, s_cb, s_n, s_ebase, s_actor, s_dec, s_coff;
     size_t qbase, owner, tiles, segs, deferred, br_best, ctrl, lcnt, out, rec;
     size_t cutbuf, cutrow, cutown, report, spool, tmeta;
+    size_t subt, subu, suba;   // subtree mode (k_sub): int32 tables, terminal utilities, exact accumulators
     size_t total;
     explicit Plan(const Game& g, const ShardInfo* sh = nullptr) {
         Layout L;
@@ -423,6 +438,11 @@ struct Plan {
         // k_tiny's int32 game tables (TinyMeta), tiny-game candidates only
         tmeta = L.take<int>(g.V <= (int64_t(1) << 20) ? (size_t)(4 * (g.D + 1) + 7 * NS + 4 * H + Q + 16) : 2);
         rec = L.take<double>((size_t)kRecRows * rec_width(g));
+        // subtree mode: reserved for candidate games only (sub_candidate)
+        const bool sc = sub_candidate(g);
+        subt = L.take<int>(sc ? sub_table_bound(g) : 2);
+        subu = L.take<R>(sc ? (size_t)g.V * g.Pc + 2 : 2);
+        suba = L.take<unsigned long long>(sc ? 3 * (Q + H) + 3 : 3);
         total = L.off + 256;
     }
 };
@@ -451,6 +471,8 @@ struct Solver final : SolverBase {
     bool use_graph = true;
     bool tiny_ = false;           // tiny game: whole iterations in one CTA, state in shared memory (k_tiny)
     TinyPlan tiny_plan_{};
+    bool sub_ = false;            // subtree mode: levels >= cut in one k_sub launch + k_sub_update
+    SubPlan sub_plan_{};
     bool use_stream_ = true;
     int stream_debug_ = 0;   // CFR_STREAM_DEBUG (timing experiments; results are garbage when set)
     bool pdl_ = true;
@@ -868,8 +890,11 @@ struct Solver final : SolverBase {
         }
         launches_per_iter = count_launches();
         {
-            cfr_status ps = setup_tiny();
+            // subtree mode first (latency-bound games beyond the tiniest), else k_tiny
+            cfr_status ps = setup_sub();
             if (ps) return ps;
+            if (!sub_ && (ps = setup_tiny())) return ps;
+            if (sub_) launches_per_iter = count_launches();
         }
         if (use_graph && g.NS > 0 && !external) {
             CU(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
@@ -928,7 +953,8 @@ struct Solver final : SolverBase {
     cfr_status setup_tiny() {
         const Game& g = *gp;
         tiny_ = false;
-        if (world > 1 || external || (cfg.flags & CFR_FLAG_NO_TINY) || !g.depth_homogeneous || g.NS == 0)
+        if (world > 1 || external || (cfg.flags & (CFR_FLAG_NO_TINY | CFR_FLAG_FORCE_SUBTREE)) || !g.depth_homogeneous ||
+            g.NS == 0)
             return CFR_OK;
         const long long nU = (long long)(plan_u_rows()) * g.Pc, nreach = 2LL * g.P * g.NS, nsig = g.Q + g.C;
         int dev = 0, optin = 0;
@@ -1071,9 +1097,223 @@ struct Solver final : SolverBase {
         return CFR_OK;
     }
 
+    // Subtree mode (k_sub, kernels/subtree.cuh):
+    // single-GPU, depth-homogeneous games of <= kSubMaxV nodes without deferred
+    // infosets that are not tiny.  The cut is the shallowest level whose every
+    // subtree fits one CTA's shared memory (CFR_SUB_CUT overrides).  On by default
+    // for those games (CFR_FLAG_NO_SUBTREE opts out); CFR_FLAG_FORCE_SUBTREE also
+    // takes games k_tiny would run.
+    void* sub_fn() const {
+        switch (gp->Pc) {
+            case 1: return (void*)k_sub<R, I, 1>;
+            case 2: return (void*)k_sub<R, I, 2>;
+            case 3: return (void*)k_sub<R, I, 3>;
+            default: return (void*)k_sub<R, I, 4>;
+        }
+    }
+    cfr_status setup_sub() {
+        const Game& g = *gp;
+        sub_ = false;
+        // flags that select another kernel family (tests, A/B) keep it unless forced
+        const int other = CFR_FLAG_NO_TINY | CFR_FLAG_NO_STREAM | CFR_FLAG_FORCE_STREAM | CFR_FLAG_FUSED_FORWARD |
+                          CFR_FLAG_INDEX64;
+        const bool forced = (cfg.flags & CFR_FLAG_FORCE_SUBTREE) != 0;
+        if (!forced && (cfg.flags & other)) return CFR_OK;
+        if (!forced) {
+            // default: latency-bound games only -- not the tiniest (k_tiny runs many
+            // iterations per launch there) and none with a level big enough for the
+            // streaming kernel (bandwidth-bound: measured faster on the levels)
+            if (g.V < kSubMinV) return CFR_OK;
+            for (const StreamLevel& f : stream_)
+                if (use_stream_ && f.ntiles > 0) return CFR_OK;
+        }
+        if (world > 1 || external || (cfg.flags & CFR_FLAG_NO_SUBTREE) || !g.depth_homogeneous || !sub_candidate(g) ||
+            !g.deferred_list.empty() || g.Pc > 4)
+            return CFR_OK;
+        const int64_t NS = g.NS;
+        const int P = g.P, Pc = g.Pc, w = (int)sizeof(R);
+        int dev = 0, optin = 0;
+        CU(cudaGetDevice(&dev));
+        CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        const long long budget = optin - 1024;
+        // the device slot tables (the numbers the level kernels use)
+        std::vector<I> fe(NS), cb(NS), eb(NS), nd(NS);
+        std::vector<unsigned char> pa(NS), ac(NS);
+        std::vector<int> nn(NS);
+        const long long nU = plan_u_rows() * Pc;
+        std::vector<R> U((size_t)nU);
+        CU(cudaStreamSynchronize(stream));
+        CU(cudaMemcpy(fe.data(), ws + plan.f_e, NS * sizeof(I), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(pa.data(), ws + plan.f_pact, NS, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(ac.data(), ws + plan.s_actor, NS, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(cb.data(), ws + plan.s_cb, NS * sizeof(I), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(eb.data(), ws + plan.s_ebase, NS * sizeof(I), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(nn.data(), ws + plan.s_n, NS * sizeof(int), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(nd.data(), ws + plan.s_node, NS * sizeof(I), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(U.data(), ws + plan.U, (size_t)nU * sizeof(R), cudaMemcpyDeviceToHost));
+        // U row -> slot (non-terminal rows), slot -> internal infoset
+        std::vector<int64_t> rowslot((size_t)plan_u_rows() + 1, -1);
+        for (int64_t x = 0; x < NS; ++x) rowslot[(size_t)nd[x]] = x;
+        std::vector<int64_t> sh(NS, -1);
+        for (const SegH& sg : g.segs)
+            for (int64_t x = sg.sb; x < sg.se; ++x) sh[x] = sg.h;
+        std::vector<int> lev(NS, 0);
+        for (int L = 0; L < g.D; ++L)
+            for (int64_t x = g.slot_ptr[L]; x < g.slot_ptr[L + 1]; ++x) lev[x] = L;
+        for (int64_t x = 0; x < NS; ++x) {
+            if (ac[x] != 0 && (sh[x] < 0 || (int64_t)eb[x] != g.qbase_int[sh[x]])) return CFR_OK;
+            if (nn[x] > 256) return CFR_OK;
+        }
+        // subtree sizes (non-terminal nodes, terminals), deepest level first
+        std::vector<int64_t> snn(NS, 0), snt(NS, 0);
+        for (int L = g.D - 1; L >= 0; --L)
+            for (int64_t x = g.slot_ptr[L]; x < g.slot_ptr[L + 1]; ++x) {
+                int64_t a = 1, t = 0;
+                for (int k = 0; k < nn[x]; ++k) {
+                    const int64_t c = rowslot[(size_t)cb[x] + k];
+                    if (c >= 0) { a += snn[c]; t += snt[c]; } else ++t;
+                }
+                snn[x] = a;
+                snt[x] = t;
+            }
+        auto bytes_of = [&](int64_t a, int64_t t) {
+            return (((a * 2 * P + 1) & ~1LL) + ((a * Pc + 1) & ~1LL) + t * Pc) * (long long)w;
+        };
+        int cut = -1;
+        long long need = 0;
+        int forced_cut = -1;
+        if (const char* e = std::getenv("CFR_SUB_CUT")) forced_cut = std::atoi(e);
+        // the shallowest cut whose subtrees fit one CTA and give >= kSubMinCTAs CTAs
+        // (else the fitting cut with the most subtrees)
+        int64_t best_n = -1;
+        for (int c = 1; c < g.D; ++c) {
+            const int64_t n = g.slot_ptr[c + 1] - g.slot_ptr[c];
+            if (n <= 0 || n > kSubMaxSub || (forced_cut >= 0 && c != forced_cut)) continue;
+            long long mx = 0;
+            for (int64_t x = g.slot_ptr[c]; x < g.slot_ptr[c + 1]; ++x) mx = std::max(mx, bytes_of(snn[x], snt[x]));
+            if (mx > budget) continue;
+            if (n > best_n) {
+                cut = c;
+                need = mx;
+                best_n = n;
+            }
+            if (n >= kSubMinCTAs) break;
+        }
+        if (cut < 0) return CFR_OK;
+        // infosets below the cut are one id range [hc, H)
+        int64_t hc = g.H;
+        for (int64_t x = g.slot_ptr[cut]; x < NS; ++x)
+            if (sh[x] >= 0) hc = std::min(hc, sh[x]);
+        for (int64_t x = 0; x < g.slot_ptr[cut]; ++x)
+            if (sh[x] >= hc) return CFR_OK;
+        // tables
+        SubPlan sp{};
+        sp.cut = cut;
+        sp.nsub = (int)(g.slot_ptr[cut + 1] - g.slot_ptr[cut]);
+        sp.hc = hc;
+        sp.qc = g.qbase_int[hc];
+        sp.nh = g.H - hc;
+        sp.nq = g.Q - sp.qc;
+        sp.bytes = (int)std::max<long long>(need, 16);
+        std::vector<int> meta, recs, chl, prs, lvl;
+        std::vector<R> tu;
+        meta.reserve((size_t)kSubMeta * sp.nsub);
+        std::vector<int64_t> cur, nxt;
+        for (int64_t root = g.slot_ptr[cut]; root < g.slot_ptr[cut + 1]; ++root) {
+            const int64_t node0 = (int64_t)recs.size() / kSubRec, term0 = (int64_t)tu.size() / Pc;
+            const int64_t lvl0 = (int64_t)lvl.size();
+            std::vector<int> lstart, pstart;
+            cur.assign(1, root);
+            std::vector<int> curpar(1, -1);
+            int64_t nloc = 0, nterm = 0;
+            while (!cur.empty()) {
+                lstart.push_back((int)nloc);
+                pstart.push_back((int)prs.size());
+                nxt.clear();
+                std::vector<int> nxtpar;
+                const int64_t base = nloc;
+                for (size_t k = 0; k < cur.size(); ++k) {
+                    const int64_t x = cur[k];
+                    const int j = (int)(base + (int64_t)k);
+                    const int cp = (int)chl.size();
+                    for (int a = 0; a < nn[x]; ++a) {
+                        const int64_t row = (int64_t)cb[x] + a;
+                        const int64_t c = rowslot[(size_t)row];
+                        if (c >= 0) {
+                            chl.push_back((int)(base + (int64_t)cur.size() + (int64_t)nxt.size()));
+                            nxt.push_back(c);
+                            nxtpar.push_back(j);
+                        } else {
+                            chl.push_back((int)(-1 - nterm));
+                            for (int q = 0; q < Pc; ++q) tu.push_back(U[(size_t)(row * Pc + q)]);
+                            ++nterm;
+                        }
+                        if (ac[x] != 0) prs.push_back((j << 8) | a);
+                    }
+                    recs.push_back(curpar[k]);
+                    recs.push_back((int)fe[x]);
+                    recs.push_back((int)pa[x]);
+                    recs.push_back((int)ac[x]);
+                    recs.push_back((int)eb[x]);
+                    recs.push_back(nn[x]);
+                    recs.push_back(cp);
+                    recs.push_back((int)sh[x]);
+                }
+                nloc += (int64_t)cur.size();
+                cur.swap(nxt);
+                curpar.swap(nxtpar);
+            }
+            const int nlev = (int)lstart.size();
+            lstart.push_back((int)nloc);
+            pstart.push_back((int)prs.size());
+            for (int v : lstart) lvl.push_back(v);
+            const int64_t plv0 = (int64_t)lvl.size();
+            for (int v : pstart) lvl.push_back(v);
+            meta.push_back((int)node0);
+            meta.push_back((int)nloc);
+            meta.push_back((int)term0);
+            meta.push_back((int)nterm);
+            meta.push_back((int)lvl0);
+            meta.push_back(nlev);
+            meta.push_back((int)plv0);
+            meta.push_back((int)root);
+            if (nloc != snn[root] || nterm != snt[root] || nloc >= (1 << 23)) return CFR_OK;
+        }
+        sp.m_sub = 0;
+        sp.m_rec = (int)meta.size();
+        sp.m_child = (int)(sp.m_rec + recs.size());
+        sp.m_pair = (int)(sp.m_child + chl.size());
+        sp.m_lvl = (int)(sp.m_pair + prs.size());
+        const size_t total = (size_t)sp.m_lvl + lvl.size();
+        if (total > sub_table_bound(g) || tu.size() > (size_t)g.V * Pc + 2) return CFR_OK;
+        std::vector<int> tab;
+        tab.reserve(total);
+        tab.insert(tab.end(), meta.begin(), meta.end());
+        tab.insert(tab.end(), recs.begin(), recs.end());
+        tab.insert(tab.end(), chl.begin(), chl.end());
+        tab.insert(tab.end(), prs.begin(), prs.end());
+        tab.insert(tab.end(), lvl.begin(), lvl.end());
+        cfr_status st = up(plan.subt, tab);
+        if (st) return st;
+        if ((st = up(plan.subu, tu))) return st;
+        CU(cudaMemsetAsync(ws + plan.suba, 0, (size_t)3 * (sp.nq + sp.nh) * sizeof(unsigned long long), stream));
+        CU(cudaFuncSetAttribute(sub_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, sp.bytes));
+        CU(cudaStreamSynchronize(stream));
+        sub_plan_ = sp;
+        sub_ = true;
+        return CFR_OK;
+    }
     int64_t count_launches() const {
         const Game& g = *gp;
         int64_t n = 0;
+        if (sub_) {
+            for (int l = 1; l <= sub_plan_.cut; ++l)
+                if (g.slot_ptr[l + 1] > g.slot_ptr[l]) ++n;
+            n += 2;   // k_sub, k_sub_update
+            for (int L = sub_plan_.cut - 1; L >= 0; --L)
+                if (g.tile_ptr[L + 1] > g.tile_ptr[L]) ++n;
+            return (cfg.variant == CFR_PLUS_ALT) ? n * g.P : n;
+        }
         for (int l = 1; l < g.D; ++l)
             if (g.slot_ptr[l + 1] > g.slot_ptr[l] && !fwd_fused(l)) ++n;
         for (int L = g.D - 1; L >= 0; --L)
@@ -1174,10 +1414,39 @@ struct Solver final : SolverBase {
     // forward level l runs inside the streaming backward kernel of level l
     bool fwd_fused(int l) const { return use_stream_ && l < (int)stream_.size() && stream_[l].ntiles > 0 && stream_[l].fused; }
 
+    void launch_sub(cudaStream_t st, std::vector<Mark>* ev) {
+        const Game& g = *gp;
+        const SubPlan sp = sub_plan_;
+        for (int l = 1; l <= sp.cut; ++l) {
+            fwd_level(st, dg.sig, l, 0);
+            mark(st, ev, 0, l);
+        }
+        const int* tab = at<int>(plan.subt);
+        const R* tu = at<R>(plan.subu);
+        unsigned long long* acc = at<unsigned long long>(plan.suba);
+        switch (g.Pc) {
+            case 1: launch(pdl_, k_sub<R, I, 1>, dim3(sp.nsub), dim3(kSubThreads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp); break;
+            case 2: launch(pdl_, k_sub<R, I, 2>, dim3(sp.nsub), dim3(kSubThreads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp); break;
+            case 3: launch(pdl_, k_sub<R, I, 3>, dim3(sp.nsub), dim3(kSubThreads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp); break;
+            default: launch(pdl_, k_sub<R, I, 4>, dim3(sp.nsub), dim3(kSubThreads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp); break;
+        }
+        const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((sp.nh + 255) / 256, 4LL * num_sms_));
+        launch(pdl_, k_sub_update<R, I>, dim3(nb), dim3(256), 0, st, dg, acc, sp);
+        mark(st, ev, 1, sp.cut);
+        for (int L = sp.cut - 1; L >= 0; --L) {
+            bwd_level<MODE_CFR>(st, dg.sig, L, 0, (L == 0 && pass_final_) ? 1 : 0);
+            mark(st, ev, 1, L);
+        }
+    }
+
     // mode MODE_CFR (forward + backward), MODE_VALUES (values under sig) or
     // MODE_BR (best-response values of player br_player; reach of sig computed before)
     void launch_lower(cudaStream_t st, int mode, const R* sig, std::vector<Mark>* ev, int br_player = 0) {
         const Game& g = *gp;
+        if (mode == MODE_CFR && sig == dg.sig && sub_) {
+            launch_sub(st, ev);
+            return;
+        }
         if (mode == MODE_CFR)
             for (int l = 1; l < g.D; ++l) {
                 if (sig == dg.sig && fwd_fused(l)) continue;
@@ -1905,6 +2174,7 @@ struct Solver final : SolverBase {
     int level_kernel(int L) const {
         const Game& g = *gp;
         if (g.tile_ptr[L + 1] <= g.tile_ptr[L]) return 0;
+        if (sub_ && L >= sub_plan_.cut) return 4;
         if (use_stream_ && stream_[L].ntiles > 0) return 3;
         return 1;
     }
