@@ -31,7 +31,10 @@ namespace cfrb {
 //     sigma_ext base of its children's edges, children, first entry in the child
 //     table, internal infoset (-1 chance)
 //   child table: >= 0 local node, < 0 -(1 + k) = the subtree's k-th terminal
-//   pair table (global index pair0 of the subtree + k): local node << 8 | action
+//   pair table (int4 per (node, action) pair): local node << 8 | action, child
+//     reference, sigma / accumulator pair index q, actor
+// (node records and pair entries are read as 16-byte vectors: one dependent L2
+// round trip per level step instead of chains of scalar loads)
 // Terminal utilities in subtree order: tu[(term0 + k) * Pc + j].
 constexpr int kSubMeta = 8;
 constexpr int kSubRec = 8;
@@ -59,7 +62,7 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
     const int* const chl = T + sp.m_child;
     const int* const prs = T + sp.m_pair;
     const int* const lv = T + sp.m_lvl + lvl0;     // [nlev + 1] local node starts per level
-    const int* const plv = T + sp.m_lvl + plv0;    // [nlev + 1] pair-table starts per level (global)
+    const int* const plv = T + sp.m_lvl + plv0;    // [nlev + 1] pair-table starts per level (global pair index)
     R* const reach = reinterpret_cast<R*>(smem_raw);                       // [nn][2P]
     R* const val = reach + (((long long)nn * 2 * P + 1) & ~1LL);           // [nn][PC]
     R* const tv = val + (((long long)nn * PC + 1) & ~1LL);                 // [nt][PC] terminal utilities
@@ -76,10 +79,10 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
     // ---- forward (Eq 2 / Eq 4 with reading Q1; k_fwd's operations)
     for (int l = 1; l < nlev; ++l) {
         for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
-            const int* e = rec + kSubRec * j;
-            const int p = e[0];
-            const R x = g.sig[e[1]];
-            const int act = e[2];
+            const int4 ea = *reinterpret_cast<const int4*>(rec + kSubRec * j);
+            const int p = ea.x;
+            const R x = g.sig[ea.y];
+            const int act = ea.z;
             for (int i = 0; i < P; ++i) {
                 const R pc = reach[p * 2 * P + i], ph = reach[p * 2 * P + P + i];
                 reach[j * 2 * P + i] = (act != i + 1) ? pc * x : pc;
@@ -92,17 +95,27 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
     for (int l = nlev - 1; l >= 0; --l) {
         // values (Eq 1: ascending actions from +0)
         for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
-            const int* e = rec + kSubRec * j;
-            const int eb = e[4], nch = e[5], cp = e[6];
+            const int4 eb4 = *reinterpret_cast<const int4*>(rec + kSubRec * j + 4);
+            const int eb = eb4.x, nch = eb4.y, cp = eb4.z;
             R v[PC];
 #pragma unroll
             for (int c = 0; c < PC; ++c) v[c] = (R)0;
-            for (int a = 0; a < nch; ++a) {
-                const R x = g.sig[eb + a];
-                const int ch = chl[cp + a];
-                const R* u = (ch >= 0) ? val + (long long)ch * PC : tv + (long long)(-1 - ch) * PC;
+            for (int a0 = 0; a0 < nch; a0 += 8) {
+                // the batch's sigma and child references in flight together
+                R x[8];
+                int ch[8];
 #pragma unroll
-                for (int c = 0; c < PC; ++c) v[c] = v[c] + x * u[c];
+                for (int k = 0; k < 8; ++k) {
+                    x[k] = (a0 + k < nch) ? g.sig[eb + a0 + k] : (R)0;
+                    ch[k] = (a0 + k < nch) ? chl[cp + a0 + k] : 0;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (a0 + k >= nch) break;
+                    const R* u = (ch[k] >= 0) ? val + (long long)ch[k] * PC : tv + (long long)(-1 - ch[k]) * PC;
+#pragma unroll
+                    for (int c = 0; c < PC; ++c) v[c] = v[c] + x[k] * u[c];
+                }
             }
 #pragma unroll
             for (int c = 0; c < PC; ++c) val[(long long)j * PC + c] = v[c];
@@ -111,36 +124,33 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
         // exact slices of the regret terms pi_check * (u(child) - u(node)) of this
         // level's (node, action) pairs; zero terms are exact zeros and skipped
         for (int k = plv[l] + tid; k < plv[l + 1]; k += nth) {
-            const int pr = prs[k];
-            const int j = pr >> 8, a = pr & 255;
-            const int* e = rec + kSubRec * j;
-            const int i = e[3];
+            const int4 pr = *reinterpret_cast<const int4*>(prs + 4LL * k);
+            const int j = pr.x >> 8, ch = pr.y, i = pr.w;
             if (g.upd_player != 0 && i != g.upd_player) continue;
             const R pc = reach[j * 2 * P + (i - 1)];
             if (pc == (R)0) continue;
             const int col = (PC == 1) ? 0 : i - 1;
-            const int ch = chl[e[6] + a];
             const R u = (ch >= 0) ? val[(long long)ch * PC + col] : tv[(long long)(-1 - ch) * PC + col];
             const R t = pc * (u - val[(long long)j * PC + col]);
             if (!finite_(t)) bad = true;
             double c0 = 0, c1 = 0, c2 = 0;
             xadd(c0, c1, c2, (double)t, g.sc0);
             if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
-            unsigned long long* ac = acc_r + ((long long)e[4] + a - sp.qc) * 3;
+            unsigned long long* ac = acc_r + ((long long)pr.z - sp.qc) * 3;
             if (c0 != 0.0) atomicAdd(ac + 0, (unsigned long long)(long long)c0);
             if (c1 != 0.0) atomicAdd(ac + 1, (unsigned long long)(long long)c1);
             if (c2 != 0.0) atomicAdd(ac + 2, (unsigned long long)(long long)c2);
         }
         // exact slices of pi_hat (Eq 5 / Eq 10 weights) of this level's player nodes
         for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
-            const int* e = rec + kSubRec * j;
-            const int i = e[3];
+            const int4 ea = *reinterpret_cast<const int4*>(rec + kSubRec * j);
+            const int i = ea.w;
             if (i == 0 || (g.upd_player != 0 && i != g.upd_player)) continue;
             const R ph = reach[j * 2 * P + P + (i - 1)];
             if (ph == (R)0) continue;
             double c0 = 0, c1 = 0, c2 = 0;
             xadd(c0, c1, c2, (double)ph, g.scp0);
-            unsigned long long* ac = acc_p + ((long long)e[7] - sp.hc) * 3;
+            unsigned long long* ac = acc_p + ((long long)rec[kSubRec * j + 7] - sp.hc) * 3;
             if (c0 != 0.0) atomicAdd(ac + 0, (unsigned long long)(long long)c0);
             if (c1 != 0.0) atomicAdd(ac + 1, (unsigned long long)(long long)c1);
             if (c2 != 0.0) atomicAdd(ac + 2, (unsigned long long)(long long)c2);

@@ -384,7 +384,7 @@ static bool sub_candidate(const Game& g) { return g.V <= kSubMaxV && g.D >= 2 &&
 // ints: per-subtree records, node records, child entries (<= V), pair entries
 // (<= V), per-level node and pair starts of every subtree
 static size_t sub_table_bound(const Game& g) {
-    return (size_t)(kSubMeta * kSubMaxSub + kSubRec * g.NS + 2 * g.V + 2 * kSubMaxSub * (g.D + 2) + 64);
+    return (size_t)(kSubMeta * kSubMaxSub + kSubRec * g.NS + 5 * g.V + 2 * kSubMaxSub * (g.D + 2) + 64);
 }
 
 template <class R, class I>
@@ -1228,7 +1228,7 @@ struct Solver final : SolverBase {
             int64_t nloc = 0, nterm = 0;
             while (!cur.empty()) {
                 lstart.push_back((int)nloc);
-                pstart.push_back((int)prs.size());
+                pstart.push_back((int)(prs.size() / 4));
                 nxt.clear();
                 std::vector<int> nxtpar;
                 const int64_t base = nloc;
@@ -1248,7 +1248,12 @@ struct Solver final : SolverBase {
                             for (int q = 0; q < Pc; ++q) tu.push_back(U[(size_t)(row * Pc + q)]);
                             ++nterm;
                         }
-                        if (ac[x] != 0) prs.push_back((j << 8) | a);
+                        if (ac[x] != 0) {   // int4: node << 8 | action, child ref, pair index q, actor
+                            prs.push_back((j << 8) | a);
+                            prs.push_back(chl.back());
+                            prs.push_back((int)(eb[x] + a));
+                            prs.push_back((int)ac[x]);
+                        }
                     }
                     recs.push_back(curpar[k]);
                     recs.push_back((int)fe[x]);
@@ -1265,7 +1270,7 @@ struct Solver final : SolverBase {
             }
             const int nlev = (int)lstart.size();
             lstart.push_back((int)nloc);
-            pstart.push_back((int)prs.size());
+            pstart.push_back((int)(prs.size() / 4));
             for (int v : lstart) lvl.push_back(v);
             const int64_t plv0 = (int64_t)lvl.size();
             for (int v : pstart) lvl.push_back(v);
@@ -1279,6 +1284,11 @@ struct Solver final : SolverBase {
             meta.push_back((int)root);
             if (nloc != snn[root] || nterm != snt[root] || nloc >= (1 << 23)) return CFR_OK;
         }
+        // sections start on 16-byte boundaries (int4 reads of records and pairs)
+        auto pad4 = [](std::vector<int>& v) { while (v.size() % 4) v.push_back(0); };
+        pad4(meta);
+        pad4(recs);
+        pad4(chl);
         sp.m_sub = 0;
         sp.m_rec = (int)meta.size();
         sp.m_child = (int)(sp.m_rec + recs.size());
