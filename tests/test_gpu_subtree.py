@@ -100,3 +100,15 @@ def test_subtree_resume_and_tracked(cuda):
     tr = pb.Solver(g, variant="cfr+", precision=64, flags=F).run_tracked(40, 20)
     o = oracle.Oracle(desc, precision=64).run(40, 1)
     assert_same("NashConv at T=40", [tr["nash_conv"][-1]], [o.exploitability()["nash_conv"]], 64)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 4])
+@pytest.mark.parametrize("name", ["leduc", "goofspiel", "liars_dice"])
+def test_subtree_longer_runs(cuda, name, variant):
+    """Longer runs (the chaotic trajectory magnifies any difference), alternating
+    updates included: one pass per player per iteration."""
+    T = 300 if name == "liars_dice" else 1000
+    out, s, o = run_pair(gamegen.by_name(name), variant, 64, T, flags=F, checks=("state",))
+    n = s.launches_per_iteration()
+    ref = pb.Solver(pb.Game(gamegen.by_name(name)), variant=1, precision=64, flags=F).launches_per_iteration()
+    assert n == (2 * ref if variant == 4 else ref)
