@@ -50,10 +50,10 @@ struct SubPlan {
 };
 
 template <class R, class I, int PC>
-__device__ __forceinline__ void sub_body(const DG<R, I>& g, const int* __restrict__ T, const R* __restrict__ tu,
-                                         unsigned long long* __restrict__ acc, const SubPlan& sp, int b, bool single) {
+__global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __restrict__ T, const R* __restrict__ tu,
+                                                     unsigned long long* __restrict__ acc, SubPlan sp) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int tid = threadIdx.x, nth = blockDim.x;
+    const int b = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
     const int P = g.P;
     const int* const mb = T + sp.m_sub + kSubMeta * b;
     const int node0 = mb[0], nn = mb[1], term0 = mb[2], nt = mb[3], lvl0 = mb[4], nlev = mb[5], plv0 = mb[6];
@@ -68,10 +68,10 @@ __device__ __forceinline__ void sub_body(const DG<R, I>& g, const int* __restric
     R* const tv = val + (((long long)nn * PC + 1) & ~1LL);                 // [nt][PC] terminal utilities
     unsigned long long* const acc_r = acc;                                 // [nq][3]
     unsigned long long* const acc_p = acc + 3 * sp.nq;                     // [nh][3]
-    if (!single) pdl_trigger();
+    pdl_trigger();
     // terminal utilities are constant: staged before the dependency wait
     for (long long k = tid; k < (long long)nt * PC; k += nth) tv[k] = tu[(long long)term0 * PC + k];
-    if (!single) pdl_wait();
+    pdl_wait();
     const long long t_iter = g.ctrl[0] + 1;
     bool bad = false;
     if (tid < 2 * P) reach[tid] = g.reach[(long long)root_slot * 2 * P + tid];   // level-c forward kernel's row
@@ -165,24 +165,20 @@ __device__ __forceinline__ void sub_body(const DG<R, I>& g, const int* __restric
     if (bad) atomicMin(&g.ctrl[1], t_iter);
 }
 
-template <class R, class I, int PC>
-__global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __restrict__ T, const R* __restrict__ tu,
-                                                     unsigned long long* __restrict__ acc, SubPlan sp) {
-    sub_body<R, I, PC>(g, T, tu, acc, sp, blockIdx.x, false);
-}
-
 // Update of every infoset below the cut: decode the exact sums, then Eq 8/15 or
 // CFR+ (or Q18), Eq 10, Eq 9 (k_deferred's operations and order); zero the sums.
 template <class R, class I>
-__device__ __forceinline__ void sub_update_body(const DG<R, I>& g, unsigned long long* __restrict__ acc, const SubPlan& sp,
-                                                long long x0, long long stride) {
+__global__ void __launch_bounds__(256) k_sub_update(DG<R, I> g, unsigned long long* __restrict__ acc, SubPlan sp) {
+    pdl_trigger();
+    pdl_wait();
     const long long t_iter = g.ctrl[0] + 1;
     const Upd<R> up = make_upd<R>(g.variant, t_iter);
     const R w = up.w;
     bool bad = false;
     unsigned long long* const acc_r = acc;
     unsigned long long* const acc_p = acc + 3 * sp.nq;
-    for (long long x = x0; x < sp.nh; x += stride) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < sp.nh; x += stride) {
         const long long h = sp.hc + x;
         const long long qb = (long long)g.qbase[h];
         const int n = (int)((long long)g.qbase[h + 1] - qb);
@@ -221,13 +217,6 @@ __device__ __forceinline__ void sub_update_body(const DG<R, I>& g, unsigned long
         }
     }
     if (bad) atomicMin(&g.ctrl[1], t_iter);
-}
-
-template <class R, class I>
-__global__ void __launch_bounds__(256) k_sub_update(DG<R, I> g, unsigned long long* __restrict__ acc, SubPlan sp) {
-    pdl_trigger();
-    pdl_wait();
-    sub_update_body<R, I>(g, acc, sp, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
 }
 
 }  // namespace cfrb

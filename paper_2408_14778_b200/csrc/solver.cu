@@ -1313,6 +1313,117 @@ struct Solver final : SolverBase {
         sub_ = true;
         return CFR_OK;
     }
+    int64_t count_launches() const {
+        const Game& g = *gp;
+        int64_t n = 0;
+        if (sub_) {
+            for (int l = 1; l <= sub_plan_.cut; ++l)
+                if (g.slot_ptr[l + 1] > g.slot_ptr[l]) ++n;
+            n += 2;   // k_sub, k_sub_update
+            for (int L = sub_plan_.cut - 1; L >= 0; --L)
+                if (g.tile_ptr[L + 1] > g.tile_ptr[L]) ++n;
+            return (cfg.variant == CFR_PLUS_ALT) ? n * g.P : n;
+        }
+        for (int l = 1; l < g.D; ++l)
+            if (g.slot_ptr[l + 1] > g.slot_ptr[l] && !fwd_fused(l)) ++n;
+        for (int L = g.D - 1; L >= 0; --L)
+            if (g.tile_ptr[L + 1] > g.tile_ptr[L]) ++n;
+        if (!g.deferred_list.empty()) ++n;
+        return (cfg.variant == CFR_PLUS_ALT) ? n * g.P : n;   // alternating updates: one pass per player
+    }
+
+    // the deepest level's reach rows in compact (actor-only) form: CFR iterations
+    // whose backward pass there is the (unfused) streaming kernel, two players
+    bool fwd_compact(int l) const {
+        return gp->P == 2 && l == gp->D - 1 && use_stream_ && l < (int)stream_.size() && stream_[l].ntiles > 0 &&
+               !stream_[l].fused && stream_[l].compact;
+    }
+    void fwd_level(cudaStream_t st, const R* sig, int l, int compact = 0) {
+        const Game& g = *gp;
+        const long long s0 = g.slot_ptr[l], s1 = g.slot_ptr[l + 1];   // reach rows = slots
+        if (s1 <= s0) return;
+        const long long n = s1 - s0;
+        const int threads = 256;
+        const long long per_block = (g.P == 2) ? threads * CFR_FWD_FW : threads;
+        const long long blocks = std::min<long long>((n + per_block - 1) / per_block, 148LL * 16);
+        if (g.P == 2)
+            launch(pdl_, k_fwd<R, I, 2>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1,
+                   compact);
+        else
+            launch(pdl_, k_fwd<R, I, 0>, dim3((unsigned)blocks), dim3(threads), 0, st, dg, sig, (long long)s0, (long long)s1,
+                   0);
+    }
+
+    template <int MODE>
+    void bwd_level(cudaStream_t st, const R* sig, int L, int br_player, int last) {
+        const Game& g = *gp;
+        const long long t0 = g.tile_ptr[L], t1 = g.tile_ptr[L + 1];
+        if (t1 <= t0) return;
+        if (MODE == MODE_CFR && sig == dg.sig && use_stream_ && stream_[L].ntiles > 0) {
+            StreamLevel f = stream_[L];
+            f.last = last;
+            f.debug = stream_debug_;
+            int per_sm = 1;
+            switch (g.Pc) {
+                case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_stream<R, I, 1>, kStreamThreads, f.bytes); break;
+                case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_stream<R, I, 2>, kStreamThreads, f.bytes); break;
+                case 3: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_stream<R, I, 3>, kStreamThreads, f.bytes); break;
+                default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bwd_stream<R, I, 4>, kStreamThreads, f.bytes); break;
+            }
+            per_sm = std::max(1, per_sm);
+            const unsigned nb = (unsigned)std::min<long long>(f.ntiles, (long long)num_sms_ * per_sm);
+            if (std::getenv("CFR_STREAM_VERBOSE"))
+                std::fprintf(stderr, "[stream] level %d: %lld tiles, maxm %d, maxseg %d, smem %d B, %d CTA/SM, grid %u\n", L,
+                             f.ntiles, f.maxm, f.maxseg, f.bytes, per_sm, nb);
+            const int* sp = at<int>(plan.spool);
+            switch (g.Pc) {
+                case 1: launch(pdl_, k_bwd_stream<R, I, 1>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
+                case 2: launch(pdl_, k_bwd_stream<R, I, 2>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
+                case 3: launch(pdl_, k_bwd_stream<R, I, 3>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
+                default: launch(pdl_, k_bwd_stream<R, I, 4>, dim3(nb), dim3(kStreamThreads), (size_t)f.bytes, st, dg, sp, f); break;
+            }
+            return;
+        }
+        const SmemLayout lay = lay_[L];
+        const size_t sm = (size_t)lay.bytes;
+        const unsigned nb = (unsigned)(t1 - t0);
+        switch (g.Pc) {
+            case 1: launch(pdl_, k_bwd<R, I, 1, MODE>, dim3(nb), dim3(kTileSlots), sm, st, dg, sig, (long long)t0, br_player, last, lay); break;
+            case 2: launch(pdl_, k_bwd<R, I, 2, MODE>, dim3(nb), dim3(kTileSlots), sm, st, dg, sig, (long long)t0, br_player, last, lay); break;
+            case 3: launch(pdl_, k_bwd<R, I, 3, MODE>, dim3(nb), dim3(kTileSlots), sm, st, dg, sig, (long long)t0, br_player, last, lay); break;
+            default: launch(pdl_, k_bwd<R, I, 4, MODE>, dim3(nb), dim3(kTileSlots), sm, st, dg, sig, (long long)t0, br_player, last, lay); break;
+        }
+    }
+
+    void deferred_update(cudaStream_t st, int last) {
+        const long long n = dg.ndef;
+        const unsigned blocks = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 8));
+        // no programmatic (PDL) edge when an NCCL all-reduce precedes it (sharded)
+        launch(pdl_ && world == 1, k_deferred<R, I>, dim3(blocks), dim3(256), 0, st, dg, last);
+    }
+
+    // ---- iteration phases.  One iteration = lower (forward + backward of the
+    // owned levels, down to the cut) -> [exchange 1: cut values] -> upper (trunk
+    // backward) -> [exchange 2: deferred exact sums] -> deferred update.  On one
+    // GPU the cut is -1: lower is the whole pass and both exchanges vanish.
+    // `ev` (optional) collects (tag, level, event) for profiling: tag 0 forward,
+    // 1 backward, 2 deferred update, 3 exchange.
+    struct Mark {
+        int tag, level;
+        cudaEvent_t e;
+    };
+    void mark(cudaStream_t st, std::vector<Mark>* ev, int tag, int level) {
+        if (!ev) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        ev->push_back(Mark{tag, level, e});
+    }
+    bool has_def() const { return !gp->deferred_list.empty(); }
+
+    // forward level l runs inside the streaming backward kernel of level l
+    bool fwd_fused(int l) const { return use_stream_ && l < (int)stream_.size() && stream_[l].ntiles > 0 && stream_[l].fused; }
+
     void launch_sub(cudaStream_t st, std::vector<Mark>* ev) {
         const Game& g = *gp;
         const SubPlan sp = sub_plan_;
