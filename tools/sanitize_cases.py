@@ -1,5 +1,6 @@
 """Small runs for compute-sanitizer (memcheck / racecheck / synccheck):
-Kuhn and Leduc (k_tiny and the per-level kernels), the synthetic n = 2 through
+Kuhn and Leduc (k_tiny, the subtree mode and the per-level kernels), Goofspiel and a
+3-player general-sum random game through the subtree mode (k_sub), the synthetic n = 2 through
 the forced streaming kernel (compact and fused forward, f64 / f32), device best
 response, and one in-process world-2 sharded iteration.  Each case checks its
 result against the oracle so a sanitizer-perturbed run cannot pass silently."""
@@ -30,6 +31,10 @@ def check(desc, variant, prec, flags, T, br=True):
 check(gamegen.kuhn(), "cfr", 64, 0, 20)
 check(gamegen.leduc(), "cfr+", 64, 0, 5)
 check(gamegen.leduc(), "cfr+", 32, pb.FLAG_NO_TINY, 3)
+# subtree mode (k_sub + k_sub_update: shared-memory subtrees, global int64 atomics)
+check(gamegen.goofspiel(), "cfr", 64, 0, 2, br=not FAST)
+check(gamegen.random_game(5, num_players=3, max_nodes=3000), "cfr", 64, pb.FLAG_FORCE_SUBTREE, 3, br=not FAST)
+check(gamegen.leduc(), "cfr+", 32, pb.FLAG_FORCE_SUBTREE, 3, br=False)
 syn = gamegen.synthetic(n_types=2, seed=1)
 check(syn, "cfr+", 64, pb.FLAG_FORCE_STREAM, 2, br=not FAST)
 check(syn, "cfr", 32, pb.FLAG_FORCE_STREAM | pb.FLAG_FUSED_FORWARD, 2, br=False)
