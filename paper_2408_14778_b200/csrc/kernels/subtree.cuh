@@ -167,6 +167,10 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
 
 // Update of every infoset below the cut: decode the exact sums, then Eq 8/15 or
 // CFR+ (or Q18), Eq 10, Eq 9 (k_deferred's operations and order); zero the sums.
+// A thread per infoset; the infoset's loads (sums, R, S_num, sigma) are all issued
+// before its first store (restrict-qualified copies of the state pointers), so
+// the chain is one round trip of loads, not one per action.
+constexpr int kSubUpdRegs = 8;   // actions kept in registers (wider infosets: generic loop)
 template <class R, class I>
 __global__ void __launch_bounds__(256) k_sub_update(DG<R, I> g, unsigned long long* __restrict__ acc, SubPlan sp) {
     pdl_trigger();
@@ -175,19 +179,74 @@ __global__ void __launch_bounds__(256) k_sub_update(DG<R, I> g, unsigned long lo
     const Upd<R> up = make_upd<R>(g.variant, t_iter);
     const R w = up.w;
     bool bad = false;
-    unsigned long long* const acc_r = acc;
-    unsigned long long* const acc_p = acc + 3 * sp.nq;
+    unsigned long long* __restrict__ const acc_r = acc;
+    unsigned long long* __restrict__ const acc_p = acc + 3 * sp.nq;
+    R* __restrict__ const reg = g.regret;
+    R* __restrict__ const snum = g.snum;
+    R* __restrict__ const sig = g.sig;
+    R* __restrict__ const sden = g.sden;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < sp.nh; x += stride) {
         const long long h = sp.hc + x;
         const long long qb = (long long)g.qbase[h];
         const int n = (int)((long long)g.qbase[h + 1] - qb);
+        const long long cq0 = qb - sp.qc;
+        if (g.upd_player != 0 && g.owner[h] != g.upd_player) {
+            // alternating updates: another player's infoset (its sums are zero)
+            continue;
+        }
         const long long p0 = (long long)acc_p[x * 3 + 0], p1 = (long long)acc_p[x * 3 + 1], p2 = (long long)acc_p[x * 3 + 2];
+        const R sd = sden[h];
+        if (n <= kSubUpdRegs) {
+            long long c[kSubUpdRegs][3];
+            R r0[kSubUpdRegs], s0[kSubUpdRegs], x0[kSubUpdRegs];
+#pragma unroll
+            for (int a = 0; a < kSubUpdRegs; ++a)
+                if (a < n) {
+                    const unsigned long long* ac = acc_r + (cq0 + a) * 3;
+                    c[a][0] = (long long)ac[0];
+                    c[a][1] = (long long)ac[1];
+                    c[a][2] = (long long)ac[2];
+                    r0[a] = reg[qb + a];
+                    s0[a] = snum[qb + a];
+                    x0[a] = sig[qb + a];
+                }
+            acc_p[x * 3 + 0] = 0;
+            acc_p[x * 3 + 1] = 0;
+            acc_p[x * 3 + 2] = 0;
+            const R pib = (R)xdec_ll(p0, p1, p2, g.rcp);
+            const R wp = w * pib;
+            R z = (R)0;
+#pragma unroll
+            for (int a = 0; a < kSubUpdRegs; ++a)
+                if (a < n) {
+                    unsigned long long* ac = acc_r + (cq0 + a) * 3;
+                    ac[0] = 0;
+                    ac[1] = 0;
+                    ac[2] = 0;
+                    const R rt = (R)xdec_ll(c[a][0], c[a][1], c[a][2], g.rc);
+                    const R r = upd_regret(up, r0[a], rt);
+                    r0[a] = r;
+                    reg[qb + a] = r;
+                    snum[qb + a] = upd_sum(up, s0[a], wp * x0[a]);
+                    z = z + ((r > (R)0) ? r : (R)0);
+                    if (!finite_(rt)) bad = true;
+                }
+            sden[h] = upd_sum(up, sd, wp);
+#pragma unroll
+            for (int a = 0; a < kSubUpdRegs; ++a)
+                if (a < n) {
+                    const R r = r0[a];
+                    const R pos = (r > (R)0) ? r : (R)0;
+                    const R nsig = (z > (R)0) ? pos / z : (R)1 / (R)n;
+                    sig[qb + a] = nsig;
+                    if (!finite_(r) || !finite_(nsig) || !finite_(z)) bad = true;
+                }
+            continue;
+        }
         acc_p[x * 3 + 0] = 0;
         acc_p[x * 3 + 1] = 0;
         acc_p[x * 3 + 2] = 0;
-        const long long cq0 = qb - sp.qc;
-        if (g.upd_player != 0 && g.owner[h] != g.upd_player) continue;   // alternating: another player's (sums are 0)
         const R pib = (R)xdec_ll(p0, p1, p2, g.rcp);
         const R wp = w * pib;
         R z = (R)0;
@@ -199,20 +258,20 @@ __global__ void __launch_bounds__(256) k_sub_update(DG<R, I> g, unsigned long lo
             ac[1] = 0;
             ac[2] = 0;
             const R rt = (R)xdec_ll(c0, c1, c2, g.rc);
-            g.regret[q] = upd_regret(up, g.regret[q], rt);
-            g.snum[q] = upd_sum(up, g.snum[q], wp * g.sig[q]);
+            reg[q] = upd_regret(up, reg[q], rt);
+            snum[q] = upd_sum(up, snum[q], wp * sig[q]);
             if (!finite_(rt)) bad = true;
         }
-        g.sden[h] = upd_sum(up, g.sden[h], wp);
+        sden[h] = upd_sum(up, sd, wp);
         for (int a = 0; a < n; ++a) {
-            const R r = g.regret[qb + a];
+            const R r = reg[qb + a];
             z = z + ((r > (R)0) ? r : (R)0);
         }
         for (int a = 0; a < n; ++a) {
-            const R r = g.regret[qb + a];
+            const R r = reg[qb + a];
             const R pos = (r > (R)0) ? r : (R)0;
             const R nsig = (z > (R)0) ? pos / z : (R)1 / (R)n;
-            g.sig[qb + a] = nsig;
+            sig[qb + a] = nsig;
             if (!finite_(r) || !finite_(nsig) || !finite_(z)) bad = true;
         }
     }
