@@ -22,21 +22,27 @@ namespace cfrb {
 // kernels; the roots' values are written to their U rows for it.
 //
 // Tables (int32, built once on the host from the device slot tables, so both
-// paths read the same numbers):
-//   per subtree b (kSubMeta ints): node0, nodes, term0, terms, lvl0 (offset of its
-//     per-level node starts), levels, pair_lvl0 (offset of its per-level pair
-//     starts), root slot; the per-level starts are local indices
-//   per local node (kSubRec ints, global index node0 + j): local parent (-1 root),
-//     sigma_ext index of the incoming edge, parent actor, own actor (0 chance),
-//     sigma_ext base of its children's edges, children, first entry in the child
-//     table, internal infoset (-1 chance)
-//   child table: >= 0 local node, < 0 -(1 + k) = the subtree's k-th terminal
-//   pair table (int4 per (node, action) pair): local node << 8 | action, child
+// paths read the same numbers), all staged into shared memory at the start:
+//   per subtree b (kSubMeta ints): node0, nodes, term0, terms, lvl0, levels,
+//     plv0, root slot, child0, edges, pair0, pairs
+//   per local node (two int4): {local parent (-1 root), child-table position of
+//     its incoming edge, parent actor | actor << 8 (0 chance), sigma_ext index of
+//     its incoming edge} and {sigma_ext base of its children's edges, children,
+//     first child-table position (local), internal infoset (-1 chance)}
+//   child table (local positions, one per edge): >= 0 local node, < 0 -(1 + k) =
+//     the subtree's k-th terminal
+//   pair table (int4 per (player node, action)): local node << 8 | action, child
 //     reference, sigma / accumulator pair index q, actor
-// (node records and pair entries are read as 16-byte vectors: one dependent L2
-// round trip per level step instead of chains of scalar loads)
+//   per level: local node starts [levels + 1], then local pair starts [levels + 1]
 // Terminal utilities in subtree order: tu[(term0 + k) * Pc + j].
-constexpr int kSubMeta = 8;
+// STAGED (the subtrees' tables fit shared memory next to their state): the tables
+// are copied in at the start and the edge probabilities of the subtree (sigma of
+// its player nodes' infosets, the chance probabilities) gathered once per
+// iteration into ev[] (one dependent round trip); every level step after that is
+// shared-memory work and a barrier.  Otherwise (larger subtrees at a shallower
+// cut) the tables and sigma are read from global memory (L2) in each level step:
+// 16-byte records, sigma and child references batched 8 actions at a time.
+constexpr int kSubMeta = 12;
 constexpr int kSubRec = 8;
 constexpr int kSubThreads = 512;
 
@@ -45,44 +51,91 @@ struct SubPlan {
     int cut;           // cut level c
     long long hc, qc;  // first internal infoset / pair below the cut (accumulator bases)
     long long nh, nq;  // infosets / pairs below the cut
-    int bytes;         // dynamic shared memory
+    int bytes;         // dynamic shared memory (the largest subtree)
+    int threads;       // CTA size
+    int staged;        // 1: tables and edge probabilities staged in shared memory
     int m_sub, m_rec, m_child, m_pair, m_lvl;   // int offsets inside the table block
 };
 
-template <class R, class I, int PC>
+// shared-memory plan of one subtree (host and device agree on it)
+struct SubSmem {
+    long long reach, val, tv, ev, rec, prs, chl, lvl, total;   // byte offsets
+};
+__host__ __device__ inline long long sub_al16(long long x) { return (x + 15) & ~15LL; }
+__host__ __device__ inline SubSmem sub_smem(long long nn, long long nt, long long ne, long long np, int nlev, int P,
+                                            int Pc, int w) {
+    SubSmem m;
+    long long o = 0;
+    m.reach = o; o += sub_al16(nn * 2 * P * w);
+    m.val = o; o += sub_al16(nn * Pc * w);
+    m.tv = o; o += sub_al16(nt * Pc * w);
+    m.ev = o; o += sub_al16(ne * w);
+    m.rec = o; o += nlev >= 0 ? nn * 4 * kSubRec : 0;
+    m.prs = o; o += np * 16;
+    m.chl = o; o += sub_al16(ne * 4);
+    m.lvl = o; o += nlev >= 0 ? sub_al16(2LL * (nlev + 1) * 4) : 0;
+    m.total = o;
+    return m;
+}
+
+template <class R, class I, int PC, bool STAGED>
 __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __restrict__ T, const R* __restrict__ tu,
                                                      unsigned long long* __restrict__ acc, SubPlan sp) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int b = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
     const int P = g.P;
     const int* const mb = T + sp.m_sub + kSubMeta * b;
-    const int node0 = mb[0], nn = mb[1], term0 = mb[2], nt = mb[3], lvl0 = mb[4], nlev = mb[5], plv0 = mb[6];
-    const int root_slot = mb[7];
-    const int* const rec = T + sp.m_rec + (long long)kSubRec * node0;
-    const int* const chl = T + sp.m_child;
-    const int* const prs = T + sp.m_pair;
-    const int* const lv = T + sp.m_lvl + lvl0;     // [nlev + 1] local node starts per level
-    const int* const plv = T + sp.m_lvl + plv0;    // [nlev + 1] pair-table starts per level (global pair index)
-    R* const reach = reinterpret_cast<R*>(smem_raw);                       // [nn][2P]
-    R* const val = reach + (((long long)nn * 2 * P + 1) & ~1LL);           // [nn][PC]
-    R* const tv = val + (((long long)nn * PC + 1) & ~1LL);                 // [nt][PC] terminal utilities
-    unsigned long long* const acc_r = acc;                                 // [nq][3]
-    unsigned long long* const acc_p = acc + 3 * sp.nq;                     // [nh][3]
+    const int node0 = mb[0], nn = mb[1], term0 = mb[2], nt = mb[3], lvl0 = mb[4], nlev = mb[5];
+    const int root_slot = mb[7], child0 = mb[8], ne = mb[9], pair0 = mb[10], np = mb[11];
+    const SubSmem L = sub_smem(nn, nt, STAGED ? ne : 0, STAGED ? np : 0, STAGED ? nlev : -1, P, PC, (int)sizeof(R));
+    R* const reach = reinterpret_cast<R*>(smem_raw + L.reach);    // [nn][2P]
+    R* const val = reinterpret_cast<R*>(smem_raw + L.val);        // [nn][PC]
+    R* const tv = reinterpret_cast<R*>(smem_raw + L.tv);          // [nt][PC] terminal utilities
+    R* const ev = reinterpret_cast<R*>(smem_raw + L.ev);          // [ne] edge probabilities (STAGED)
+    const int4* const grec = reinterpret_cast<const int4*>(T + sp.m_rec + (long long)kSubRec * node0);
+    const int4* const gprs = reinterpret_cast<const int4*>(T + sp.m_pair) + pair0;
+    const int* const gchl = T + sp.m_child + child0;
+    const int* const glv = T + sp.m_lvl + lvl0;
+    int4* const srec = reinterpret_cast<int4*>(smem_raw + L.rec);
+    int4* const sprs = reinterpret_cast<int4*>(smem_raw + L.prs);
+    int* const schl = reinterpret_cast<int*>(smem_raw + L.chl);
+    int* const slv = reinterpret_cast<int*>(smem_raw + L.lvl);
+    const int4* const rec = STAGED ? srec : grec;                 // [nn][2]
+    const int4* const prs = STAGED ? sprs : gprs;                 // [np]
+    const int* const chl = STAGED ? schl : gchl;                  // [ne]
+    const int* const lv = STAGED ? slv : glv;                     // [nlev + 1] nodes, then [nlev + 1] pairs
+    const int* const plv = lv + nlev + 1;
+    unsigned long long* const acc_r = acc;                        // [nq][3]
+    unsigned long long* const acc_p = acc + 3 * sp.nq;            // [nh][3]
     pdl_trigger();
-    // terminal utilities are constant: staged before the dependency wait
+    // the constant tables and terminal utilities: staged before the dependency wait
+    if (STAGED) {
+        for (int k = tid; k < 2 * nn; k += nth) srec[k] = grec[k];
+        for (int k = tid; k < np; k += nth) sprs[k] = gprs[k];
+        for (int k = tid; k < ne; k += nth) schl[k] = gchl[k];
+        for (int k = tid; k < 2 * (nlev + 1); k += nth) slv[k] = glv[k];
+    }
     for (long long k = tid; k < (long long)nt * PC; k += nth) tv[k] = tu[(long long)term0 * PC + k];
     pdl_wait();
     const long long t_iter = g.ctrl[0] + 1;
     bool bad = false;
+    if (STAGED) {
+        __syncthreads();
+        // edge probabilities of this iteration (sigma is constant during the pass)
+        for (int j = tid; j < nn; j += nth) {
+            const int4 bb = rec[2 * j + 1];
+            for (int a = 0; a < bb.y; ++a) ev[bb.z + a] = g.sig[bb.x + a];
+        }
+    }
     if (tid < 2 * P) reach[tid] = g.reach[(long long)root_slot * 2 * P + tid];   // level-c forward kernel's row
     __syncthreads();
     // ---- forward (Eq 2 / Eq 4 with reading Q1; k_fwd's operations)
     for (int l = 1; l < nlev; ++l) {
         for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
-            const int4 ea = *reinterpret_cast<const int4*>(rec + kSubRec * j);
+            const int4 ea = rec[2 * j];
             const int p = ea.x;
-            const R x = g.sig[ea.y];
-            const int act = ea.z;
+            const R x = STAGED ? ev[ea.y] : g.sig[ea.w];
+            const int act = ea.z & 255;
             for (int i = 0; i < P; ++i) {
                 const R pc = reach[p * 2 * P + i], ph = reach[p * 2 * P + P + i];
                 reach[j * 2 * P + i] = (act != i + 1) ? pc * x : pc;
@@ -95,26 +148,36 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
     for (int l = nlev - 1; l >= 0; --l) {
         // values (Eq 1: ascending actions from +0)
         for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
-            const int4 eb4 = *reinterpret_cast<const int4*>(rec + kSubRec * j + 4);
-            const int eb = eb4.x, nch = eb4.y, cp = eb4.z;
+            const int4 bb = rec[2 * j + 1];
+            const int eb = bb.x, nch = bb.y, cp = bb.z;
             R v[PC];
 #pragma unroll
             for (int c = 0; c < PC; ++c) v[c] = (R)0;
-            for (int a0 = 0; a0 < nch; a0 += 8) {
-                // the batch's sigma and child references in flight together
-                R x[8];
-                int ch[8];
+            if (STAGED) {
+                for (int a = 0; a < nch; ++a) {
+                    const R x = ev[cp + a];
+                    const int ch = chl[cp + a];
+                    const R* u = (ch >= 0) ? val + (long long)ch * PC : tv + (long long)(-1 - ch) * PC;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    x[k] = (a0 + k < nch) ? g.sig[eb + a0 + k] : (R)0;
-                    ch[k] = (a0 + k < nch) ? chl[cp + a0 + k] : 0;
+                    for (int c = 0; c < PC; ++c) v[c] = v[c] + x * u[c];
                 }
+            } else {
+                for (int a0 = 0; a0 < nch; a0 += 8) {
+                    // the batch's sigma and child references in flight together
+                    R x[8];
+                    int ch[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    if (a0 + k >= nch) break;
-                    const R* u = (ch[k] >= 0) ? val + (long long)ch[k] * PC : tv + (long long)(-1 - ch[k]) * PC;
+                    for (int k = 0; k < 8; ++k) {
+                        x[k] = (a0 + k < nch) ? g.sig[eb + a0 + k] : (R)0;
+                        ch[k] = (a0 + k < nch) ? chl[cp + a0 + k] : 0;
+                    }
 #pragma unroll
-                    for (int c = 0; c < PC; ++c) v[c] = v[c] + x[k] * u[c];
+                    for (int k = 0; k < 8; ++k) {
+                        if (a0 + k >= nch) break;
+                        const R* u = (ch[k] >= 0) ? val + (long long)ch[k] * PC : tv + (long long)(-1 - ch[k]) * PC;
+#pragma unroll
+                        for (int c = 0; c < PC; ++c) v[c] = v[c] + x[k] * u[c];
+                    }
                 }
             }
 #pragma unroll
@@ -124,7 +187,7 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
         // exact slices of the regret terms pi_check * (u(child) - u(node)) of this
         // level's (node, action) pairs; zero terms are exact zeros and skipped
         for (int k = plv[l] + tid; k < plv[l + 1]; k += nth) {
-            const int4 pr = *reinterpret_cast<const int4*>(prs + 4LL * k);
+            const int4 pr = prs[k];
             const int j = pr.x >> 8, ch = pr.y, i = pr.w;
             if (g.upd_player != 0 && i != g.upd_player) continue;
             const R pc = reach[j * 2 * P + (i - 1)];
@@ -143,14 +206,14 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
         }
         // exact slices of pi_hat (Eq 5 / Eq 10 weights) of this level's player nodes
         for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
-            const int4 ea = *reinterpret_cast<const int4*>(rec + kSubRec * j);
-            const int i = ea.w;
+            const int4 ea = rec[2 * j];
+            const int i = ea.z >> 8;
             if (i == 0 || (g.upd_player != 0 && i != g.upd_player)) continue;
             const R ph = reach[j * 2 * P + P + (i - 1)];
             if (ph == (R)0) continue;
             double c0 = 0, c1 = 0, c2 = 0;
             xadd(c0, c1, c2, (double)ph, g.scp0);
-            unsigned long long* ac = acc_p + ((long long)rec[kSubRec * j + 7] - sp.hc) * 3;
+            unsigned long long* ac = acc_p + ((long long)rec[2 * j + 1].w - sp.hc) * 3;
             if (c0 != 0.0) atomicAdd(ac + 0, (unsigned long long)(long long)c0);
             if (c1 != 0.0) atomicAdd(ac + 1, (unsigned long long)(long long)c1);
             if (c2 != 0.0) atomicAdd(ac + 2, (unsigned long long)(long long)c2);

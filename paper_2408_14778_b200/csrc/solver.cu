@@ -380,6 +380,7 @@ constexpr int64_t kSubMaxV = int64_t(1) << 22;
 constexpr int64_t kSubMaxSub = 16384;
 constexpr int64_t kSubMinV = 2048;      // default: below this k_tiny (many iterations per launch) wins (Kuhn)
 constexpr int64_t kSubMinCTAs = 24;     // preferred minimum of subtrees (CTAs) when choosing the cut
+constexpr int64_t kSubStreamV = int64_t(1) << 20;   // above: games with streaming levels keep the level path
 static bool sub_candidate(const Game& g) { return g.V <= kSubMaxV && g.D >= 2 && g.NS > 0; }
 // ints: per-subtree records, node records, child entries (<= V), pair entries
 // (<= V), per-level node and pair starts of every subtree
@@ -1103,12 +1104,12 @@ struct Solver final : SolverBase {
     // subtree fits one CTA's shared memory (CFR_SUB_CUT overrides).  On by default
     // for those games (CFR_FLAG_NO_SUBTREE opts out); CFR_FLAG_FORCE_SUBTREE also
     // takes games k_tiny would run.
-    void* sub_fn() const {
+    void* sub_fn(bool staged) const {
         switch (gp->Pc) {
-            case 1: return (void*)k_sub<R, I, 1>;
-            case 2: return (void*)k_sub<R, I, 2>;
-            case 3: return (void*)k_sub<R, I, 3>;
-            default: return (void*)k_sub<R, I, 4>;
+            case 1: return staged ? (void*)k_sub<R, I, 1, true> : (void*)k_sub<R, I, 1, false>;
+            case 2: return staged ? (void*)k_sub<R, I, 2, true> : (void*)k_sub<R, I, 2, false>;
+            case 3: return staged ? (void*)k_sub<R, I, 3, true> : (void*)k_sub<R, I, 3, false>;
+            default: return staged ? (void*)k_sub<R, I, 4, true> : (void*)k_sub<R, I, 4, false>;
         }
     }
     cfr_status setup_sub() {
@@ -1121,11 +1122,13 @@ struct Solver final : SolverBase {
         if (!forced && (cfg.flags & other)) return CFR_OK;
         if (!forced) {
             // default: latency-bound games only -- not the tiniest (k_tiny runs many
-            // iterations per launch there) and none with a level big enough for the
-            // streaming kernel (bandwidth-bound: measured faster on the levels)
+            // iterations per launch there), and above kSubStreamV nodes none with a
+            // level big enough for the streaming kernel (bandwidth-bound: measured
+            // faster on the levels, Battleship-7; Battleship-5 is faster in k_sub)
             if (g.V < kSubMinV) return CFR_OK;
-            for (const StreamLevel& f : stream_)
-                if (use_stream_ && f.ntiles > 0) return CFR_OK;
+            if (g.V > kSubStreamV)
+                for (const StreamLevel& f : stream_)
+                    if (use_stream_ && f.ntiles > 0) return CFR_OK;
         }
         if (world > 1 || external || (cfg.flags & CFR_FLAG_NO_SUBTREE) || !g.depth_homogeneous || !sub_candidate(g) ||
             !g.deferred_list.empty() || g.Pc > 4)
@@ -1165,40 +1168,57 @@ struct Solver final : SolverBase {
             if (nn[x] > 256) return CFR_OK;
         }
         // subtree sizes (non-terminal nodes, terminals), deepest level first
-        std::vector<int64_t> snn(NS, 0), snt(NS, 0);
+        // subtree sizes (non-terminal nodes, terminals, player (node, action) pairs,
+        // levels), deepest level first
+        std::vector<int64_t> snn(NS, 0), snt(NS, 0), snp(NS, 0), sdep(NS, 0);
         for (int L = g.D - 1; L >= 0; --L)
             for (int64_t x = g.slot_ptr[L]; x < g.slot_ptr[L + 1]; ++x) {
-                int64_t a = 1, t = 0;
+                int64_t a = 1, t = 0, q = ac[x] != 0 ? nn[x] : 0, d = 1;
                 for (int k = 0; k < nn[x]; ++k) {
                     const int64_t c = rowslot[(size_t)cb[x] + k];
-                    if (c >= 0) { a += snn[c]; t += snt[c]; } else ++t;
+                    if (c >= 0) { a += snn[c]; t += snt[c]; q += snp[c]; d = std::max(d, 1 + sdep[c]); } else ++t;
                 }
                 snn[x] = a;
                 snt[x] = t;
+                snp[x] = q;
+                sdep[x] = d;
             }
-        auto bytes_of = [&](int64_t a, int64_t t) {
-            return (((a * 2 * P + 1) & ~1LL) + ((a * Pc + 1) & ~1LL) + t * Pc) * (long long)w;
+        auto bytes_of = [&](int64_t x, bool staged) {
+            return staged ? sub_smem(snn[x], snt[x], snn[x] - 1 + snt[x], snp[x], (int)sdep[x], P, Pc, w).total
+                          : sub_smem(snn[x], snt[x], 0, 0, -1, P, Pc, w).total;
         };
-        int cut = -1;
-        long long need = 0;
         int forced_cut = -1;
         if (const char* e = std::getenv("CFR_SUB_CUT")) forced_cut = std::atoi(e);
-        // the shallowest cut whose subtrees fit one CTA and give >= kSubMinCTAs CTAs
-        // (else the fitting cut with the most subtrees)
-        int64_t best_n = -1;
-        for (int c = 1; c < g.D; ++c) {
-            const int64_t n = g.slot_ptr[c + 1] - g.slot_ptr[c];
-            if (n <= 0 || n > kSubMaxSub || (forced_cut >= 0 && c != forced_cut)) continue;
-            long long mx = 0;
-            for (int64_t x = g.slot_ptr[c]; x < g.slot_ptr[c + 1]; ++x) mx = std::max(mx, bytes_of(snn[x], snt[x]));
-            if (mx > budget) continue;
-            if (n > best_n) {
-                cut = c;
-                need = mx;
-                best_n = n;
+        int forced_staged = -1;
+        if (const char* e = std::getenv("CFR_SUB_STAGED")) forced_staged = std::atoi(e);
+        // per layout: the shallowest cut whose subtrees fit one CTA and give >=
+        // kSubMinCTAs CTAs (else the fitting cut with the most subtrees)
+        auto pick = [&](bool staged, long long* need_out) {
+            int cut = -1;
+            int64_t best_n = -1;
+            for (int c = 1; c < g.D; ++c) {
+                const int64_t n = g.slot_ptr[c + 1] - g.slot_ptr[c];
+                if (n <= 0 || n > kSubMaxSub || (forced_cut >= 0 && c != forced_cut)) continue;
+                long long mx = 0;
+                for (int64_t x = g.slot_ptr[c]; x < g.slot_ptr[c + 1]; ++x) mx = std::max(mx, bytes_of(x, staged));
+                if (mx > budget) continue;
+                if (n > best_n) {
+                    cut = c;
+                    *need_out = mx;
+                    best_n = n;
+                }
+                if (n >= kSubMinCTAs) break;
             }
-            if (n >= kSubMinCTAs) break;
-        }
+            return cut;
+        };
+        long long need_s = 0, need_g = 0;
+        const int cut_s = pick(true, &need_s), cut_g = pick(false, &need_g);
+        // staged tables unless they need a deeper cut (more trunk launches, e.g.
+        // liar's dice in f64, whose per-deal bid trees are large and skewed)
+        bool staged = cut_s >= 0 && (cut_g < 0 || cut_s <= cut_g);
+        if (forced_staged >= 0) staged = forced_staged != 0 && cut_s >= 0;
+        const int cut = staged ? cut_s : cut_g;
+        const long long need = staged ? need_s : need_g;
         if (cut < 0) return CFR_OK;
         // infosets below the cut are one id range [hc, H)
         int64_t hc = g.H;
@@ -1209,6 +1229,7 @@ struct Solver final : SolverBase {
         // tables
         SubPlan sp{};
         sp.cut = cut;
+        sp.staged = staged ? 1 : 0;
         sp.nsub = (int)(g.slot_ptr[cut + 1] - g.slot_ptr[cut]);
         sp.hc = hc;
         sp.qc = g.qbase_int[hc];
@@ -1219,27 +1240,30 @@ struct Solver final : SolverBase {
         std::vector<R> tu;
         meta.reserve((size_t)kSubMeta * sp.nsub);
         std::vector<int64_t> cur, nxt;
+        int64_t maxw = 32;   // widest level step (nodes or pairs) of any subtree: the CTA size
         for (int64_t root = g.slot_ptr[cut]; root < g.slot_ptr[cut + 1]; ++root) {
             const int64_t node0 = (int64_t)recs.size() / kSubRec, term0 = (int64_t)tu.size() / Pc;
-            const int64_t lvl0 = (int64_t)lvl.size();
+            const int64_t lvl0 = (int64_t)lvl.size(), child0 = (int64_t)chl.size(), pair0 = (int64_t)prs.size() / 4;
             std::vector<int> lstart, pstart;
             cur.assign(1, root);
-            std::vector<int> curpar(1, -1);
+            std::vector<int> curpar(1, -1), curin(1, 0);
             int64_t nloc = 0, nterm = 0;
             while (!cur.empty()) {
                 lstart.push_back((int)nloc);
-                pstart.push_back((int)(prs.size() / 4));
+                pstart.push_back((int)(prs.size() / 4 - pair0));
+                const int64_t p_before = (int64_t)prs.size() / 4;
                 nxt.clear();
-                std::vector<int> nxtpar;
+                std::vector<int> nxtpar, nxtin;
                 const int64_t base = nloc;
                 for (size_t k = 0; k < cur.size(); ++k) {
                     const int64_t x = cur[k];
                     const int j = (int)(base + (int64_t)k);
-                    const int cp = (int)chl.size();
+                    const int cp = (int)((int64_t)chl.size() - child0);
                     for (int a = 0; a < nn[x]; ++a) {
                         const int64_t row = (int64_t)cb[x] + a;
                         const int64_t c = rowslot[(size_t)row];
                         if (c >= 0) {
+                            nxtin.push_back((int)((int64_t)chl.size() - child0));
                             chl.push_back((int)(base + (int64_t)cur.size() + (int64_t)nxt.size()));
                             nxt.push_back(c);
                             nxtpar.push_back(j);
@@ -1256,21 +1280,23 @@ struct Solver final : SolverBase {
                         }
                     }
                     recs.push_back(curpar[k]);
+                    recs.push_back(curin[k]);
+                    recs.push_back((int)pa[x] | ((int)ac[x] << 8));
                     recs.push_back((int)fe[x]);
-                    recs.push_back((int)pa[x]);
-                    recs.push_back((int)ac[x]);
                     recs.push_back((int)eb[x]);
                     recs.push_back(nn[x]);
                     recs.push_back(cp);
                     recs.push_back((int)sh[x]);
                 }
+                maxw = std::max<int64_t>(maxw, std::max<int64_t>((int64_t)cur.size(), (int64_t)prs.size() / 4 - p_before));
                 nloc += (int64_t)cur.size();
                 cur.swap(nxt);
                 curpar.swap(nxtpar);
+                curin.swap(nxtin);
             }
             const int nlev = (int)lstart.size();
             lstart.push_back((int)nloc);
-            pstart.push_back((int)(prs.size() / 4));
+            pstart.push_back((int)(prs.size() / 4 - pair0));
             for (int v : lstart) lvl.push_back(v);
             const int64_t plv0 = (int64_t)lvl.size();
             for (int v : pstart) lvl.push_back(v);
@@ -1282,13 +1308,21 @@ struct Solver final : SolverBase {
             meta.push_back(nlev);
             meta.push_back((int)plv0);
             meta.push_back((int)root);
-            if (nloc != snn[root] || nterm != snt[root] || nloc >= (1 << 23)) return CFR_OK;
+            meta.push_back((int)child0);
+            meta.push_back((int)((int64_t)chl.size() - child0));
+            meta.push_back((int)pair0);
+            meta.push_back((int)((int64_t)prs.size() / 4 - pair0));
+            if (nloc != snn[root] || nterm != snt[root] || (int64_t)prs.size() / 4 - pair0 != snp[root] || nlev != sdep[root] ||
+                nloc >= (1 << 23))
+                return CFR_OK;
         }
-        // sections start on 16-byte boundaries (int4 reads of records and pairs)
+        sp.threads = (int)std::min<int64_t>(kSubThreads, (maxw + 31) / 32 * 32);
+        // sections start on 16-byte boundaries (int4 copies of records and pairs)
         auto pad4 = [](std::vector<int>& v) { while (v.size() % 4) v.push_back(0); };
         pad4(meta);
         pad4(recs);
         pad4(chl);
+        if (chl.size() - (size_t)0 > (size_t)INT32_MAX) return CFR_OK;
         sp.m_sub = 0;
         sp.m_rec = (int)meta.size();
         sp.m_child = (int)(sp.m_rec + recs.size());
@@ -1307,7 +1341,7 @@ struct Solver final : SolverBase {
         if (st) return st;
         if ((st = up(plan.subu, tu))) return st;
         CU(cudaMemsetAsync(ws + plan.suba, 0, (size_t)3 * (sp.nq + sp.nh) * sizeof(unsigned long long), stream));
-        CU(cudaFuncSetAttribute(sub_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, sp.bytes));
+        CU(cudaFuncSetAttribute(sub_fn(sp.staged != 0), cudaFuncAttributeMaxDynamicSharedMemorySize, sp.bytes));
         CU(cudaStreamSynchronize(stream));
         sub_plan_ = sp;
         sub_ = true;
@@ -1434,12 +1468,16 @@ struct Solver final : SolverBase {
         const int* tab = at<int>(plan.subt);
         const R* tu = at<R>(plan.subu);
         unsigned long long* acc = at<unsigned long long>(plan.suba);
+#define CFRB_SUB(PC)                                                                                               \
+    (sp.staged ? launch(pdl_, k_sub<R, I, PC, true>, dim3(sp.nsub), dim3(sp.threads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp) \
+               : launch(pdl_, k_sub<R, I, PC, false>, dim3(sp.nsub), dim3(sp.threads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp))
         switch (g.Pc) {
-            case 1: launch(pdl_, k_sub<R, I, 1>, dim3(sp.nsub), dim3(kSubThreads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp); break;
-            case 2: launch(pdl_, k_sub<R, I, 2>, dim3(sp.nsub), dim3(kSubThreads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp); break;
-            case 3: launch(pdl_, k_sub<R, I, 3>, dim3(sp.nsub), dim3(kSubThreads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp); break;
-            default: launch(pdl_, k_sub<R, I, 4>, dim3(sp.nsub), dim3(kSubThreads), (size_t)sp.bytes, st, dg, tab, tu, acc, sp); break;
+            case 1: CFRB_SUB(1); break;
+            case 2: CFRB_SUB(2); break;
+            case 3: CFRB_SUB(3); break;
+            default: CFRB_SUB(4); break;
         }
+#undef CFRB_SUB
         const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((sp.nh + 255) / 256, 4LL * num_sms_));
         launch(pdl_, k_sub_update<R, I>, dim3(nb), dim3(256), 0, st, dg, acc, sp);
         mark(st, ev, 1, sp.cut);

@@ -112,3 +112,16 @@ def test_subtree_longer_runs(cuda, name, variant):
     n = s.launches_per_iteration()
     ref = pb.Solver(pb.Game(gamegen.by_name(name)), variant=1, precision=64, flags=F).launches_per_iteration()
     assert n == (2 * ref if variant == 4 else ref)
+
+
+@pytest.mark.parametrize("staged", ["0", "1"])
+@pytest.mark.parametrize("name,precision", [("leduc", 64), ("goofspiel", 64), ("liars_dice", 32),
+                                            ("battleship3", 64)])
+def test_subtree_table_layouts(cuda, name, precision, staged, monkeypatch):
+    """Both k_sub layouts: tables and edge probabilities staged in shared memory,
+    or read from global memory in each level step (CFR_SUB_STAGED forces one)."""
+    from gamegen.battleship import paper_battleship
+    desc = paper_battleship(name) if name.startswith("battleship") else gamegen.by_name(name)
+    monkeypatch.setenv("CFR_SUB_STAGED", staged)
+    out, s, o = run_pair(desc, 1, precision, 40, flags=F)
+    sub_levels(s)
