@@ -774,7 +774,10 @@ struct Solver final : SolverBase {
             // ~50 KB) resident per SM (measured best, tools/stream_sweep.py)
             int tile = (sizeof(R) == 4 && !(cfg.flags & CFR_FLAG_FUSED_FORWARD)) ? 2 * kStreamConsumers : kStreamConsumers;
             if (const char* e = std::getenv("CFR_STREAM_TILE")) tile = std::max(32, std::min(1024, std::atoi(e)));
-            stream_ = stream_levels<R, I>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : num_sms_, stages, tile,
+            // levels with fewer tiles than min_tiles stay on the tile kernel (CFR_STREAM_MIN_TILES: A/B)
+            int min_tiles = num_sms_;
+            if (const char* e = std::getenv("CFR_STREAM_MIN_TILES")) min_tiles = std::max(1, std::atoi(e));
+            stream_ = stream_levels<R, I>(g, s_cb_u, &sp, (cfg.flags & CFR_FLAG_FORCE_STREAM) ? 1 : min_tiles, stages, tile,
                                           (cfg.flags & CFR_FLAG_FUSED_FORWARD) != 0, std::getenv("CFR_NO_COMPACT") == nullptr,
                                           tile_contrib_);
             if (sp.size() > stream_pool_bound(g)) {
