@@ -44,7 +44,7 @@ namespace cfrb {
 // 16-byte records, sigma and child references batched 8 actions at a time.
 constexpr int kSubMeta = 12;
 constexpr int kSubRec = 8;
-constexpr int kSubThreads = 512;
+constexpr int kSubThreads = 1024;
 
 struct SubPlan {
     int nsub;          // subtrees (= CTAs)
@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
     for (int l = nlev - 1; l >= 0; --l) {
         // values (Eq 1: ascending actions from +0)
         for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
+            const int4 ea = rec[2 * j];
             const int4 bb = rec[2 * j + 1];
             const int eb = bb.x, nch = bb.y, cp = bb.z;
             R v[PC];
@@ -182,6 +183,20 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
             }
 #pragma unroll
             for (int c = 0; c < PC; ++c) val[(long long)j * PC + c] = v[c];
+            // exact slices of pi_hat (Eq 5 / Eq 10 weights) of a player node (the
+            // reach factors are final since the forward pass)
+            const int i = ea.z >> 8;
+            if (i != 0 && (g.upd_player == 0 || i == g.upd_player)) {
+                const R ph = reach[j * 2 * P + P + (i - 1)];
+                if (ph != (R)0) {
+                    double c0 = 0, c1 = 0, c2 = 0;
+                    xadd(c0, c1, c2, (double)ph, g.scp0);
+                    unsigned long long* ac = acc_p + ((long long)bb.w - sp.hc) * 3;
+                    if (c0 != 0.0) atomicAdd(ac + 0, (unsigned long long)(long long)c0);
+                    if (c1 != 0.0) atomicAdd(ac + 1, (unsigned long long)(long long)c1);
+                    if (c2 != 0.0) atomicAdd(ac + 2, (unsigned long long)(long long)c2);
+                }
+            }
         }
         __syncthreads();
         // exact slices of the regret terms pi_check * (u(child) - u(node)) of this
@@ -200,20 +215,6 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
             xadd(c0, c1, c2, (double)t, g.sc0);
             if (PC == 1 && i == 2) { c0 = -c0; c1 = -c1; c2 = -c2; }   // u2 = -u1 storage
             unsigned long long* ac = acc_r + ((long long)pr.z - sp.qc) * 3;
-            if (c0 != 0.0) atomicAdd(ac + 0, (unsigned long long)(long long)c0);
-            if (c1 != 0.0) atomicAdd(ac + 1, (unsigned long long)(long long)c1);
-            if (c2 != 0.0) atomicAdd(ac + 2, (unsigned long long)(long long)c2);
-        }
-        // exact slices of pi_hat (Eq 5 / Eq 10 weights) of this level's player nodes
-        for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
-            const int4 ea = rec[2 * j];
-            const int i = ea.z >> 8;
-            if (i == 0 || (g.upd_player != 0 && i != g.upd_player)) continue;
-            const R ph = reach[j * 2 * P + P + (i - 1)];
-            if (ph == (R)0) continue;
-            double c0 = 0, c1 = 0, c2 = 0;
-            xadd(c0, c1, c2, (double)ph, g.scp0);
-            unsigned long long* ac = acc_p + ((long long)rec[2 * j + 1].w - sp.hc) * 3;
             if (c0 != 0.0) atomicAdd(ac + 0, (unsigned long long)(long long)c0);
             if (c1 != 0.0) atomicAdd(ac + 1, (unsigned long long)(long long)c1);
             if (c2 != 0.0) atomicAdd(ac + 2, (unsigned long long)(long long)c2);
