@@ -42,6 +42,14 @@ namespace cfrb {
 // shared-memory work and a barrier.  Otherwise (larger subtrees at a shallower
 // cut) the tables and sigma are read from global memory (L2) in each level step:
 // 16-byte records, sigma and child references batched 8 actions at a time.
+// -DCFR_SUB_CHECKS builds (tools/sub_checks.sh) trap on any out-of-range table
+// entry or shared-memory index: the bounds checks that stand in for
+// compute-sanitizer, which is closed on this pool.  Product builds compile them out.
+#ifdef CFR_SUB_CHECKS
+#define SUB_CHECK(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define SUB_CHECK(c) do { } while (0)
+#endif
 constexpr int kSubMeta = 12;
 constexpr int kSubRec = 8;
 constexpr int kSubThreads = 1024;
@@ -88,6 +96,13 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
     const int node0 = mb[0], nn = mb[1], term0 = mb[2], nt = mb[3], lvl0 = mb[4], nlev = mb[5];
     const int root_slot = mb[7], child0 = mb[8], ne = mb[9], pair0 = mb[10], np = mb[11];
     const SubSmem L = sub_smem(nn, nt, STAGED ? ne : 0, STAGED ? np : 0, STAGED ? nlev : -1, P, PC, (int)sizeof(R));
+#ifdef CFR_SUB_CHECKS
+    {
+        unsigned dyn = 0;
+        asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        SUB_CHECK(L.total <= (long long)dyn && nn >= 1 && nt >= 0 && ne == nn - 1 + nt && np >= 0 && nlev >= 1);
+    }
+#endif
     R* const reach = reinterpret_cast<R*>(smem_raw + L.reach);    // [nn][2P]
     R* const val = reinterpret_cast<R*>(smem_raw + L.val);        // [nn][PC]
     R* const tv = reinterpret_cast<R*>(smem_raw + L.tv);          // [nt][PC] terminal utilities
@@ -124,6 +139,7 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
         // edge probabilities of this iteration (sigma is constant during the pass)
         for (int j = tid; j < nn; j += nth) {
             const int4 bb = rec[2 * j + 1];
+            SUB_CHECK(bb.z >= 0 && bb.y >= 0 && bb.z + bb.y <= ne && bb.x >= 0);
             for (int a = 0; a < bb.y; ++a) ev[bb.z + a] = g.sig[bb.x + a];
         }
     }
@@ -134,6 +150,7 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
         for (int j = lv[l] + tid; j < lv[l + 1]; j += nth) {
             const int4 ea = rec[2 * j];
             const int p = ea.x;
+            SUB_CHECK(j < nn && p >= 0 && p < j && ea.y >= 0 && ea.y < ne && ea.w >= 0);
             const R x = STAGED ? ev[ea.y] : g.sig[ea.w];
             const int act = ea.z & 255;
             for (int i = 0; i < P; ++i) {
@@ -151,6 +168,7 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
             const int4 ea = rec[2 * j];
             const int4 bb = rec[2 * j + 1];
             const int eb = bb.x, nch = bb.y, cp = bb.z;
+            SUB_CHECK(j < nn && cp >= 0 && nch >= 0 && cp + nch <= ne);
             R v[PC];
 #pragma unroll
             for (int c = 0; c < PC; ++c) v[c] = (R)0;
@@ -158,6 +176,7 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
                 for (int a = 0; a < nch; ++a) {
                     const R x = ev[cp + a];
                     const int ch = chl[cp + a];
+                    SUB_CHECK(ch < nn && ch >= -nt && (ch < 0 || ch > j));
                     const R* u = (ch >= 0) ? val + (long long)ch * PC : tv + (long long)(-1 - ch) * PC;
 #pragma unroll
                     for (int c = 0; c < PC; ++c) v[c] = v[c] + x * u[c];
@@ -175,6 +194,7 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         if (a0 + k >= nch) break;
+                        SUB_CHECK(ch[k] < nn && ch[k] >= -nt && (ch[k] < 0 || ch[k] > j));
                         const R* u = (ch[k] >= 0) ? val + (long long)ch[k] * PC : tv + (long long)(-1 - ch[k]) * PC;
 #pragma unroll
                         for (int c = 0; c < PC; ++c) v[c] = v[c] + x[k] * u[c];
@@ -189,6 +209,7 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
             if (i != 0 && (g.upd_player == 0 || i == g.upd_player)) {
                 const R ph = reach[j * 2 * P + P + (i - 1)];
                 if (ph != (R)0) {
+                    SUB_CHECK(bb.w >= sp.hc && bb.w < sp.hc + sp.nh && i <= P);
                     double c0 = 0, c1 = 0, c2 = 0;
                     xadd(c0, c1, c2, (double)ph, g.scp0);
                     unsigned long long* ac = acc_p + ((long long)bb.w - sp.hc) * 3;
@@ -204,6 +225,8 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
         for (int k = plv[l] + tid; k < plv[l + 1]; k += nth) {
             const int4 pr = prs[k];
             const int j = pr.x >> 8, ch = pr.y, i = pr.w;
+            SUB_CHECK(k < np && j >= 0 && j < nn && ch < nn && ch >= -nt && i >= 1 && i <= P && pr.z >= sp.qc &&
+                      pr.z < sp.qc + sp.nq);
             if (g.upd_player != 0 && i != g.upd_player) continue;
             const R pc = reach[j * 2 * P + (i - 1)];
             if (pc == (R)0) continue;
