@@ -1125,16 +1125,18 @@ struct Solver final : SolverBase {
         if (!forced && (cfg.flags & other)) return CFR_OK;
         if (!forced) {
             // default: latency-bound games only -- not the tiniest (k_tiny runs many
-            // iterations per launch there), and above kSubStreamV nodes none with a
-            // level big enough for the streaming kernel (bandwidth-bound: measured
-            // faster on the levels, Battleship-7; Battleship-5 is faster in k_sub)
+            // iterations per launch there); above kSubStreamV nodes, a game with a
+            // level big enough for the streaming kernel keeps the level path when
+            // most of its nodes are terminals (bandwidth-bound: Battleship-7, 92 %
+            // terminals, 120 vs 190 us/it) and takes k_sub otherwise (Goofspiel-6,
+            // 26 % terminals, 163 vs 292 us/it)
             if (g.V < kSubMinV) return CFR_OK;
-            if (g.V > kSubStreamV)
+            if (g.V > kSubStreamV && 2 * g.num_terminals > g.V)
                 for (const StreamLevel& f : stream_)
                     if (use_stream_ && f.ntiles > 0) return CFR_OK;
         }
         if (world > 1 || external || (cfg.flags & CFR_FLAG_NO_SUBTREE) || !g.depth_homogeneous || !sub_candidate(g) ||
-            !g.deferred_list.empty() || g.Pc > 4)
+            g.Pc > 4)
             return CFR_OK;
         const int64_t NS = g.NS;
         const int P = g.P, Pc = g.Pc, w = (int)sizeof(R);
@@ -1229,6 +1231,11 @@ struct Solver final : SolverBase {
             if (sh[x] >= 0) hc = std::min(hc, sh[x]);
         for (int64_t x = 0; x < g.slot_ptr[cut]; ++x)
             if (sh[x] >= hc) return CFR_OK;
+        // deferred infosets (member groups split across tiles) are fine below the cut
+        // -- every infoset there is accumulated globally and updated by k_sub_update --
+        // but not in the trunk, whose level kernels update in-tile
+        for (const int64_t h : g.deferred_list)
+            if (h < hc) return CFR_OK;
         // tables
         SubPlan sp{};
         sp.cut = cut;
@@ -1617,7 +1624,7 @@ struct Solver final : SolverBase {
                 }
                 mark(st, ev, 3, -1);
             }
-            launch_update(st, ev);
+            if (!sub_) launch_update(st, ev);   // subtree mode: every deferred infoset is below the cut (k_sub_update)
         }
         dg.upd_player = 0;
         pass_final_ = 1;

@@ -125,3 +125,13 @@ def test_subtree_table_layouts(cuda, name, precision, staged, monkeypatch):
     monkeypatch.setenv("CFR_SUB_STAGED", staged)
     out, s, o = run_pair(desc, 1, precision, 40, flags=F)
     sub_levels(s)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_subtree_with_deferred_infosets(cuda, precision):
+    """Goofspiel-6 (2.0 M nodes; infosets of up to 230 members, split across tiles and
+    so deferred on the level path): below the cut every infoset is accumulated
+    globally anyway, so the subtree mode takes them (k_deferred is not launched)."""
+    desc = gamegen.goofspiel(6)
+    out, s, o = run_pair(desc, 1, precision, 6, flags=F, checks=("state",))
+    sub_levels(s)
