@@ -264,6 +264,21 @@ def per_game(pb, torch, with_oracle: bool):
         if name in PAPER_SETUP_S:
             e["setup_s"]["paper"] = PAPER_SETUP_S[name]
         del s
+        if "k_sub" in e["kernels"]:
+            # the same game on the per-level kernels (CFR_FLAG_NO_SUBTREE): what the
+            # subtree mode buys on this line
+            s = pb.Solver(g, variant=variant, precision=prec, flags=pb.FLAG_NO_SUBTREE)
+            s.run(5)
+            e0.record(s.stream)
+            s.enqueue(iters)
+            e1.record(s.stream)
+            s.sync()
+            ms_l = e0.elapsed_time(e1) / iters
+            e["level_path"] = {"it_per_s": round(1e3 / ms_l, 1), "launches_per_iter": s.launches_per_iteration(),
+                               "kernels": sorted({k for k in s.level_kernels() if k})
+                               if s.launches_per_iteration() > 1 else ["k_tiny"]}
+            e["subtree_speedup"] = round(ms_l / ms, 2)
+            del s
         if with_oracle:
             import oracle
 
