@@ -80,3 +80,20 @@ def test_overflow_streaming_kernel(cuda, precision, big):
     assert (np.abs(u - v[par]) > fmax)[leaf_parents[par]].any()
     s = expect_numerical(desc, "cfr", precision, pb.FLAG_FORCE_STREAM, 6, 1)
     assert "k_bwd_stream" in s.level_kernels()
+
+
+@pytest.mark.parametrize("precision,big", [(64, 1.7e308), (32, 3.3e38)])
+@pytest.mark.parametrize("name", ["leduc", "goofspiel"])
+def test_overflow_subtree_mode(cuda, name, precision, big):
+    """A saturated game through the subtree mode (k_sub + k_sub_update, the default
+    for these games) reports the same first non-finite iteration as the per-level
+    kernels (CFR_FLAG_NO_SUBTREE)."""
+    desc = saturated(gamegen.by_name(name), big)
+    ref = pb.Solver(pb.Game(desc), variant="cfr", precision=precision, flags=pb.FLAG_NO_SUBTREE)
+    with pytest.raises(pb.NativeError) as ei:
+        ref.run(8)
+    assert ei.value.status == CFR_ERR_NUMERICAL, ei.value
+    import re
+    t_bad = int(re.search(r"iteration (\d+)", str(ei.value)).group(1))
+    s = expect_numerical(desc, "cfr", precision, 0, 8, t_bad)
+    assert "k_sub" in s.level_kernels()

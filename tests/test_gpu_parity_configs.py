@@ -103,8 +103,13 @@ def test_bench_shaped_default_flags(cuda):
 @pytest.mark.parametrize("precision,T", [(64, 20), (32, 10)])
 def test_goofspiel6_paper_scale(cuda, precision, T):
     """Goofspiel with 6 cards (2.0M nodes, the second real workload at the scale of
-    the paper's Experiment 2): default kernel choice (streaming levels included),
-    bit-identical to the oracle."""
-    out, s, _ = run_pair(gamegen.goofspiel(6), 1, precision, T)
+    the paper's Experiment 2): the default kernel choice (the subtree mode, k_sub)
+    and the per-level kernels (streaming levels included), both bit-identical to
+    the oracle."""
+    desc = gamegen.goofspiel(6)
+    out, s, _ = run_pair(desc, 1, precision, T)
+    assert "k_sub" in s.level_kernels()
+    out, s, _ = run_pair(desc, 1, precision, T, flags=pb.FLAG_NO_SUBTREE,
+                         oracle_obj=oracle.Oracle(desc, precision=precision))
     if precision == 64:   # (f32 rows of its widest levels are too short for the streaming tiles)
         assert "k_bwd_stream" in s.level_kernels()
