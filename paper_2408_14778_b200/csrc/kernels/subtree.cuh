@@ -62,6 +62,11 @@ struct SubPlan {
     int bytes;         // dynamic shared memory (the largest subtree)
     int threads;       // CTA size
     int staged;        // 1: tables and edge probabilities staged in shared memory
+    int trunk;         // 1: the trunk (depths < c) holds chance nodes only -- k_sub computes each
+                       //    root's reach along its path, k_sub_update's last CTA the trunk values
+    int m_path;        // trunk: per subtree the sigma_ext edges root path, top-down (cut ints each)
+    int m_trunk;       // trunk: per trunk slot {U row of the node, first child U row, sigma_ext base, children}
+    int ntrunk;        // trunk slots (levels 0..c-1, level-major)
     int m_sub, m_rec, m_child, m_pair, m_lvl;   // int offsets inside the table block
 };
 
@@ -143,7 +148,26 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
             for (int a = 0; a < bb.y; ++a) ev[bb.z + a] = g.sig[bb.x + a];
         }
     }
-    if (tid < 2 * P) reach[tid] = g.reach[(long long)root_slot * 2 * P + tid];   // level-c forward kernel's row
+    if (sp.trunk) {
+        // chance-only trunk: the root's reach is the path product of its chance edges
+        // (k_fwd's operations with a chance parent: every pi_check times the edge's
+        // probability, top-down from the root row of ones; pi_hat unchanged)
+        if (tid == 0) {
+            R pc[8];
+            for (int i = 0; i < P; ++i) pc[i] = (R)1;
+            const int* path = T + sp.m_path + (long long)sp.cut * b;
+            for (int k = 0; k < sp.cut; ++k) {
+                const R x = g.sig[path[k]];
+                for (int i = 0; i < P; ++i) pc[i] = pc[i] * x;
+            }
+            for (int i = 0; i < P; ++i) {
+                reach[i] = pc[i];
+                reach[P + i] = (R)1;
+            }
+        }
+    } else if (tid < 2 * P) {
+        reach[tid] = g.reach[(long long)root_slot * 2 * P + tid];   // level-c forward kernel's row
+    }
     __syncthreads();
     // ---- forward (Eq 2 / Eq 4 with reading Q1; k_fwd's operations)
     for (int l = 1; l < nlev; ++l) {
@@ -258,8 +282,9 @@ __global__ void __launch_bounds__(kSubThreads) k_sub(DG<R, I> g, const int* __re
 // before its first store (restrict-qualified copies of the state pointers), so
 // the chain is one round trip of loads, not one per action.
 constexpr int kSubUpdRegs = 8;   // actions kept in registers (wider infosets: generic loop)
-template <class R, class I>
-__global__ void __launch_bounds__(256) k_sub_update(DG<R, I> g, unsigned long long* __restrict__ acc, SubPlan sp) {
+template <class R, class I, int PC>
+__global__ void __launch_bounds__(256) k_sub_update(DG<R, I> g, unsigned long long* __restrict__ acc, SubPlan sp,
+                                                    const int* __restrict__ T, int last) {
     pdl_trigger();
     pdl_wait();
     const long long t_iter = g.ctrl[0] + 1;
@@ -363,6 +388,49 @@ __global__ void __launch_bounds__(256) k_sub_update(DG<R, I> g, unsigned long lo
         }
     }
     if (bad) atomicMin(&g.ctrl[1], t_iter);
+    if (sp.trunk || last) {
+        // the last CTA to finish: the chance-only trunk's values (Eq 1, depths c-1..0,
+        // k_bwd's operations) from the subtree roots' values, then the iteration count
+        __shared__ int is_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const unsigned long long prev = atomicAdd((unsigned long long*)&g.ctrl[2], 1ULL);
+            is_last = (prev == gridDim.x - 1) ? 1 : 0;
+        }
+        __syncthreads();
+        if (is_last) {
+            __threadfence();
+            if (sp.trunk) {
+                const int4* tr = reinterpret_cast<const int4*>(T + sp.m_trunk);
+                // trunk slots are level-major: deepest level last, so walk back by level
+                for (int L = sp.cut - 1; L >= 0; --L) {
+                    for (int k = threadIdx.x; k < sp.ntrunk; k += blockDim.x) {
+                        const int4 e = tr[k];   // {node U row, first child U row, sigma_ext base, children | level << 16}
+                        if ((e.w >> 16) != L) continue;
+                        const int nch = e.w & 0xffff;
+                        R v[PC];
+#pragma unroll
+                        for (int c = 0; c < PC; ++c) v[c] = (R)0;
+                        for (int a = 0; a < nch; ++a) {
+                            const R x = g.sig[e.z + a];
+#pragma unroll
+                            for (int c = 0; c < PC; ++c) v[c] = v[c] + x * g.U[(long long)(e.y + a) * PC + c];
+                        }
+#pragma unroll
+                        for (int c = 0; c < PC; ++c) g.U[(long long)e.x * PC + c] = v[c];
+                    }
+                    __threadfence_block();
+                    __syncthreads();
+                }
+            }
+            if (threadIdx.x == 0) {
+                if (last) g.ctrl[0] = t_iter;
+                g.ctrl[2] = 0;
+            }
+        }
+    }
 }
+
 
 }  // namespace cfrb

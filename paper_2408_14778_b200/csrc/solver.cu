@@ -385,7 +385,8 @@ static bool sub_candidate(const Game& g) { return g.V <= kSubMaxV && g.D >= 2 &&
 // ints: per-subtree records, node records, child entries (<= V), pair entries
 // (<= V), per-level node and pair starts of every subtree
 static size_t sub_table_bound(const Game& g) {
-    return (size_t)(kSubMeta * kSubMaxSub + kSubRec * g.NS + 5 * g.V + 2 * kSubMaxSub * (g.D + 2) + 64);
+    return (size_t)(kSubMeta * kSubMaxSub + kSubRec * g.NS + 5 * g.V + 2 * kSubMaxSub * (g.D + 2) + 16 * kSubMaxSub +
+                    4 * g.NS + 64);
 }
 
 template <class R, class I>
@@ -1145,12 +1146,13 @@ struct Solver final : SolverBase {
         CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         const long long budget = optin - 1024;
         // the device slot tables (the numbers the level kernels use)
-        std::vector<I> fe(NS), cb(NS), eb(NS), nd(NS);
+        std::vector<I> fe(NS), cb(NS), eb(NS), nd(NS), fpar(NS);
         std::vector<unsigned char> pa(NS), ac(NS);
         std::vector<int> nn(NS);
         const long long nU = plan_u_rows() * Pc;
         std::vector<R> U((size_t)nU);
         CU(cudaStreamSynchronize(stream));
+        CU(cudaMemcpy(fpar.data(), ws + plan.f_parent, NS * sizeof(I), cudaMemcpyDeviceToHost));
         CU(cudaMemcpy(fe.data(), ws + plan.f_e, NS * sizeof(I), cudaMemcpyDeviceToHost));
         CU(cudaMemcpy(pa.data(), ws + plan.f_pact, NS, cudaMemcpyDeviceToHost));
         CU(cudaMemcpy(ac.data(), ws + plan.s_actor, NS, cudaMemcpyDeviceToHost));
@@ -1333,12 +1335,50 @@ struct Solver final : SolverBase {
         pad4(recs);
         pad4(chl);
         if (chl.size() - (size_t)0 > (size_t)INT32_MAX) return CFR_OK;
+        // chance-only trunk (every slot above the cut a chance node): each root's
+        // sigma_ext path top-down, and the trunk slots for k_sub_update's last CTA
+        std::vector<int> path, trunk;
+        {
+            bool chance_trunk = P <= 8 && cut <= 16 && g.slot_ptr[cut] <= 65536;
+            for (int64_t x = 0; x < g.slot_ptr[cut] && chance_trunk; ++x) chance_trunk = ac[x] == 0;
+            if (const char* e = std::getenv("CFR_SUB_TRUNK"))
+                if (std::atoi(e) == 0) chance_trunk = false;
+            if (chance_trunk) {
+                for (int64_t root = g.slot_ptr[cut]; root < g.slot_ptr[cut + 1] && chance_trunk; ++root) {
+                    std::vector<int> up;
+                    int64_t x = root;
+                    for (int k = 0; k < cut; ++k) {
+                        if (x <= 0 || lev[x] != cut - k) { chance_trunk = false; break; }
+                        up.push_back((int)fe[x]);
+                        x = (int64_t)fpar[x];
+                    }
+                    if (x != 0) chance_trunk = false;
+                    for (int k = cut - 1; k >= 0 && chance_trunk; --k) path.push_back(up[k]);
+                }
+                for (int64_t x = 0; x < g.slot_ptr[cut] && chance_trunk; ++x) {
+                    trunk.push_back((int)nd[x]);
+                    trunk.push_back((int)cb[x]);
+                    trunk.push_back((int)eb[x]);
+                    trunk.push_back(nn[x] | (lev[x] << 16));
+                }
+            }
+            sp.trunk = chance_trunk ? 1 : 0;
+            if (!chance_trunk) {
+                path.clear();
+                trunk.clear();
+            }
+        }
+        pad4(lvl);
+        pad4(path);
         sp.m_sub = 0;
         sp.m_rec = (int)meta.size();
         sp.m_child = (int)(sp.m_rec + recs.size());
         sp.m_pair = (int)(sp.m_child + chl.size());
         sp.m_lvl = (int)(sp.m_pair + prs.size());
-        const size_t total = (size_t)sp.m_lvl + lvl.size();
+        sp.m_path = (int)(sp.m_lvl + lvl.size());
+        sp.m_trunk = (int)(sp.m_path + path.size());
+        sp.ntrunk = (int)(trunk.size() / 4);
+        const size_t total = (size_t)sp.m_trunk + trunk.size();
         if (total > sub_table_bound(g) || tu.size() > (size_t)g.V * Pc + 2) return CFR_OK;
         std::vector<int> tab;
         tab.reserve(total);
@@ -1347,6 +1387,8 @@ struct Solver final : SolverBase {
         tab.insert(tab.end(), chl.begin(), chl.end());
         tab.insert(tab.end(), prs.begin(), prs.end());
         tab.insert(tab.end(), lvl.begin(), lvl.end());
+        tab.insert(tab.end(), path.begin(), path.end());
+        tab.insert(tab.end(), trunk.begin(), trunk.end());
         cfr_status st = up(plan.subt, tab);
         if (st) return st;
         if ((st = up(plan.subu, tu))) return st;
@@ -1360,6 +1402,7 @@ struct Solver final : SolverBase {
     int64_t count_launches() const {
         const Game& g = *gp;
         int64_t n = 0;
+        if (sub_ && sub_plan_.trunk) return (cfg.variant == CFR_PLUS_ALT) ? 2 * g.P : 2;
         if (sub_) {
             for (int l = 1; l <= sub_plan_.cut; ++l)
                 if (g.slot_ptr[l + 1] > g.slot_ptr[l]) ++n;
@@ -1471,10 +1514,11 @@ struct Solver final : SolverBase {
     void launch_sub(cudaStream_t st, std::vector<Mark>* ev) {
         const Game& g = *gp;
         const SubPlan sp = sub_plan_;
-        for (int l = 1; l <= sp.cut; ++l) {
-            fwd_level(st, dg.sig, l, 0);
-            mark(st, ev, 0, l);
-        }
+        if (!sp.trunk)
+            for (int l = 1; l <= sp.cut; ++l) {
+                fwd_level(st, dg.sig, l, 0);
+                mark(st, ev, 0, l);
+            }
         const int* tab = at<int>(plan.subt);
         const R* tu = at<R>(plan.subu);
         unsigned long long* acc = at<unsigned long long>(plan.suba);
@@ -1489,8 +1533,15 @@ struct Solver final : SolverBase {
         }
 #undef CFRB_SUB
         const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((sp.nh + 255) / 256, 4LL * num_sms_));
-        launch(pdl_, k_sub_update<R, I>, dim3(nb), dim3(256), 0, st, dg, acc, sp);
+        const int last = (sp.trunk && pass_final_) ? 1 : 0;
+        switch (g.Pc) {
+            case 1: launch(pdl_, k_sub_update<R, I, 1>, dim3(nb), dim3(256), 0, st, dg, acc, sp, tab, last); break;
+            case 2: launch(pdl_, k_sub_update<R, I, 2>, dim3(nb), dim3(256), 0, st, dg, acc, sp, tab, last); break;
+            case 3: launch(pdl_, k_sub_update<R, I, 3>, dim3(nb), dim3(256), 0, st, dg, acc, sp, tab, last); break;
+            default: launch(pdl_, k_sub_update<R, I, 4>, dim3(nb), dim3(256), 0, st, dg, acc, sp, tab, last); break;
+        }
         mark(st, ev, 1, sp.cut);
+        if (sp.trunk) return;   // the trunk's values and the iteration count: k_sub_update's last CTA
         for (int L = sp.cut - 1; L >= 0; --L) {
             bwd_level<MODE_CFR>(st, dg.sig, L, 0, (L == 0 && pass_final_) ? 1 : 0);
             mark(st, ev, 1, L);

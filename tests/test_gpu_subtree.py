@@ -135,3 +135,21 @@ def test_subtree_with_deferred_infosets(cuda, precision):
     desc = gamegen.goofspiel(6)
     out, s, o = run_pair(desc, 1, precision, 6, flags=F, checks=("state",))
     sub_levels(s)
+
+
+@pytest.mark.parametrize("trunk", ["1", "0"])
+@pytest.mark.parametrize("name,variant", [("leduc", 0), ("leduc", 4), ("liars_dice", 1)])
+def test_subtree_chance_trunk(cuda, name, variant, trunk, monkeypatch):
+    """A chance-only trunk (Leduc's and liar's dice's deals) folded into the subtree
+    launches: k_sub computes each root's reach along its chance path and
+    k_sub_update's last CTA the trunk values and the iteration count -- two launches
+    per pass; CFR_SUB_TRUNK=0 keeps the trunk's level kernels.  Both match the
+    oracle."""
+    monkeypatch.setenv("CFR_SUB_TRUNK", trunk)
+    T = 40 if name == "liars_dice" else 300
+    out, s, o = run_pair(gamegen.by_name(name), variant, 64, T, flags=F)
+    passes = 2 if variant == 4 else 1
+    if trunk == "1":
+        assert s.launches_per_iteration() == 2 * passes
+    else:
+        assert s.launches_per_iteration() > 2 * passes
