@@ -143,10 +143,14 @@ typedef struct {
                          /* (they are used automatically for >= 2^31 entries)     */
                          /* bit 9: disable the subtree kernel (k_sub: the levels  */
                          /* below a cut in one launch, subtree state in shared    */
-                         /* memory, exact int64 infoset sums; default for         */
-                         /* single-GPU games of <= 2^22 nodes that k_tiny does    */
-                         /* not take); bit 10: the subtree    */
-                         /* kernel even where k_tiny fits                         */
+                         /* memory, exact int64 infoset sums, */
+                         /* DESIGN.md §6.3; default for single-GPU, depth-        */
+                         /* homogeneous games of 2,048 - 2^22 nodes without       */
+                         /* deferred infosets above the cut, and above 2^20 nodes */
+                         /* only without streaming-size levels or with fewer than */
+                         /* half the nodes terminal; flags 4/5/6/7/8 keep the     */
+                         /* level kernels); bit 10: the subtree kernel whenever   */
+                         /* a cut fits (also where k_tiny would run)              */
     int32_t reserved;
 } cfr_solver_config;
 
