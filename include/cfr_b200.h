@@ -6,8 +6,9 @@
  * level-by-level backward value pass, per-infoset aggregation, regret and
  * average-strategy accumulation) as hand-written sm_100a CUDA kernels: per-level
  * kernels captured in a CUDA Graph (big levels through the TMA-streamed backward
- * kernel), or, for games whose state fits one CTA's shared memory, one
- * single-CTA launch per enqueue.  Update rules: CFR, CFR+, linear CFR, DCFR and
+ * kernel); for latency-bound games the levels below a cut as one subtree launch
+ * plus one update launch (the subtree mode, CFR_FLAG_NO_SUBTREE); for games whose
+ * state fits one CTA's shared memory, one single-CTA launch per enqueue.  Update rules: CFR, CFR+, linear CFR, DCFR and
  * alternating-update CFR+ (cfr_variant).  Everything below is plain C: host or device pointers and
  * sizes, no C++ or torch types.  No exception ever crosses this boundary; every
  * call returns a cfr_status and, on failure, leaves a message in
