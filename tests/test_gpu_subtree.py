@@ -153,3 +153,19 @@ def test_subtree_chance_trunk(cuda, name, variant, trunk, monkeypatch):
         assert s.launches_per_iteration() == 2 * passes
     else:
         assert s.launches_per_iteration() > 2 * passes
+
+
+def test_chance_trunk_tracked_and_profile(cuda):
+    """Leduc through the folded chance trunk: the in-graph exploitability curve and
+    the per-launch profile run on it, and the curve matches the oracle."""
+    desc = gamegen.leduc()
+    g = pb.Game(desc)
+    s = pb.Solver(g, variant="cfr+", precision=64)
+    assert s.launches_per_iteration() == 2
+    tr = s.run_tracked(40, 20)
+    o = oracle.Oracle(desc, precision=64).run(40, 1)
+    assert list(tr["T"]) == [20, 40]
+    assert_same("NashConv at T=40", [tr["nash_conv"][-1]], [o.exploitability()["nash_conv"]], 64)
+    p = s.profile(3)
+    assert p["bwd_ms"] > 0
+    assert s.iteration == 43
