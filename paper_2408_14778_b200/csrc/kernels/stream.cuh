@@ -365,7 +365,10 @@ __global__ void __launch_bounds__(kStreamThreads, CFR_STREAM_MINB) k_bwd_stream(
                         // chunks would otherwise give 2-way conflicts); the additions
                         // stay in ascending action order
                         const V* sg4 = reinterpret_cast<const V*>(sg);
-                        const int d = (m >> 2) & 1;
+                        // (f64 only: for float4 rows the selects cost more than the
+                        // conflicts -- L10 f32 0.871 vs 0.892 ms without the stagger,
+                        // f64 1.385 vs 1.352 ms)
+                        const int d = (sizeof(R) == 8) ? ((m >> 2) & 1) : 0;
                         const int nc = n / E;
                         int c = 0;
                         for (; c + 1 < nc; c += 2) {
